@@ -1,0 +1,97 @@
+"""Model shapes, token grids and seeded parameter sets (inputs only, no method arithmetic).
+
+Shapes: BASELINE.json `configs` + SURVEY.md §8 shape table (F, L from public Wan2.1
+configs, marked [ext] there).  Token grid: SURVEY.md §8 "Token grids" — Wan2.1-VAE
+stride (4, 8, 8), patch (1, 2, 2): n = F_lat * (h/16) * (w/16), F_lat = 1 + (frames-1)/4,
+64 latent floats per token.
+"""
+from dataclasses import dataclass
+
+import numpy as np
+
+from .rng import (GLOBAL_SEED_OFFSET, TID, gain_bf16_bits, linear_weight_bits, modulation_f32,
+                  vector_bf16_bits)
+
+
+@dataclass(frozen=True)
+class ModelShape:
+    name: str
+    dim: int
+    heads: int
+    ffn: int
+    layers: int
+    lat: int = 64            # P_lat = C * pt * ph * pw = 16 * 1 * 2 * 2
+    freq_dim: int = 256      # sinusoidal time-embedding width (Wan [ext])
+    weight_seed: int = 1234
+
+    @property
+    def head_dim(self):
+        return self.dim // self.heads
+
+    def with_layers(self, layers):
+        return ModelShape(self.name, self.dim, self.heads, self.ffn, layers, self.lat,
+                          self.freq_dim, self.weight_seed)
+
+
+TINY = ModelShape("tiny", 384, 6, 1536, 1)
+WAN_1_3B = ModelShape("wan-1.3b", 1536, 12, 8960, 30)
+WAN_14B = ModelShape("wan-14b", 5120, 40, 13824, 40)
+MODELS = {m.name: m for m in (TINY, WAN_1_3B, WAN_14B)}
+
+
+def token_grid(width, height, frames=1):
+    """(F_lat, H_t, W_t) token grid of a request (SURVEY.md §8 'Token grids')."""
+    if width % 16 or height % 16 or (frames - 1) % 4:
+        raise ValueError("width/height must be multiples of 16 and frames = 1 mod 4")
+    return (1 + (frames - 1) // 4, height // 16, width // 16)
+
+
+def seq_shards(n, p):
+    """Contiguous token shard bounds of n tokens over p ranks (SURVEY.md §8(c) reading 10)."""
+    return [((i * n) // p, ((i + 1) * n) // p) for i in range(p)]
+
+
+def block_params(shape: ModelShape, layer: int):
+    """Seeded parameters of block `layer`. bf16 tensors are uint16 bit patterns."""
+    s = shape.weight_seed + layer
+    D, F = shape.dim, shape.ffn
+    return {
+        "w_qkv": linear_weight_bits(s, TID["w_qkv"], 3 * D, D),
+        "b_qkv": vector_bf16_bits(s, TID["b_qkv"], 3 * D),
+        "g_q": gain_bf16_bits(s, TID["g_q"], D),
+        "g_k": gain_bf16_bits(s, TID["g_k"], D),
+        "w_o": linear_weight_bits(s, TID["w_o"], D, D),
+        "b_o": vector_bf16_bits(s, TID["b_o"], D),
+        "w_1": linear_weight_bits(s, TID["w_1"], F, D),
+        "b_1": vector_bf16_bits(s, TID["b_1"], F),
+        "w_2": linear_weight_bits(s, TID["w_2"], D, F),
+        "b_2": vector_bf16_bits(s, TID["b_2"], D),
+        "mod": modulation_f32(s, TID["mod"], 6, D),
+    }
+
+
+def global_params(shape: ModelShape):
+    s = shape.weight_seed + GLOBAL_SEED_OFFSET
+    D, P, T = shape.dim, shape.lat, shape.freq_dim
+    return {
+        "w_pe": linear_weight_bits(s, TID["w_pe"], D, P),
+        "b_pe": vector_bf16_bits(s, TID["b_pe"], D),
+        "w_t1": linear_weight_bits(s, TID["w_t1"], D, T),
+        "b_t1": vector_bf16_bits(s, TID["b_t1"], D),
+        "w_t2": linear_weight_bits(s, TID["w_t2"], D, D),
+        "b_t2": vector_bf16_bits(s, TID["b_t2"], D),
+        "w_tp": linear_weight_bits(s, TID["w_tp"], 6 * D, D),
+        "b_tp": vector_bf16_bits(s, TID["b_tp"], 6 * D),
+        "mod_head": modulation_f32(s, TID["mod_head"], 2, D),
+        "w_head": linear_weight_bits(s, TID["w_head"], P, D),
+        "b_head": vector_bf16_bits(s, TID["b_head"], P),
+    }
+
+
+def as_f64(params):
+    """Exact upcast of a parameter dict (bf16 bits or fp32) to fp64 arrays."""
+    from .rng import bf16_bits_to_f64
+    out = {}
+    for k, v in params.items():
+        out[k] = bf16_bits_to_f64(v) if v.dtype == np.uint16 else v.astype(np.float64)
+    return out
