@@ -1,0 +1,156 @@
+/* gs.h — C-ABI of the GenServe DiT-step hot path on B200 (libgs.so).
+ *
+ * The calls follow the paper's statement of the scheduling problem (§4.4,
+ * P:408-420): a request r is allocated a GPU set X_r(t) with |X_r| in {0} u P,
+ * P = {1, 2, 4, 8} (P:92 Listing genserve-api, "elastic_sp=[1,2,4,8]"; "Images use
+ * at most one GPU ... videos use |X_v(t)| in {0} u P"), and the transition
+ * X_r(t) -> X_r(t + D_round) expresses start, continue, preempt, resume and reconfigure
+ * (P:415).  Preemption happens only at denoising-step boundaries and the latent stays in
+ * device memory (§1; §4.2 "its latent state is retained in device memory");
+ * SP degree changes between steps (§4.3, "downgrading the SP degree").
+ * One "step" is one reverse-diffusion step (P:129-133 Eq. reverse) = one DiT forward + a
+ * FlowMatch-Euler update (DESIGN.md readings).
+ *
+ * Ranks and processes.  A context owns one CUDA device and one or more *ranks* (global
+ * indices into the job's GPUs).  Production: one process per GPU (torchrun), each with one
+ * rank; SP exchanges use NCCL over NVLink (gs_init with an NCCL unique id).  Test fixture:
+ * gs_init_emulated() puts W virtual ranks in one process on one device and performs the
+ * same exchanges with device copies (all calls then act on every rank at once).
+ * All calls that move data between ranks (gs_submit, gs_run_steps, gs_resume) are
+ * collective over the ranks they name: every process owning one of those ranks must make
+ * the same call with the same arguments (SPMD).
+ *
+ * Errors.  Every call returns GS_OK (0) or a negative GS_E* code; nothing throws across the
+ * ABI.  gs_last_error() returns a context-owned message valid until the next call on that
+ * context.  Pointers: "host" arguments are borrowed for the duration of the call; "device"
+ * arguments (debug entry points only) must be device memory of the context's device, owned
+ * by the caller.  The context owns all memory it allocates (weights, latents, arenas).
+ */
+#ifndef GS_H_
+#define GS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gs_ctx gs_ctx;
+typedef uint64_t gs_req;
+
+enum {
+  GS_OK = 0,
+  GS_EINVAL = -1,        /* bad shape / argument ("UnknownConfiguration")        */
+  GS_ESTATE = -2,        /* contract violation: wrong placement, paused, overlap    */
+  GS_ENOMEM = -3,        /* device allocation failed                                        */
+  GS_ECUDA = -4,         /* CUDA runtime / kernel error                                     */
+  GS_ENCCL = -5,         /* NCCL error                                                      */
+  GS_EUNSUPPORTED = -6   /* configuration not supported by this build                       */
+};
+
+enum { GS_REQ_PLACED = 0, GS_REQ_RUNNING = 1, GS_REQ_PAUSED = 2, GS_REQ_DONE = 3 };
+
+/* DiT model shape (SURVEY.md §8 shape table; Wan2.1-style block, reading 1).
+ * Weights are generated on the device from the counter RNG:
+ * block l uses seed weight_seed + l, global tensors weight_seed + 1000000. */
+typedef struct {
+  int dim;        /* D, multiple of 64, <= 8192                        */
+  int heads;      /* H, head dim D/H in {64, 128}                      */
+  int ffn;        /* F, multiple of 256                                */
+  int layers;     /* L                                                 */
+  int lat;        /* latent floats per token (64)                      */
+  int freq_dim;   /* sinusoidal time-embedding width (256)            */
+  float rope_theta; /* 10000                                           */
+  float eps;      /* LayerNorm / RMSNorm epsilon (1e-6)                */
+  float flow_shift; /* FlowMatch shift s (5.0)                         */
+  uint64_t weight_seed;
+} gs_model_desc;
+
+/* ------------------------------------------------------------------ context */
+/* Writes NCCL's 128-byte unique id to out (host, >= 128 bytes). Call on one process and
+ * broadcast the bytes (e.g. with torch.distributed) before gs_init. */
+int gs_nccl_unique_id(void* out128);
+/* One process per GPU: `device` is the local CUDA ordinal, `rank` in [0, world_size).
+ * world_size == 1 needs no unique id (nccl_uid may be NULL). */
+int gs_init(int device, int world_size, int rank, const void* nccl_uid, gs_ctx** out);
+/* Test fixture: world_size virtual ranks on one device in this process (exchanges are
+ * device-to-device copies; same kernels and shard shapes as the NCCL path). */
+int gs_init_emulated(int device, int world_size, gs_ctx** out);
+void gs_destroy(gs_ctx* ctx);
+const char* gs_last_error(gs_ctx* ctx);
+/* Number of SMs of the context's device, world size, ranks owned by this process. */
+int gs_info(gs_ctx* ctx, int* num_sms, int* world_size, int* nlocal);
+
+/* ------------------------------------------------------------------ models */
+int gs_model_create(gs_ctx* ctx, const gs_model_desc* desc, int* model_id);
+/* Copy one weight tensor to host (parity rung T1). layer = -1 for global tensors.
+ * name in {w_qkv,b_qkv,g_q,g_k,w_o,b_o,w_1,b_1,w_2,b_2,mod} (block) or
+ * {w_pe,b_pe,w_t1,b_t1,w_t2,b_t2,w_tp,b_tp,mod_head,w_head,b_head} (global).
+ * bytes must equal the tensor size (bf16 tensors: 2 B/elem, mod tables fp32). */
+int gs_get_weight(gs_ctx* ctx, int model, int layer, const char* name, void* host, size_t bytes);
+
+/* ------------------------------------------------------------------ requests */
+/* Submit a request: resolution w x h (multiples of 16), frames (1 for images, = 1 mod 4),
+ * `steps` denoising steps (sigma schedule of DESIGN.md reading 5).  The initial latent
+ * z_T [n, lat] fp32 (token-major, n = (1 + (frames-1)/4) * (h/16) * (w/16)) is generated
+ * from noise_seed, or copied from init_latent (host, n*lat floats) if non-NULL.  The request
+ * is placed token-sharded on `ranks` (p = nranks in {1,2,4,8}, distinct, in SP order). */
+int gs_submit(gs_ctx* ctx, int model, int width, int height, int frames, int steps,
+              uint64_t noise_seed, const float* init_latent, const int* ranks, int nranks,
+              gs_req* out);
+/* Run k steps of a batch of requests (all placed on exactly `ranks`, same model, not paused,
+ * k <= remaining steps of each).  Returns after the last step completed or after the step
+ * boundary at which a preemption was requested (steps actually run -> *steps_run).
+ * Bit-exact w.r.t. SP degree, batch composition and preempt/resume. */
+int gs_run_steps(gs_ctx* ctx, const gs_req* reqs, int nreq, const int* ranks, int nranks, int k,
+                 int* steps_run);
+/* Request preemption; effective at the next step boundary (or immediately if idle).  Safe to
+ * call from another thread while gs_run_steps is running. steps_done_out may be NULL. */
+int gs_preempt(gs_ctx* ctx, gs_req req, int* steps_done_out);
+/* Resume / reconfigure at a step boundary onto `ranks` (p' = nranks): re-shards the latent
+ * (pure copy of contiguous token ranges, interval intersections of old and new shards). */
+int gs_resume(gs_ctx* ctx, gs_req req, const int* ranks, int nranks);
+/* state in GS_REQ_*; ranks_out (host, >= 8 ints) may be NULL. */
+int gs_query(gs_ctx* ctx, gs_req req, int* steps_done, int* steps_total, int* nranks,
+             int* ranks_out, int* state, int* n_tokens);
+/* Copy the latent [n, lat] fp32 to host: every shard owned by this process is written to
+ * its token range (in emulated mode: the whole latent). */
+int gs_read_latent(gs_ctx* ctx, gs_req req, float* host, size_t nfloats);
+int gs_release(gs_ctx* ctx, gs_req req);
+
+/* ------------------------------------------------------------------ measurement */
+/* Enable per-kernel-class CUDA-event timing inside gs_run_steps (events on the launching
+ * stream); gs_stats writes a JSON object {"class": {"ms": total, "n": launches}, ...,
+ * "launches": total kernel launches} accumulated since the last reset. */
+int gs_profile(gs_ctx* ctx, int enable, int reset);
+int gs_stats(gs_ctx* ctx, char* json, size_t len);
+/* The CUDA stream (cudaStream_t) the context launches rank `rank`'s work on, as a pointer. */
+int gs_stream(gs_ctx* ctx, int rank, void** stream_out);
+
+/* ------------------------------------------------------------------ parity / debug entry points
+ * Single device, rank-independent, caller-owned buffers. */
+/* GEMM C = A W^T with epilogue epi (0 bf16, 1 GELU-bf16, 2 fp32, 3 gated-residual fp32,
+ * 4 Euler fp32; see csrc/kernels.h).  A [M,K] bf16, W [N,K] bf16, bias [N] bf16 (or NULL),
+ * out [M,N] (bf16 or fp32), gate_a [N] fp32, gate_b [B,gate_b_stride] fp32, row_req [M] int32,
+ * dsig (host, 8 floats) — all device pointers except dsig.  K % 64 == 0, N % 32 == 0. */
+int gs_debug_gemm(gs_ctx* ctx, int epi, int M, int N, int K, const void* A, const void* W,
+                  const void* bias, void* out, const float* gate_a, const float* gate_b,
+                  int gate_b_stride, const int* row_req, const float* dsig_host);
+/* Attention over packed requests: Q/K/V/O bf16 [rows, heads, d] with row strides (elements);
+ * seq_off/seq_len host int arrays of nreq entries (rows of each request). d in {64, 128}. */
+int gs_debug_attention(gs_ctx* ctx, const void* q, const void* k, const void* v, void* o, int heads,
+                       int d, int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
+                       int nreq);
+/* One DiT block (model, layer) at p = 1 on host data: x [N, D] fp32 in/out (rows of the nreq
+ * requests concatenated), grids [nreq*3] (F_t, H_t, W_t), tok_lo [nreq] first request-local
+ * token of each row segment, n_rows [nreq], t [nreq] timesteps (e = time-embedding(t)). */
+int gs_debug_block(gs_ctx* ctx, int model, int layer, float* x, int nreq, const int* grids,
+                   const int* tok_lo, const int* n_rows, const float* t);
+/* Time embedding of nreq timesteps: e0 [nreq, D], e [nreq, 6D] fp32 (host outputs). */
+int gs_debug_time_embed(gs_ctx* ctx, int model, int nreq, const float* t, float* e0, float* e);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GS_H_ */

@@ -1,1 +1,250 @@
-"""GenServe DiT-step hot path on B200 (sm_100a): thin Python binding over libgs.so."""
+"""GenServe DiT-step hot path on B200 (sm_100a): thin ctypes binding over libgs.so.
+
+Argument marshalling only — every step of the path runs in the CUDA kernels of
+`csrc/` behind the C-ABI declared in `include/gs.h`.  There is no CPU fallback: if
+libgs.so is missing or fails to load, `load()` raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgs.so")
+
+GS_OK, GS_EINVAL, GS_ESTATE, GS_ENOMEM, GS_ECUDA, GS_ENCCL, GS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
+REQ_PLACED, REQ_RUNNING, REQ_PAUSED, REQ_DONE = 0, 1, 2, 3
+EPI_BF16, EPI_GELU_BF16, EPI_F32, EPI_RESID_F32, EPI_EULER_F32 = 0, 1, 2, 3, 4
+
+
+class GsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"gs error {code}: {msg}")
+        self.code = code
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("heads", ctypes.c_int), ("ffn", ctypes.c_int),
+                ("layers", ctypes.c_int), ("lat", ctypes.c_int), ("freq_dim", ctypes.c_int),
+                ("rope_theta", ctypes.c_float), ("eps", ctypes.c_float),
+                ("flow_shift", ctypes.c_float), ("weight_seed", ctypes.c_uint64)]
+
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_IP = ctypes.POINTER(ctypes.c_int)
+_FP = ctypes.POINTER(ctypes.c_float)
+_U64 = ctypes.c_uint64
+_SIG = {
+    "gs_nccl_unique_id": [_P],
+    "gs_init": [_I, _I, _I, _P, ctypes.POINTER(_P)],
+    "gs_init_emulated": [_I, _I, ctypes.POINTER(_P)],
+    "gs_destroy": [_P],
+    "gs_last_error": [_P],
+    "gs_info": [_P, _IP, _IP, _IP],
+    "gs_model_create": [_P, ctypes.POINTER(ModelDesc), _IP],
+    "gs_get_weight": [_P, _I, _I, ctypes.c_char_p, _P, ctypes.c_size_t],
+    "gs_submit": [_P, _I, _I, _I, _I, _I, _U64, _FP, _IP, _I, ctypes.POINTER(_U64)],
+    "gs_run_steps": [_P, ctypes.POINTER(_U64), _I, _IP, _I, _I, _IP],
+    "gs_preempt": [_P, _U64, _IP],
+    "gs_resume": [_P, _U64, _IP, _I],
+    "gs_query": [_P, _U64, _IP, _IP, _IP, _IP, _IP, _IP],
+    "gs_read_latent": [_P, _U64, _FP, ctypes.c_size_t],
+    "gs_release": [_P, _U64],
+    "gs_profile": [_P, _I, _I],
+    "gs_stats": [_P, ctypes.c_char_p, ctypes.c_size_t],
+    "gs_stream": [_P, _I, ctypes.POINTER(_P)],
+    "gs_debug_gemm": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _FP],
+    "gs_debug_attention": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _IP, _IP, _I],
+    "gs_debug_block": [_P, _I, _I, _FP, _I, _IP, _IP, _IP, _FP],
+    "gs_debug_time_embed": [_P, _I, _I, _FP, _FP, _FP],
+}
+_lib = None
+
+
+def load(path=LIB_PATH):
+    """Load libgs.so (raises if absent — the product path has no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, args in _SIG.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_char_p if name == "gs_last_error" else (None if name == "gs_destroy" else ctypes.c_int)
+    _lib = lib
+    return lib
+
+
+def _ints(xs):
+    arr = (ctypes.c_int * max(len(xs), 1))(*xs)
+    return arr
+
+
+def _fl(xs):
+    return (ctypes.c_float * max(len(xs), 1))(*xs)
+
+
+def _ptr(x):
+    """Device pointer of a torch tensor (or int / None)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    rc = load().gs_nccl_unique_id(buf)
+    if rc != GS_OK:
+        raise GsError(rc, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+class Context:
+    """One process-side context: a CUDA device and its ranks (see include/gs.h)."""
+
+    def __init__(self, device=0, world_size=1, rank=0, nccl_uid=None, emulated=False):
+        lib = load()
+        self._lib = lib
+        h = ctypes.c_void_p()
+        if emulated:
+            rc = lib.gs_init_emulated(device, world_size, ctypes.byref(h))
+        else:
+            rc = lib.gs_init(device, world_size, rank, nccl_uid, ctypes.byref(h))
+        self._h = h
+        if rc != GS_OK:
+            msg = lib.gs_last_error(h).decode() if h.value else "init failed"
+            raise GsError(rc, msg)
+        self.world_size = world_size
+        self.rank = rank
+        self.emulated = emulated
+
+    def _ck(self, rc):
+        if rc != GS_OK:
+            raise GsError(rc, self._lib.gs_last_error(self._h).decode())
+        return rc
+
+    def close(self):
+        if self._h and self._h.value:
+            self._lib.gs_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self):
+        a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        self._ck(self._lib.gs_info(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return {"num_sms": a.value, "world_size": b.value, "nlocal": c.value}
+
+    # ---------------------------------------------------------------- models
+    def model_create(self, dim, heads, ffn, layers, weight_seed=1234, lat=64, freq_dim=256,
+                     rope_theta=10000.0, eps=1e-6, flow_shift=5.0):
+        d = ModelDesc(dim, heads, ffn, layers, lat, freq_dim, rope_theta, eps, flow_shift, weight_seed)
+        mid = ctypes.c_int()
+        self._ck(self._lib.gs_model_create(self._h, ctypes.byref(d), ctypes.byref(mid)))
+        return mid.value
+
+    def get_weight(self, model, layer, name, shape, dtype):
+        out = np.empty(shape, dtype=dtype)
+        self._ck(self._lib.gs_get_weight(self._h, model, layer, name.encode(),
+                                         out.ctypes.data_as(ctypes.c_void_p), out.nbytes))
+        return out
+
+    # ---------------------------------------------------------------- requests
+    def submit(self, model, width, height, frames, steps, noise_seed, ranks, init_latent=None):
+        rid = ctypes.c_uint64()
+        lat = None
+        if init_latent is not None:
+            init_latent = np.ascontiguousarray(init_latent, dtype=np.float32)
+            lat = init_latent.ctypes.data_as(_FP)
+        self._ck(self._lib.gs_submit(self._h, model, width, height, frames, steps, noise_seed, lat,
+                                     _ints(ranks), len(ranks), ctypes.byref(rid)))
+        return rid.value
+
+    def run_steps(self, reqs, ranks, k):
+        ids = (ctypes.c_uint64 * len(reqs))(*reqs)
+        done = ctypes.c_int()
+        self._ck(self._lib.gs_run_steps(self._h, ids, len(reqs), _ints(ranks), len(ranks), k,
+                                        ctypes.byref(done)))
+        return done.value
+
+    def preempt(self, req):
+        s = ctypes.c_int()
+        self._ck(self._lib.gs_preempt(self._h, req, ctypes.byref(s)))
+        return s.value
+
+    def resume(self, req, ranks):
+        self._ck(self._lib.gs_resume(self._h, req, _ints(ranks), len(ranks)))
+
+    def query(self, req):
+        v = [ctypes.c_int() for _ in range(5)]
+        ranks = (ctypes.c_int * 8)()
+        self._ck(self._lib.gs_query(self._h, req, ctypes.byref(v[0]), ctypes.byref(v[1]),
+                                    ctypes.byref(v[2]), ranks, ctypes.byref(v[3]),
+                                    ctypes.byref(v[4])))
+        return {"steps_done": v[0].value, "steps_total": v[1].value,
+                "ranks": list(ranks[:v[2].value]), "state": v[3].value, "n_tokens": v[4].value}
+
+    def read_latent(self, req, n_tokens=None, lat=64):
+        if n_tokens is None:
+            n_tokens = self.query(req)["n_tokens"]
+        out = np.zeros((n_tokens, lat), dtype=np.float32)
+        self._ck(self._lib.gs_read_latent(self._h, req, out.ctypes.data_as(_FP), out.size))
+        return out
+
+    def release(self, req):
+        self._ck(self._lib.gs_release(self._h, req))
+
+    # ---------------------------------------------------------------- measurement
+    def profile(self, enable=True, reset=True):
+        self._ck(self._lib.gs_profile(self._h, int(enable), int(reset)))
+
+    def stats(self):
+        import json
+        buf = ctypes.create_string_buffer(1 << 16)
+        self._ck(self._lib.gs_stats(self._h, buf, len(buf)))
+        return json.loads(buf.value.decode())
+
+    def stream_ptr(self, rank=None):
+        s = ctypes.c_void_p()
+        self._ck(self._lib.gs_stream(self._h, self.rank if rank is None else rank, ctypes.byref(s)))
+        return s.value
+
+    # ---------------------------------------------------------------- debug entry points
+    def debug_gemm(self, epi, M, N, K, A, W, bias, out, gate_a=None, gate_b=None, gate_b_stride=0,
+                   row_req=None, dsig=None):
+        ds = _fl(list(dsig) + [0.0] * (8 - len(dsig))) if dsig is not None else None
+        self._ck(self._lib.gs_debug_gemm(self._h, epi, M, N, K, _ptr(A), _ptr(W), _ptr(bias),
+                                         _ptr(out), _ptr(gate_a), _ptr(gate_b), gate_b_stride,
+                                         _ptr(row_req), ds))
+
+    def debug_attention(self, q, k, v, o, heads, d, seq_off, seq_len, q_rs=None, kv_rs=None,
+                        o_rs=None):
+        q_rs = heads * d if q_rs is None else q_rs
+        kv_rs = heads * d if kv_rs is None else kv_rs
+        o_rs = heads * d if o_rs is None else o_rs
+        self._ck(self._lib.gs_debug_attention(self._h, _ptr(q), _ptr(k), _ptr(v), _ptr(o), heads,
+                                              d, q_rs, kv_rs, o_rs, _ints(seq_off),
+                                              _ints(seq_len), len(seq_len)))
+
+    def debug_block(self, model, layer, x, grids, tok_lo, n_rows, t):
+        x = np.ascontiguousarray(x, dtype=np.float32).copy()
+        flat = [g for grid in grids for g in grid]
+        self._ck(self._lib.gs_debug_block(self._h, model, layer, x.ctypes.data_as(_FP), len(n_rows),
+                                          _ints(flat), _ints(tok_lo), _ints(n_rows), _fl(t)))
+        return x
+
+    def debug_time_embed(self, model, t, dim):
+        e0 = np.zeros((len(t), dim), np.float32)
+        e = np.zeros((len(t), 6 * dim), np.float32)
+        self._ck(self._lib.gs_debug_time_embed(self._h, model, len(t), _fl(t),
+                                               e0.ctypes.data_as(_FP), e.ctypes.data_as(_FP)))
+        return e0, e

@@ -1,0 +1,304 @@
+// tcgen05 flash attention, non-causal, varlen block-diagonal:
+//   O_h = softmax(Q_h K_h^T / sqrt(d)) V_h per request (oracle: oracle/dit.py attention()).
+//
+// Design (B200-first; FlashAttention-4-style structure, written from scratch):
+//   * one CTA = one head x two 128-row Q tiles of one request (256 query rows);
+//   * warp 0: TMA producer (Q once; K_j, V_j into a 2-stage ring, 128B swizzle);
+//   * warp 1: TMEM owner + single-thread tcgen05.mma issuer;
+//   * warps 4..7 / 8..11: softmax warpgroups WG0 / WG1, one thread per query row;
+//   * TMEM (512 cols): S_w = Q_w K_j^T at cols [128w, 128w+128) (fp32), P_w (bf16 pairs)
+//     written over S_w cols [128w, 128w+64), O_w at cols [256+128w, 256+128w+d);
+//   * MMA issue order S0_0, S1_0, {PV0_j, S0_{j+1}, PV1_j, S1_{j+1}}: WG0's softmax of tile j+1
+//     overlaps PV1_j / S1_{j+1} on the tensor core and vice versa (ping-pong);
+//   * online softmax in fp32 (exp2 domain) with lazy rescale: O is rescaled only when the
+//     running max grows by more than 2^8 (values stay <= 256 otherwise, exact in fp32).
+// Bit-exactness (SURVEY.md §8(a) invariant 3): Q and KV tiles start at each request's first
+// token, the KV loop always covers the request in the same order, tiles never mix requests
+// (out-of-request columns are masked to p = 0).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "kernels.h"
+#include "ptx.cuh"
+#include "tma.h"
+
+namespace gs {
+namespace {
+
+constexpr int MAX_REQ = 64;
+constexpr int THREADS = 384;
+
+struct SeqTable {
+  int nreq;
+  int off[MAX_REQ];
+  int len[MAX_REQ];
+  int tile_start[MAX_REQ + 1];  // prefix sum of ceil(len / 256)
+};
+
+template <int HD>
+struct Cfg {
+  static constexpr int BOXES = HD / 64;                  // 64-element (128 B) column boxes
+  static constexpr int TILE_BYTES = 128 * HD * 2;        // one 128-row tile
+  static constexpr int ST = HD == 128 ? 2 : 4;           // KV stages
+  static constexpr int Q_OFF = 0;
+  static constexpr int KV_OFF = 2 * TILE_BYTES;
+  static constexpr int STAGE_BYTES = 2 * TILE_BYTES;     // K + V
+  static constexpr int BAR_OFF = KV_OFF + ST * STAGE_BYTES;
+  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
+                   const __grid_constant__ SeqTable tab, float scale_log2) {
+  using C = Cfg<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* kfull = bars + 1;
+  uint64_t* vfull = kfull + C::ST;
+  uint64_t* kvempty = vfull + C::ST;
+  uint64_t* sfull = kvempty + C::ST;  // [2]
+  uint64_t* pfull = sfull + 2;        // [2]
+  uint64_t* ofull = pfull + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+
+  // locate (request, pair-of-tiles) of this CTA
+  int r = 0;
+  while (r + 1 < tab.nreq && static_cast<int>(blockIdx.x) >= tab.tile_start[r + 1]) ++r;
+  const int pair = blockIdx.x - tab.tile_start[r];
+  const int kv_off = tab.off[r], kv_len = tab.len[r];
+  const int q_row0 = kv_off + pair * 256;
+  const int q_rows = min(256, kv_len - pair * 256);
+  const int nkv = (kv_len + 127) / 128;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < C::ST; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&vfull[s], 1);
+      mbar_init(&kvempty[s], 1);
+    }
+    for (int w = 0; w < 2; ++w) {
+      mbar_init(&sfull[w], 1);
+      mbar_init(&pfull[w], 4);
+      mbar_init(&ofull[w], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
+      for (int w = 0; w < 2; ++w)
+        for (int b = 0; b < C::BOXES; ++b)
+          tma_load_3d(&tmQ, q_full, smem + C::Q_OFF + w * C::TILE_BYTES + b * 16384, b * 64, head,
+                      q_row0 + w * 128);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % C::ST;
+        const uint32_t ph = (j / C::ST) & 1;
+        mbar_wait(&kvempty[s], ph ^ 1);
+        uint8_t* sk = smem + C::KV_OFF + s * C::STAGE_BYTES;
+        uint8_t* sv = sk + C::TILE_BYTES;
+        mbar_arrive_expect_tx(&kfull[s], C::TILE_BYTES);
+        for (int b = 0; b < C::BOXES; ++b)
+          tma_load_3d(&tmK, &kfull[s], sk + b * 16384, b * 64, head, kv_off + j * 128);
+        mbar_arrive_expect_tx(&vfull[s], C::TILE_BYTES);
+        for (int b = 0; b < C::BOXES; ++b)
+          tma_load_3d(&tmV, &vfull[s], sv + b * 16384, b * 64, head, kv_off + j * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
+      const uint32_t sq = smem_u32(smem + C::Q_OFF);
+      const uint32_t skv = smem_u32(smem + C::KV_OFF);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int w, int j) {
+        const int s = j % C::ST;
+        mbar_wait(&kfull[s], (j / C::ST) & 1);
+        tc_fence_after();
+        const uint32_t qa = sq + w * C::TILE_BYTES;
+        const uint32_t kb = skv + s * C::STAGE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          mma_ss(tmem + w * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
+                 idesc_s, kk > 0);
+        }
+        mma_commit(&sfull[w]);
+      };
+      auto issue_pv = [&](int w, int j) {
+        const int s = j % C::ST;
+        mbar_wait(&pfull[w], j & 1);
+        mbar_wait(&vfull[s], (j / C::ST) & 1);
+        tc_fence_after();
+        const uint32_t vb = skv + s * C::STAGE_BYTES + C::TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          mma_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
+                 idesc_o, (j > 0) || (kk > 0));
+        }
+      };
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        issue_pv(0, j);
+        if (j + 1 < nkv) issue_s(0, j + 1);
+        issue_pv(1, j);
+        mma_commit(&kvempty[j % C::ST]);
+        if (j + 1 < nkv) issue_s(1, j + 1);
+      }
+      mma_commit(&ofull[0]);
+      mma_commit(&ofull[1]);
+    }
+  } else if (warp >= 4) {
+    const int w = (warp - 4) >> 2;  // softmax warpgroup
+    const int quarter = warp & 3;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tS = tmem + lane_base + w * 128;
+    const uint32_t tO = tmem + lane_base + 256 + w * 128;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&sfull[w], j & 1);
+      tc_fence_after();
+      const int kv_valid = min(128, kv_len - j * 128);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        GS_TMEM_LD32(tS + c * 32, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < kv_valid) mx = fmaxf(mx, __uint_as_float(v[i]));
+      }
+      const float m_tile = mx * scale_log2;
+      const bool need = m_tile > m_run + 8.0f;
+      const float alpha = need ? ex2_approx(m_run - m_tile) : 1.0f;
+      if (need) m_run = m_tile;
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t v[32];
+          GS_TMEM_LD32(tO + c * 32, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+          GS_TMEM_ST32(tO + c * 32, v);
+        }
+      }
+      l_run *= alpha;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        GS_TMEM_LD32(tS + c * 32, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int col = c * 32 + 2 * i;
+          const float p0 = col < kv_valid ? ex2_approx(fmaf(__uint_as_float(v[2 * i]), scale_log2, -m_run)) : 0.f;
+          const float p1 = col + 1 < kv_valid ? ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), scale_log2, -m_run)) : 0.f;
+          sum += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        GS_TMEM_ST16(tS + c * 16, pk);
+      }
+      l_run += sum;
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[w]);
+    }
+    // epilogue: O / l -> bf16 -> global
+    mbar_wait(&ofull[w], 0);
+    tc_fence_after();
+    const int row_in = w * 128 + quarter * 32 + lane;
+    const float inv = 1.0f / l_run;
+    __nv_bfloat16* orow = O + static_cast<long long>(q_row0 + row_in) * o_rs + head * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t v[32];
+      GS_TMEM_LD32(tO + c * 32, v);
+      tmem_ld_wait();
+      if (row_in < q_rows) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int HD>
+cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
+                   int kv_rs, int o_rs, const SeqTable& tab, int total_rows, cudaStream_t stream) {
+  using C = Cfg<HD>;
+  CUtensorMap tq, tk, tv;
+  if (!make_tma_3d_bf16(&tq, Q, HD, heads, total_rows, HD * 2ull, q_rs * 2ull, 64, 1, 128) ||
+      !make_tma_3d_bf16(&tk, K, HD, heads, total_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128) ||
+      !make_tma_3d_bf16(&tv, V, HD, heads, total_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
+    return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
+  dim3 grid(tab.tile_start[tab.nreq], heads);
+  attn_tc_kernel<HD><<<grid, THREADS, C::SMEM, stream>>>(tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs,
+                                                          tab, scale_log2);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
+                         int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
+                         int nreq, int num_sms, cudaStream_t stream) {
+  (void)num_sms;
+  if (nreq < 1 || nreq > MAX_REQ || (d != 64 && d != 128) || heads < 1) return cudaErrorInvalidValue;
+  SeqTable tab{};
+  tab.nreq = nreq;
+  int total_rows = 0;
+  tab.tile_start[0] = 0;
+  for (int r = 0; r < nreq; ++r) {
+    if (seq_len[r] < 1) return cudaErrorInvalidValue;
+    tab.off[r] = seq_off[r];
+    tab.len[r] = seq_len[r];
+    tab.tile_start[r + 1] = tab.tile_start[r] + (seq_len[r] + 255) / 256;
+    total_rows = std::max(total_rows, seq_off[r] + seq_len[r]);
+  }
+  return d == 128 ? launch<128>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream)
+                  : launch<64>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
+}
+
+}  // namespace gs

@@ -1,0 +1,285 @@
+// Element-wise / row-wise kernels of the DiT step (HBM-bound; SURVEY.md §8(a) rows a2, a4, a6,
+// a11, a14): LayerNorm + adaLN modulate, qk-RMSNorm + 3-axis RoPE + Ulysses send-layout pack,
+// the time-embedding MLP (tiny GEMVs), fp32 -> bf16 conversion.
+//
+// Every row reduction uses a fixed order that depends only on D (thread-strided partial sums,
+// xor-shuffle tree, then warp partials summed in warp order), so a row's result does not
+// depend on where the row sits in the batch (SURVEY.md §8(a) invariant 2).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace gs {
+namespace {
+
+constexpr int ROW_THREADS = 128;
+constexpr int MAXV = 16;  // float4 / uint4 per thread per row -> D <= 8192
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over the 128 threads of the CTA in a fixed order; result broadcast to all threads.
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  return (red[0] + red[1]) + (red[2] + red[3]);
+}
+
+// ------------------------------------------------------------------ LN + modulate
+__global__ void __launch_bounds__(ROW_THREADS)
+    ln_modulate_kernel(const float* __restrict__ x, int D, const float* __restrict__ sh_a,
+                       const float* __restrict__ sh_b, const float* __restrict__ sc_a,
+                       const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
+                       float eps, __nv_bfloat16* __restrict__ out) {
+  __shared__ float red[4];
+  const long long row = blockIdx.x;
+  const int nv = D >> 2;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * D);
+  float4 v[MAXV];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int c = threadIdx.x + i * ROW_THREADS;
+    if (c < nv) {
+      v[i] = xr[c];
+      s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+    }
+  }
+  const float mean = block_sum(s, red) / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int c = threadIdx.x + i * ROW_THREADS;
+    if (c < nv) {
+      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
+      q += (a * a + b * b) + (cc * cc + d * d);
+    }
+  }
+  const float rstd = rsqrtf(block_sum(q, red) / D + eps);
+  const int r = row_req[row];
+  const float4* sha = reinterpret_cast<const float4*>(sh_a);
+  const float4* sca = reinterpret_cast<const float4*>(sc_a);
+  const float4* shb = reinterpret_cast<const float4*>(sh_b + (long long)r * b_stride);
+  const float4* scb = reinterpret_cast<const float4*>(sc_b + (long long)r * b_stride);
+  uint2* o = reinterpret_cast<uint2*>(out + row * D);
+#pragma unroll
+  for (int i = 0; i < MAXV; ++i) {
+    const int c = threadIdx.x + i * ROW_THREADS;
+    if (c < nv) {
+      const float4 a1 = __ldg(sha + c), b1 = __ldg(shb + c), a2 = __ldg(sca + c), b2 = __ldg(scb + c);
+      const float y0 = (v[i].x - mean) * rstd * (1.f + (a2.x + b2.x)) + (a1.x + b1.x);
+      const float y1 = (v[i].y - mean) * rstd * (1.f + (a2.y + b2.y)) + (a1.y + b1.y);
+      const float y2 = (v[i].z - mean) * rstd * (1.f + (a2.z + b2.z)) + (a1.z + b1.z);
+      const float y3 = (v[i].w - mean) * rstd * (1.f + (a2.w + b2.w)) + (a1.w + b1.w);
+      __nv_bfloat162 p0 = __floats2bfloat162_rn(y0, y1), p1 = __floats2bfloat162_rn(y2, y3);
+      o[c] = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ qk-RMSNorm + RoPE + pack
+__device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__global__ void __launch_bounds__(ROW_THREADS)
+    qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int D, int d,
+                             const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
+                             float eps, const RopeParams rp, const PackParams pk,
+                             __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
+                             __nv_bfloat16* __restrict__ v_out) {
+  __shared__ float red[4];
+  const long long row = blockIdx.x;
+  const int nv = D >> 3;  // uint4 chunks (8 elements) per q/k/v row
+  const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
+  uint4 qv[MAXV / 2], kv[MAXV / 2];
+  float sq = 0.f, sk = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV / 2; ++i) {
+    const int c = threadIdx.x + i * ROW_THREADS;
+    if (c < nv) {
+      qv[i] = src[c];
+      kv[i] = src[nv + c];
+      float f[8];
+      unpack8(qv[i], f);
+      sq += ((f[0] * f[0] + f[1] * f[1]) + (f[2] * f[2] + f[3] * f[3])) +
+            ((f[4] * f[4] + f[5] * f[5]) + (f[6] * f[6] + f[7] * f[7]));
+      unpack8(kv[i], f);
+      sk += ((f[0] * f[0] + f[1] * f[1]) + (f[2] * f[2] + f[3] * f[3])) +
+            ((f[4] * f[4] + f[5] * f[5]) + (f[6] * f[6] + f[7] * f[7]));
+    }
+  }
+  const float rq = rsqrtf(block_sum(sq, red) / D + eps);
+  const float rk = rsqrtf(block_sum(sk, red) / D + eps);
+
+  const int r = rp.row_req[row];
+  const int tok = rp.row_tok[row];
+  const int Ht = rp.req_grid[3 * r + 1], Wt = rp.req_grid[3 * r + 2];
+  const int pf = tok / (Ht * Wt), ph = (tok / Wt) % Ht, pw = tok % Wt;
+  const int half = d >> 1;
+  const uint4* gq = reinterpret_cast<const uint4*>(g_q);
+  const uint4* gk = reinterpret_cast<const uint4*>(g_k);
+#pragma unroll
+  for (int i = 0; i < MAXV / 2; ++i) {
+    const int c = threadIdx.x + i * ROW_THREADS;
+    if (c < nv) {
+      const int e0 = c * 8;
+      const int h = e0 / d, i0 = e0 - h * d;
+      int h0 = pk.head_off[0], h1 = pk.head_off[1];
+      long long doff = pk.dest_off[0];
+#pragma unroll
+      for (int t = 1; t < 8; ++t) {
+        if (t < pk.ndest && h >= pk.head_off[t]) {
+          h0 = pk.head_off[t];
+          h1 = pk.head_off[t + 1];
+          doff = pk.dest_off[t];
+        }
+      }
+      const long long o = doff + (row * (h1 - h0) + (h - h0)) * (long long)d + i0;
+      float fq[8], fk[8], wq[8], wk[8];
+      unpack8(qv[i], fq);
+      unpack8(kv[i], fk);
+      unpack8(__ldg(gq + c), wq);
+      unpack8(__ldg(gk + c), wk);
+      uint32_t oq[4], ok[4];
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        const int slot = (i0 >> 1) + p;
+        const int ax = __ldg(rp.slot_axis + slot);
+        const int pa = ax == 0 ? pf : (ax == 1 ? ph : pw);
+        const float2 cs = __ldg(rp.cs_tab + (long long)pa * half + slot);
+        const float q0 = fq[2 * p] * rq * wq[2 * p], q1 = fq[2 * p + 1] * rq * wq[2 * p + 1];
+        const float k0 = fk[2 * p] * rk * wk[2 * p], k1 = fk[2 * p + 1] * rk * wk[2 * p + 1];
+        oq[p] = pack_bf16x2(q0 * cs.x - q1 * cs.y, q0 * cs.y + q1 * cs.x);
+        ok[p] = pack_bf16x2(k0 * cs.x - k1 * cs.y, k0 * cs.y + k1 * cs.x);
+      }
+      *reinterpret_cast<uint4*>(q_out + o) = make_uint4(oq[0], oq[1], oq[2], oq[3]);
+      *reinterpret_cast<uint4*>(k_out + o) = make_uint4(ok[0], ok[1], ok[2], ok[3]);
+      *reinterpret_cast<uint4*>(v_out + o) = src[2 * nv + c];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ time embedding
+struct TVals {
+  float t[8];
+};
+
+__global__ void sinusoid_kernel(TVals tv, int B, int freq_dim, float* out) {
+  const int half = freq_dim / 2;
+  for (int i = threadIdx.x; i < B * half; i += blockDim.x) {
+    const int b = i / half, j = i - b * half;
+    const double w = exp(-log(10000.0) * (double)j / (double)half);
+    const double a = (double)tv.t[b] * w;
+    out[b * freq_dim + j] = (float)cos(a);
+    out[b * freq_dim + half + j] = (float)sin(a);
+  }
+}
+
+// y[b, n] = sum_k W[n, k] in[b, k] + bias[n]; one warp per output n, B <= 8.
+__global__ void gemv_kernel(const float* __restrict__ in, const __nv_bfloat16* __restrict__ W,
+                            const __nv_bfloat16* __restrict__ bias, int N, int K, int B,
+                            float* __restrict__ out, float* __restrict__ out_silu) {
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= N) return;
+  float acc[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) acc[b] = 0.f;
+  const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(W + (long long)n * K);
+  for (int k2 = lane; k2 < K / 2; k2 += 32) {
+    const float2 w = __bfloat1622float2(w2[k2]);
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (b < B) acc[b] += w.x * in[b * K + 2 * k2] + w.y * in[b * K + 2 * k2 + 1];
+  }
+  const float bn = __bfloat162float(bias[n]);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    if (b < B) {
+      const float y = warp_sum(acc[b]) + bn;
+      if (lane == 0) {
+        if (out) out[b * N + n] = y;
+        if (out_silu) out_silu[b * N + n] = y / (1.f + __expf(-y));
+      }
+    }
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                   long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(in)[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    reinterpret_cast<uint2*>(out)[i] =
+        make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+  }
+}
+
+}  // namespace
+
+cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const float* sh_b,
+                        const float* sc_a, const float* sc_b, int b_stride, const int* row_req,
+                        float eps, __nv_bfloat16* out, cudaStream_t stream) {
+  if (M == 0) return cudaSuccess;
+  if (D % 4 || D > 4 * MAXV * ROW_THREADS) return cudaErrorInvalidValue;
+  ln_modulate_kernel<<<M, ROW_THREADS, 0, stream>>>(x, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req,
+                                                     eps, out);
+  return cudaGetLastError();
+}
+
+cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
+                              const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,
+                              const RopeParams& rp, const PackParams& pk, __nv_bfloat16* q_out,
+                              __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream) {
+  if (M == 0) return cudaSuccess;
+  const int d = D / heads;
+  if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > 8)
+    return cudaErrorInvalidValue;
+  qk_norm_rope_pack_kernel<<<M, ROW_THREADS, 0, stream>>>(qkv, D, d, g_q, g_k, eps, rp, pk, q_out,
+                                                           k_out, v_out);
+  return cudaGetLastError();
+}
+
+cudaError_t time_embed(const TimeEmbedW& w, int B, const float* t_host, float* scratch, float* e0,
+                       float* e, cudaStream_t stream) {
+  if (B < 1 || B > 8) return cudaErrorInvalidValue;
+  TVals tv{};
+  for (int b = 0; b < B; ++b) tv.t[b] = t_host[b];
+  const int D = w.D, T = w.freq_dim;
+  float* sin_buf = scratch;              // [B, T]
+  float* h1 = scratch + 8 * T;           // [B, D]
+  float* se0 = h1 + 8 * D;               // [B, D]
+  sinusoid_kernel<<<1, 256, 0, stream>>>(tv, B, T, sin_buf);
+  const int wpb = 8;  // warps per block
+  gemv_kernel<<<(D + wpb - 1) / wpb, 32 * wpb, 0, stream>>>(sin_buf, w.w_t1, w.b_t1, D, T, B, nullptr, h1);
+  gemv_kernel<<<(D + wpb - 1) / wpb, 32 * wpb, 0, stream>>>(h1, w.w_t2, w.b_t2, D, D, B, e0, se0);
+  gemv_kernel<<<(6 * D + wpb - 1) / wpb, 32 * wpb, 0, stream>>>(se0, w.w_tp, w.b_tp, 6 * D, D, B, e, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t f32_to_bf16(const float* in, __nv_bfloat16* out, long long n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 4) return cudaErrorInvalidValue;
+  long long blocks = (n / 4 + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  f32_to_bf16_kernel<<<(int)blocks, 256, 0, stream>>>(in, out, n / 4);
+  return cudaGetLastError();
+}
+
+}  // namespace gs

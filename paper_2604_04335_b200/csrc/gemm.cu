@@ -1,0 +1,259 @@
+// tcgen05 GEMM for the DiT linear layers:
+//   C[M,N] = A[M,K] . W[N,K]^T, bf16 operands, fp32 accumulation in TMEM, fused epilogues
+//   (bias; GELU-tanh; fp32 gated residual x += g (.) (acc + b); Euler z += dsig (acc + b)).
+//
+// Design (B200-first):
+//   * persistent kernel, one CTA per SM, static tile schedule (tile t = blockIdx.x + i*grid);
+//   * warp 0: TMA producer (128B-swizzled K-major tiles, 4-stage mbarrier ring);
+//   * warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16);
+//   * warps 2..5: epilogue (tcgen05.ld 32x32b -> registers -> fused epilogue -> global);
+//   * two TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps the
+//     main loop of tile i+1.
+// Bit-exactness across M (SURVEY.md §8(a) invariant 1): no split-K, no atomics, the same
+// MMA shape and K order for every tile, each output row depends only on its own A row.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+#include "tma.h"
+
+namespace gs {
+
+namespace {
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int THREADS = 192;
+constexpr uint32_t TMEM_COLS = 512;
+
+__device__ __forceinline__ float gelu_tanh_f(float u) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * u * (1.0f + tanh_approx(k0 * (u + k1 * u * u * u)));
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int row, int col0,
+                                               const EpiParams& ep) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  if (ep.bias != nullptr) {
+    const uint4* bp = reinterpret_cast<const uint4*>(ep.bias + col0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 b = __ldg(bp + q);
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(b2[e]);
+        v[q * 8 + 2 * e] += f.x;
+        v[q * 8 + 2 * e + 1] += f.y;
+      }
+    }
+  }
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float a = v[2 * i], b = v[2 * i + 1];
+      if constexpr (EPI == EPI_GELU_BF16) {
+        a = gelu_tanh_f(a);
+        b = gelu_tanh_f(b);
+      }
+      pk[i] = pack_bf16x2(a, b);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) +
+                                          static_cast<size_t>(row) * ep.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  } else if constexpr (EPI == EPI_F32) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
+                                            static_cast<size_t>(row) * ep.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  } else if constexpr (EPI == EPI_RESID_F32) {
+    const int req = ep.row_req[row];
+    const float4* ga = reinterpret_cast<const float4*>(ep.gate_a + col0);
+    const float4* gb =
+        reinterpret_cast<const float4*>(ep.gate_b + static_cast<size_t>(req) * ep.gate_b_stride + col0);
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
+                                            static_cast<size_t>(row) * ep.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 a = __ldg(ga + q), b = __ldg(gb + q), x = dst[q];
+      x.x += (a.x + b.x) * v[4 * q + 0];
+      x.y += (a.y + b.y) * v[4 * q + 1];
+      x.z += (a.z + b.z) * v[4 * q + 2];
+      x.w += (a.w + b.w) * v[4 * q + 3];
+      dst[q] = x;
+    }
+  } else if constexpr (EPI == EPI_EULER_F32) {
+    const float ds = ep.dsig[ep.row_req[row]];
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
+                                            static_cast<size_t>(row) * ep.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 x = dst[q];
+      x.x += ds * v[4 * q + 0];
+      x.y += ds * v[4 * q + 1];
+      x.z += ds * v[4 * q + 2];
+      x.w += ds * v[4 * q + 3];
+      dst[q] = x;
+    }
+  }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   int M, int N, int K, const __grid_constant__ EpiParams ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;                 // [STAGES]
+  uint64_t* empty = bars + STAGES;       // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;   // [2]
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n, num_k = K / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int mb = t % num_m, nb = t / num_m;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(&tmA, &full[stage], sa, kb * BK, mb * BM);
+          tma_load_2d(&tmB, &full[stage], sa + A_BYTES, kb * BK, nb * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = sdesc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t bd = sdesc_sw128(sb + kk * 32, 16, 1024);
+            mma_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[as]);
+      }
+    }
+  } else {
+    // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    const int quarter = warp & 3;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const int mb = t % num_m, nb = t / num_m;
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[as], aphase);
+      tc_fence_after();
+      const int row = mb * BM + quarter * 32 + lane;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int col0 = nb * BN + c * 32;
+        if (col0 >= N) break;  // warp-uniform
+        uint32_t r[32];
+        GS_TMEM_LD32(tbase + c * 32, r);
+        tmem_ld_wait();
+        if (row < M) epilogue_chunk<EPI>(r, row, col0, ep);
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[as]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <int EPI>
+cudaError_t launch(int M, int N, int K, const void* A, int lda, const void* W, int ldw,
+                   const EpiParams& ep, int num_sms, cudaStream_t stream) {
+  CUtensorMap ta, tb;
+  if (!make_tma_2d_bf16(&ta, A, K, M, static_cast<uint64_t>(lda) * 2, BK, BM)) return cudaErrorInvalidValue;
+  if (!make_tma_2d_bf16(&tb, W, K, N, static_cast<uint64_t>(ldw) * 2, BK, BN)) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < num_sms ? tiles : num_sms;
+  gemm_tc_kernel<EPI><<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t gemm_bf16_tc(int epi, int M, int N, int K, const void* A, int lda, const void* W,
+                         int ldw, const EpiParams& ep, int num_sms, cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || K % BK != 0 || N % 32 != 0 || lda % 8 || ldw % 8)
+    return cudaErrorInvalidValue;
+  switch (epi) {
+    case EPI_BF16: return launch<EPI_BF16>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+    case EPI_GELU_BF16: return launch<EPI_GELU_BF16>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+    case EPI_F32: return launch<EPI_F32>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+    case EPI_RESID_F32: return launch<EPI_RESID_F32>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+    case EPI_EULER_F32: return launch<EPI_EULER_F32>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace gs

@@ -1,0 +1,1190 @@
+// libgs.so: C-ABI (include/gs.h) and host runtime of the DiT-step hot path.
+//
+// Executor for one batched denoising step at SP degree p (SURVEY.md §3 "Ours", §8(a)):
+//   time-embed -> patch-embed GEMM -> L x { LN1+mod -> QKV GEMM -> qk-RMSNorm+RoPE+pack ->
+//   a2a seq->head -> flash attention -> a2a head->seq -> O GEMM (+gated residual) ->
+//   LN2+mod -> MLP-up GEMM (+GELU) -> MLP-down GEMM (+gated residual) } -> head LN+mod ->
+//   head GEMM (+Euler update of the latent shard).
+// The latent stays token-sharded across steps; preemption is checked at step boundaries;
+// resume re-shards by copying contiguous token ranges (interval intersections).
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "runtime.h"
+
+using namespace gs;
+
+namespace {
+
+constexpr int MAX_BATCH = 8;
+
+int fail(gs_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, GS_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NK(call)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      return fail(c, GS_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+#define RET(call)               \
+  do {                          \
+    int rc_ = (call);           \
+    if (rc_ != GS_OK) return rc_; \
+  } while (0)
+
+int ensure(gs_ctx* c, DevBuf& b, size_t bytes) {
+  if (bytes <= b.cap) return GS_OK;
+  if (b.p) {
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaFree(b.p));
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  size_t want = bytes + bytes / 8 + 256;
+  if (cudaMalloc(&b.p, want) != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    return fail(c, GS_ENOMEM, "cudaMalloc(%zu) failed", want);
+  }
+  b.cap = want;
+  return GS_OK;
+}
+
+// ------------------------------------------------------------------ profiling scopes
+cudaEvent_t get_event(gs_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Scope {
+  gs_ctx* c;
+  const char* name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Scope(gs_ctx* c_, const char* n, int launches) : c(c_), name(n) {
+    c->launches += launches;
+    if (c->prof) {
+      a = get_event(c);
+      b = get_event(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~Scope() {
+    if (c->prof) {
+      cudaEventRecord(b, c->stream);
+      c->prof_pending.push_back({name, {a, b}});
+    }
+  }
+};
+
+void prof_flush(gs_ctx* c) {
+  for (auto& pe : c->prof_pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pe.second.first, pe.second.second);
+    auto& p = c->prof_tab[pe.first];
+    p.ms += ms;
+    p.n += 1;
+    c->event_pool.push_back(pe.second.first);
+    c->event_pool.push_back(pe.second.second);
+  }
+  c->prof_pending.clear();
+}
+
+int local_index(gs_ctx* c, int rank) {
+  if (c->emulated) return (rank >= 0 && rank < c->world) ? rank : -1;
+  return rank == c->my_rank ? 0 : -1;
+}
+
+// Contiguous shard i of n tokens over p ranks (reading 10).
+inline void shard_bounds(int n, int p, int i, int* lo, int* hi) {
+  *lo = static_cast<int>((static_cast<long long>(i) * n) / p);
+  *hi = static_cast<int>((static_cast<long long>(i + 1) * n) / p);
+}
+
+// Contiguous head split: positions < H mod p get ceil(H/p) heads (reading 9).
+inline int head_off(int H, int p, int j) { return j * (H / p) + std::min(j, H % p); }
+
+double sigma_at(int i, int S, double shift) {
+  const double u = 1.0 - static_cast<double>(i) / S;
+  return shift * u / (1.0 + (shift - 1.0) * u);
+}
+
+bool valid_p(int p) { return p == 1 || p == 2 || p == 4 || p == 8; }
+
+int check_ranks(gs_ctx* c, const int* ranks, int n) {
+  if (!ranks || !valid_p(n)) return fail(c, GS_EINVAL, "SP degree %d not in {1,2,4,8}", n);
+  for (int i = 0; i < n; ++i) {
+    if (ranks[i] < 0 || ranks[i] >= c->world) return fail(c, GS_EINVAL, "rank %d out of range", ranks[i]);
+    for (int j = 0; j < i; ++j)
+      if (ranks[i] == ranks[j]) return fail(c, GS_EINVAL, "duplicate rank %d", ranks[i]);
+  }
+  return GS_OK;
+}
+
+// ------------------------------------------------------------------ weights
+struct WSpec {
+  const char* name;
+  uint32_t tid;
+  int kind;
+  long long rows, cols;  // elements = rows * cols
+  int fan_in;            // > 0: scale sqrt(3/fan_in)
+  float scale;
+};
+
+int gen(gs_ctx* c, Model& m, void** dst, const WSpec& s, uint64_t seed) {
+  const long long n = s.rows * s.cols;
+  const size_t bytes = n * (s.kind == RNG_F32_SCALED ? 4 : 2);
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, GS_ENOMEM, "weight alloc %s (%zu B) failed", s.name, bytes);
+  }
+  m.allocs.push_back(p);
+  const float scale = s.fan_in > 0 ? static_cast<float>(std::sqrt(3.0 / s.fan_in)) : s.scale;
+  CK(rng_fill(p, n, seed, s.tid, s.kind, scale, c->stream));
+  *dst = p;
+  return GS_OK;
+}
+
+// Tensor table of one block / the global parameters (names and tensor ids match synth/rng.py TID).
+std::vector<WSpec> block_specs(const gs_model_desc& d) {
+  const long long D = d.dim, F = d.ffn;
+  return {
+      {"w_qkv", 1, RNG_BF16_SCALED, 3 * D, D, (int)D, 0},
+      {"b_qkv", 2, RNG_BF16_SCALED, 1, 3 * D, 0, 0.1f},
+      {"g_q", 3, RNG_BF16_GAIN, 1, D, 0, 0},
+      {"g_k", 4, RNG_BF16_GAIN, 1, D, 0, 0},
+      {"w_o", 5, RNG_BF16_SCALED, D, D, (int)D, 0},
+      {"b_o", 6, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"w_1", 7, RNG_BF16_SCALED, F, D, (int)D, 0},
+      {"b_1", 8, RNG_BF16_SCALED, 1, F, 0, 0.1f},
+      {"w_2", 9, RNG_BF16_SCALED, D, F, (int)F, 0},
+      {"b_2", 10, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"mod", 11, RNG_F32_SCALED, 6, D, 0, 0.5f},
+  };
+}
+std::vector<WSpec> global_specs(const gs_model_desc& d) {
+  const long long D = d.dim, P = d.lat, T = d.freq_dim;
+  return {
+      {"w_pe", 20, RNG_BF16_SCALED, D, P, (int)P, 0},
+      {"b_pe", 21, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"w_t1", 22, RNG_BF16_SCALED, D, T, (int)T, 0},
+      {"b_t1", 23, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"w_t2", 24, RNG_BF16_SCALED, D, D, (int)D, 0},
+      {"b_t2", 25, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"w_tp", 26, RNG_BF16_SCALED, 6 * D, D, (int)D, 0},
+      {"b_tp", 27, RNG_BF16_SCALED, 1, 6 * D, 0, 0.1f},
+      {"mod_head", 28, RNG_F32_SCALED, 2, D, 0, 0.5f},
+      {"w_head", 29, RNG_BF16_SCALED, P, D, (int)D, 0},
+      {"b_head", 30, RNG_BF16_SCALED, 1, P, 0, 0.1f},
+  };
+}
+
+void** block_slot(BlockW& b, const char* name) {
+  if (!strcmp(name, "w_qkv")) return (void**)&b.w_qkv;
+  if (!strcmp(name, "b_qkv")) return (void**)&b.b_qkv;
+  if (!strcmp(name, "g_q")) return (void**)&b.g_q;
+  if (!strcmp(name, "g_k")) return (void**)&b.g_k;
+  if (!strcmp(name, "w_o")) return (void**)&b.w_o;
+  if (!strcmp(name, "b_o")) return (void**)&b.b_o;
+  if (!strcmp(name, "w_1")) return (void**)&b.w_1;
+  if (!strcmp(name, "b_1")) return (void**)&b.b_1;
+  if (!strcmp(name, "w_2")) return (void**)&b.w_2;
+  if (!strcmp(name, "b_2")) return (void**)&b.b_2;
+  if (!strcmp(name, "mod")) return (void**)&b.mod;
+  return nullptr;
+}
+void** global_slot(Model& m, const char* name) {
+  if (!strcmp(name, "w_pe")) return (void**)&m.w_pe;
+  if (!strcmp(name, "b_pe")) return (void**)&m.b_pe;
+  if (!strcmp(name, "w_t1")) return (void**)&m.w_t1;
+  if (!strcmp(name, "b_t1")) return (void**)&m.b_t1;
+  if (!strcmp(name, "w_t2")) return (void**)&m.w_t2;
+  if (!strcmp(name, "b_t2")) return (void**)&m.b_t2;
+  if (!strcmp(name, "w_tp")) return (void**)&m.w_tp;
+  if (!strcmp(name, "b_tp")) return (void**)&m.b_tp;
+  if (!strcmp(name, "mod_head")) return (void**)&m.mod_head;
+  if (!strcmp(name, "w_head")) return (void**)&m.w_head;
+  if (!strcmp(name, "b_head")) return (void**)&m.b_head;
+  return nullptr;
+}
+
+// ------------------------------------------------------------------ batch plan
+struct Plan {
+  int p = 1, B = 0, D = 0, H = 0, hd = 0, F = 0;
+  Model* m = nullptr;
+  std::vector<Request*> reqs;
+  std::vector<int> ranks;
+  std::vector<int> hoff;      // p + 1
+  std::vector<int> off_full;  // B
+  int rows_full = 0;
+  std::vector<std::vector<int>> lo, hi, loff;  // [pos][req]
+  std::vector<int> rows;                        // [pos]
+  int H_loc(int j) const { return hoff[j + 1] - hoff[j]; }
+};
+
+void make_plan(Plan& P, Model* m, const std::vector<Request*>& reqs, const int* ranks, int p) {
+  P.m = m;
+  P.p = p;
+  P.B = static_cast<int>(reqs.size());
+  P.D = m->desc.dim;
+  P.H = m->desc.heads;
+  P.hd = m->hd;
+  P.F = m->desc.ffn;
+  P.reqs = reqs;
+  P.ranks.assign(ranks, ranks + p);
+  P.hoff.resize(p + 1);
+  for (int j = 0; j <= p; ++j) P.hoff[j] = head_off(P.H, p, j);
+  P.off_full.resize(P.B);
+  P.rows_full = 0;
+  for (int r = 0; r < P.B; ++r) {
+    P.off_full[r] = P.rows_full;
+    P.rows_full += reqs[r]->n;
+  }
+  P.lo.assign(p, std::vector<int>(P.B));
+  P.hi.assign(p, std::vector<int>(P.B));
+  P.loff.assign(p, std::vector<int>(P.B));
+  P.rows.assign(p, 0);
+  for (int i = 0; i < p; ++i) {
+    int acc = 0;
+    for (int r = 0; r < P.B; ++r) {
+      shard_bounds(reqs[r]->n, p, i, &P.lo[i][r], &P.hi[i][r]);
+      P.loff[i][r] = acc;
+      acc += P.hi[i][r] - P.lo[i][r];
+    }
+    P.rows[i] = acc;
+  }
+}
+
+// Size the arena of position i and upload its row maps.
+int prepare_rank(gs_ctx* c, const Plan& P, int i, RankArena& A) {
+  const size_t rows = std::max(P.rows[i], 1), rf = std::max(P.rows_full, 1);
+  const size_t D = P.D, F = P.F, lat = P.m->desc.lat;
+  const size_t hl = static_cast<size_t>(P.H_loc(i)) * P.hd;
+  RET(ensure(c, A.x, rows * D * 4));
+  RET(ensure(c, A.a, rows * D * 2));
+  RET(ensure(c, A.qkv, rows * 3 * D * 2));
+  RET(ensure(c, A.qs, rows * D * 2));
+  RET(ensure(c, A.ks, rows * D * 2));
+  RET(ensure(c, A.vs, rows * D * 2));
+  if (P.p > 1) {
+    RET(ensure(c, A.qr, rf * hl * 2));
+    RET(ensure(c, A.kr, rf * hl * 2));
+    RET(ensure(c, A.vr, rf * hl * 2));
+    RET(ensure(c, A.o, rf * hl * 2));
+    RET(ensure(c, A.orecv, rows * D * 2));
+    RET(ensure(c, A.ostage, rows * D * 2));
+  } else {
+    RET(ensure(c, A.o, rows * D * 2));
+  }
+  RET(ensure(c, A.h, rows * F * 2));
+  RET(ensure(c, A.zpack, rows * lat * 4));
+  RET(ensure(c, A.zb, rows * lat * 2));
+  RET(ensure(c, A.e0, MAX_BATCH * D * 4));
+  RET(ensure(c, A.e, MAX_BATCH * 6 * D * 4));
+  RET(ensure(c, A.temb, (MAX_BATCH * P.m->desc.freq_dim + 2 * MAX_BATCH * D) * 4));
+  RET(ensure(c, A.row_req, rows * 4));
+  RET(ensure(c, A.row_tok, rows * 4));
+  RET(ensure(c, A.req_grid, MAX_BATCH * 3 * 4));
+  std::vector<int> rr(P.rows[i]), rt(P.rows[i]), grid(P.B * 3);
+  for (int r = 0; r < P.B; ++r) {
+    for (int t = P.lo[i][r]; t < P.hi[i][r]; ++t) {
+      rr[P.loff[i][r] + t - P.lo[i][r]] = r;
+      rt[P.loff[i][r] + t - P.lo[i][r]] = t;
+    }
+    for (int a = 0; a < 3; ++a) grid[3 * r + a] = P.reqs[r]->grid[a];
+  }
+  if (P.rows[i] > 0) {
+    CK(cudaMemcpyAsync(A.row_req.p, rr.data(), rr.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(A.row_tok.p, rt.data(), rt.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  }
+  CK(cudaMemcpyAsync(A.req_grid.p, grid.data(), grid.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+  return GS_OK;
+}
+
+// gather (dir = 0) / scatter (dir = 1) request shards <-> packed latent of position i
+int move_latent(gs_ctx* c, const Plan& P, int i, RankArena& A, int dir) {
+  const size_t lat = P.m->desc.lat;
+  for (int r = 0; r < P.B; ++r) {
+    const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * lat * 4;
+    if (!cnt) continue;
+    float* packed = A.zpack.as<float>() + static_cast<size_t>(P.loff[i][r]) * lat;
+    float* shard = P.reqs[r]->shards[i].z;
+    if (dir == 0)
+      CK(cudaMemcpyAsync(packed, shard, cnt, cudaMemcpyDeviceToDevice, c->stream));
+    else
+      CK(cudaMemcpyAsync(shard, packed, cnt, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return GS_OK;
+}
+
+// ------------------------------------------------------------------ exchanges
+// seq -> head: Q/K/V chunk j of position i (rows of i, heads of j) -> recv buffers of j.
+int exchange_qkv(gs_ctx* c, const Plan& P) {
+  Scope sc(c, "a2a_qkv", 0);
+  const size_t d = P.hd;
+  if (c->emulated) {
+    for (int i = 0; i < P.p; ++i) {
+      RankArena& S = c->local[P.ranks[i]];
+      for (int j = 0; j < P.p; ++j) {
+        RankArena& R = c->local[P.ranks[j]];
+        const size_t Hj = P.H_loc(j);
+        const size_t chunk = static_cast<size_t>(P.rows[i]) * P.hoff[j] * d;
+        for (int r = 0; r < P.B; ++r) {
+          const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * Hj * d;
+          if (!cnt) continue;
+          const size_t so = chunk + static_cast<size_t>(P.loff[i][r]) * Hj * d;
+          const size_t ro = static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * Hj * d;
+          CK(cudaMemcpyAsync(R.qr.as<bf16>() + ro, S.qs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
+          CK(cudaMemcpyAsync(R.kr.as<bf16>() + ro, S.ks.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
+          CK(cudaMemcpyAsync(R.vr.as<bf16>() + ro, S.vs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
+        }
+      }
+    }
+    return GS_OK;
+  }
+  int me = -1;
+  for (int i = 0; i < P.p; ++i)
+    if (P.ranks[i] == c->my_rank) me = i;
+  RankArena& A = c->local[0];
+  NK(ncclGroupStart());
+  for (int j = 0; j < P.p; ++j) {  // my rows -> j
+    const size_t Hj = P.H_loc(j);
+    const size_t chunk = static_cast<size_t>(P.rows[me]) * P.hoff[j] * d;
+    for (int r = 0; r < P.B; ++r) {
+      const size_t cnt = static_cast<size_t>(P.hi[me][r] - P.lo[me][r]) * Hj * d;
+      if (!cnt) continue;
+      const size_t so = chunk + static_cast<size_t>(P.loff[me][r]) * Hj * d;
+      if (j == me) {
+        const size_t ro = static_cast<size_t>(P.off_full[r] + P.lo[me][r]) * Hj * d;
+        CK(cudaMemcpyAsync(A.qr.as<bf16>() + ro, A.qs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(A.kr.as<bf16>() + ro, A.ks.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(A.vr.as<bf16>() + ro, A.vs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
+      } else {
+        NK(ncclSend(A.qs.as<bf16>() + so, cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
+        NK(ncclSend(A.ks.as<bf16>() + so, cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
+        NK(ncclSend(A.vs.as<bf16>() + so, cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
+      }
+    }
+  }
+  const size_t Hm = P.H_loc(me);
+  for (int i = 0; i < P.p; ++i) {  // rows of i, my heads
+    if (i == me) continue;
+    for (int r = 0; r < P.B; ++r) {
+      const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * Hm * d;
+      if (!cnt) continue;
+      const size_t ro = static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * Hm * d;
+      NK(ncclRecv(A.qr.as<bf16>() + ro, cnt * 2, ncclUint8, P.ranks[i], c->comm, c->stream));
+      NK(ncclRecv(A.kr.as<bf16>() + ro, cnt * 2, ncclUint8, P.ranks[i], c->comm, c->stream));
+      NK(ncclRecv(A.vr.as<bf16>() + ro, cnt * 2, ncclUint8, P.ranks[i], c->comm, c->stream));
+    }
+  }
+  NK(ncclGroupEnd());
+  return GS_OK;
+}
+
+// head -> seq: attention output of position j (all rows, heads of j) -> rows' owners.
+int exchange_o(gs_ctx* c, const Plan& P) {
+  Scope sc(c, "a2a_o", 0);
+  const size_t d = P.hd, D = P.D;
+  if (c->emulated) {
+    for (int j = 0; j < P.p; ++j) {
+      RankArena& S = c->local[P.ranks[j]];
+      const size_t w = static_cast<size_t>(P.H_loc(j)) * d;
+      for (int i = 0; i < P.p; ++i) {
+        RankArena& R = c->local[P.ranks[i]];
+        for (int r = 0; r < P.B; ++r) {
+          const size_t cnt = P.hi[i][r] - P.lo[i][r];
+          if (!cnt) continue;
+          CK(cudaMemcpy2DAsync(R.orecv.as<bf16>() + static_cast<size_t>(P.loff[i][r]) * D + P.hoff[j] * d, D * 2,
+                               S.o.as<bf16>() + static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * w, w * 2, w * 2, cnt,
+                               cudaMemcpyDeviceToDevice, c->stream));
+        }
+      }
+    }
+    return GS_OK;
+  }
+  int me = -1;
+  for (int i = 0; i < P.p; ++i)
+    if (P.ranks[i] == c->my_rank) me = i;
+  RankArena& A = c->local[0];
+  const size_t wm = static_cast<size_t>(P.H_loc(me)) * d;
+  // staging layout: [src j][req r][rows][H_j d]
+  std::vector<size_t> stage_off(P.p * P.B);
+  size_t acc = 0;
+  for (int j = 0; j < P.p; ++j)
+    for (int r = 0; r < P.B; ++r) {
+      stage_off[j * P.B + r] = acc;
+      acc += static_cast<size_t>(P.hi[me][r] - P.lo[me][r]) * P.H_loc(j) * d;
+    }
+  NK(ncclGroupStart());
+  for (int i = 0; i < P.p; ++i) {
+    if (i == me) continue;
+    for (int r = 0; r < P.B; ++r) {
+      const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * wm;
+      if (!cnt) continue;
+      NK(ncclSend(A.o.as<bf16>() + static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * wm, cnt * 2, ncclUint8,
+                  P.ranks[i], c->comm, c->stream));
+    }
+  }
+  for (int j = 0; j < P.p; ++j) {
+    if (j == me) continue;
+    const size_t wj = static_cast<size_t>(P.H_loc(j)) * d;
+    for (int r = 0; r < P.B; ++r) {
+      const size_t cnt = static_cast<size_t>(P.hi[me][r] - P.lo[me][r]) * wj;
+      if (!cnt) continue;
+      NK(ncclRecv(A.ostage.as<bf16>() + stage_off[j * P.B + r], cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
+    }
+  }
+  NK(ncclGroupEnd());
+  for (int j = 0; j < P.p; ++j) {
+    const size_t wj = static_cast<size_t>(P.H_loc(j)) * d;
+    for (int r = 0; r < P.B; ++r) {
+      const size_t cnt = P.hi[me][r] - P.lo[me][r];
+      if (!cnt) continue;
+      const bf16* src = (j == me) ? A.o.as<bf16>() + static_cast<size_t>(P.off_full[r] + P.lo[me][r]) * wm
+                                  : A.ostage.as<bf16>() + stage_off[j * P.B + r];
+      CK(cudaMemcpy2DAsync(A.orecv.as<bf16>() + static_cast<size_t>(P.loff[me][r]) * D + P.hoff[j] * d, D * 2, src,
+                           wj * 2, wj * 2, cnt, cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+  return GS_OK;
+}
+
+// ------------------------------------------------------------------ one step
+int gemm(gs_ctx* c, const char* name, int epi, int M, int N, int K, const void* A, const void* W,
+         const EpiParams& ep) {
+  if (M == 0) return GS_OK;
+  Scope sc(c, name, 1);
+  CK(gemm_bf16_tc(epi, M, N, K, A, K, W, K, ep, c->num_sms, c->stream));
+  return GS_OK;
+}
+
+EpiParams epi(void* out, int ldo, const bf16* bias) {
+  EpiParams e{};
+  e.out = out;
+  e.ldo = ldo;
+  e.bias = bias;
+  return e;
+}
+
+// Pre-attention part of layer l (or the step prologue when l < 0) for position i.
+int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
+  const int M = P.rows[i], D = P.D;
+  const BlockW& w = P.m->blocks[l];
+  const float eps = P.m->desc.eps;
+  {
+    Scope sc(c, "ln_mod", 1);
+    if (M) CK(ln_modulate(A.x.as<float>(), M, D, w.mod + 0 * D, A.e.as<float>() + 0 * D, w.mod + 1 * D,
+                          A.e.as<float>() + 1 * D, 6 * D, A.row_req.as<int>(), eps, A.a.as<bf16>(), c->stream));
+  }
+  RET(gemm(c, "gemm_qkv", EPI_BF16, M, 3 * D, D, A.a.p, w.w_qkv, epi(A.qkv.p, 3 * D, w.b_qkv)));
+  {
+    Scope sc(c, "qk_norm_rope", 1);
+    RopeParams rp{A.row_req.as<int>(), A.row_tok.as<int>(), A.req_grid.as<int>(), P.m->cs_tab, P.m->slot_axis,
+                  P.m->p_max};
+    PackParams pk{};
+    pk.ndest = P.p;
+    pk.rows = M;
+    for (int j = 0; j <= P.p; ++j) pk.head_off[j] = P.hoff[j];
+    for (int j = 0; j < P.p; ++j) pk.dest_off[j] = static_cast<long long>(M) * P.hoff[j] * P.hd;
+    if (M) CK(qk_norm_rope_pack(A.qkv.as<bf16>(), M, D, P.H, w.g_q, w.g_k, eps, rp, pk, A.qs.as<bf16>(),
+                                A.ks.as<bf16>(), A.vs.as<bf16>(), c->stream));
+  }
+  return GS_OK;
+}
+
+int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
+  Scope sc(c, "attention", 1);
+  const int Hj = P.H_loc(j);
+  if (Hj == 0) return GS_OK;
+  std::vector<int> so(P.B), sl(P.B);
+  for (int r = 0; r < P.B; ++r) {
+    so[r] = P.off_full[r];
+    sl[r] = P.reqs[r]->n;
+  }
+  const int rs = Hj * P.hd;
+  if (P.p == 1)
+    CK(attention_tc(A.qs.p, A.ks.p, A.vs.p, A.o.p, Hj, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
+                    c->stream));
+  else
+    CK(attention_tc(A.qr.p, A.kr.p, A.vr.p, A.o.p, Hj, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
+                    c->stream));
+  return GS_OK;
+}
+
+int block_post(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
+  const int M = P.rows[i], D = P.D, F = P.F;
+  const BlockW& w = P.m->blocks[l];
+  EpiParams eo = epi(A.x.p, D, w.b_o);
+  eo.gate_a = w.mod + 2 * D;
+  eo.gate_b = A.e.as<float>() + 2 * D;
+  eo.gate_b_stride = 6 * D;
+  eo.row_req = A.row_req.as<int>();
+  const void* oin = P.p == 1 ? A.o.p : A.orecv.p;
+  RET(gemm(c, "gemm_o", EPI_RESID_F32, M, D, D, oin, w.w_o, eo));
+  {
+    Scope sc(c, "ln_mod", 1);
+    if (M) CK(ln_modulate(A.x.as<float>(), M, D, w.mod + 3 * D, A.e.as<float>() + 3 * D, w.mod + 4 * D,
+                          A.e.as<float>() + 4 * D, 6 * D, A.row_req.as<int>(), P.m->desc.eps, A.a.as<bf16>(),
+                          c->stream));
+  }
+  RET(gemm(c, "gemm_mlp_up", EPI_GELU_BF16, M, F, D, A.a.p, w.w_1, epi(A.h.p, F, w.b_1)));
+  EpiParams e2 = epi(A.x.p, D, w.b_2);
+  e2.gate_a = w.mod + 5 * D;
+  e2.gate_b = A.e.as<float>() + 5 * D;
+  e2.gate_b_stride = 6 * D;
+  e2.row_req = A.row_req.as<int>();
+  RET(gemm(c, "gemm_mlp_down", EPI_RESID_F32, M, D, F, A.h.p, w.w_2, e2));
+  return GS_OK;
+}
+
+int step_prologue(gs_ctx* c, const Plan& P, int i, RankArena& A, const float* t) {
+  const int M = P.rows[i], D = P.D;
+  Model* m = P.m;
+  {
+    Scope sc(c, "time_embed", 4);
+    TimeEmbedW tw{m->w_t1, m->b_t1, m->w_t2, m->b_t2, m->w_tp, m->b_tp, D, m->desc.freq_dim};
+    CK(time_embed(tw, P.B, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), c->stream));
+  }
+  {
+    Scope sc(c, "patch_embed", 1);
+    if (M) CK(f32_to_bf16(A.zpack.as<float>(), A.zb.as<bf16>(), static_cast<long long>(M) * m->desc.lat, c->stream));
+  }
+  RET(gemm(c, "patch_embed", EPI_F32, M, D, m->desc.lat, A.zb.p, m->w_pe, epi(A.x.p, D, m->b_pe)));
+  return GS_OK;
+}
+
+int step_epilogue(gs_ctx* c, const Plan& P, int i, RankArena& A, const float* dsig) {
+  const int M = P.rows[i], D = P.D;
+  Model* m = P.m;
+  {
+    Scope sc(c, "head", 1);
+    if (M) CK(ln_modulate(A.x.as<float>(), M, D, m->mod_head, A.e0.as<float>(), m->mod_head + D, A.e0.as<float>(), D,
+                          A.row_req.as<int>(), m->desc.eps, A.a.as<bf16>(), c->stream));
+  }
+  EpiParams eh = epi(A.zpack.p, m->desc.lat, m->b_head);
+  eh.row_req = A.row_req.as<int>();
+  for (int r = 0; r < P.B; ++r) eh.dsig[r] = dsig[r];
+  RET(gemm(c, "head", EPI_EULER_F32, M, m->desc.lat, D, A.a.p, m->w_head, eh));
+  return GS_OK;
+}
+
+// Positions of the plan owned by this process.
+std::vector<int> local_positions(gs_ctx* c, const Plan& P) {
+  std::vector<int> out;
+  for (int i = 0; i < P.p; ++i)
+    if (local_index(c, P.ranks[i]) >= 0) out.push_back(i);
+  return out;
+}
+
+int run_one_step(gs_ctx* c, const Plan& P, const std::vector<int>& mine) {
+  float t[MAX_BATCH], dsig[MAX_BATCH];
+  for (int r = 0; r < P.B; ++r) {
+    const Request* q = P.reqs[r];
+    const double s0 = sigma_at(q->step_idx, q->steps, P.m->desc.flow_shift);
+    const double s1 = sigma_at(q->step_idx + 1, q->steps, P.m->desc.flow_shift);
+    t[r] = static_cast<float>(1000.0 * s0);
+    dsig[r] = static_cast<float>(s1 - s0);
+  }
+  for (int i : mine) RET(step_prologue(c, P, i, c->local[local_index(c, P.ranks[i])], t));
+  for (int l = 0; l < P.m->desc.layers; ++l) {
+    for (int i : mine) RET(block_pre(c, P, i, c->local[local_index(c, P.ranks[i])], l));
+    if (P.p > 1) RET(exchange_qkv(c, P));
+    for (int i : mine) RET(block_attn(c, P, i, c->local[local_index(c, P.ranks[i])]));
+    if (P.p > 1) RET(exchange_o(c, P));
+    for (int i : mine) RET(block_post(c, P, i, c->local[local_index(c, P.ranks[i])], l));
+  }
+  for (int i : mine) RET(step_epilogue(c, P, i, c->local[local_index(c, P.ranks[i])], dsig));
+  return GS_OK;
+}
+
+// Agree on "stop at this boundary" across the SP group (NCCL mode): OR of local flags.
+int agree_stop(gs_ctx* c, const Plan& P, int local_flag, int* stop) {
+  if (c->emulated || P.p == 1) {
+    *stop = local_flag;
+    return GS_OK;
+  }
+  int me = 0;
+  for (int i = 0; i < P.p; ++i)
+    if (P.ranks[i] == c->my_rank) me = i;
+  c->h_flag[0] = local_flag;
+  CK(cudaMemcpyAsync(c->d_flag, c->h_flag, 4, cudaMemcpyHostToDevice, c->stream));
+  NK(ncclGroupStart());
+  for (int j = 0; j < P.p; ++j) {
+    if (j == me) continue;
+    NK(ncclSend(c->d_flag, 1, ncclInt32, P.ranks[j], c->comm, c->stream));
+    NK(ncclRecv(c->d_flag + 1 + j, 1, ncclInt32, P.ranks[j], c->comm, c->stream));
+  }
+  NK(ncclGroupEnd());
+  CK(cudaMemcpyAsync(c->h_flag + 1, c->d_flag + 1, 8 * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int s = local_flag;
+  for (int j = 0; j < P.p; ++j)
+    if (j != me) s |= c->h_flag[1 + j];
+  *stop = s;
+  return GS_OK;
+}
+
+Request* find_req(gs_ctx* c, gs_req id) {
+  std::lock_guard<std::mutex> g(c->table_mu);
+  auto it = c->reqs.find(id);
+  return it == c->reqs.end() ? nullptr : it->second.get();
+}
+
+int alloc_shard(gs_ctx* c, Shard& s, int lat) {
+  const size_t bytes = static_cast<size_t>(std::max(s.hi - s.lo, 1)) * lat * 4;
+  if (cudaMalloc(&s.z, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    s.z = nullptr;
+    return fail(c, GS_ENOMEM, "latent shard alloc failed");
+  }
+  return GS_OK;
+}
+
+}  // namespace
+
+// ==================================================================== C-ABI
+extern "C" {
+
+int gs_nccl_unique_id(void* out128) {
+  if (!out128) return GS_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return GS_ENCCL;
+  memcpy(out128, &id, sizeof(id));
+  return GS_OK;
+}
+
+static int init_common(gs_ctx* c, int device) {
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaMallocHost(&c->h_flag, 16 * 4));
+  CK(cudaMalloc(&c->d_flag, 16 * 4));
+  return GS_OK;
+}
+
+int gs_init(int device, int world_size, int rank, const void* nccl_uid, gs_ctx** out) {
+  if (!out || world_size < 1 || rank < 0 || rank >= world_size) return GS_EINVAL;
+  gs_ctx* c = new gs_ctx();
+  c->device = device;
+  c->world = world_size;
+  c->my_rank = rank;
+  int rc = init_common(c, device);
+  if (rc != GS_OK) {
+    *out = c;
+    return rc;
+  }
+  c->local.resize(1);
+  c->local[0].rank = rank;
+  if (world_size > 1) {
+    if (!nccl_uid) {
+      *out = c;
+      return fail(c, GS_EINVAL, "world_size > 1 needs an NCCL unique id");
+    }
+    ncclUniqueId id;
+    memcpy(&id, nccl_uid, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, world_size, id, rank);
+    if (r != ncclSuccess) {
+      *out = c;
+      return fail(c, GS_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+  }
+  *out = c;
+  return GS_OK;
+}
+
+int gs_init_emulated(int device, int world_size, gs_ctx** out) {
+  if (!out || world_size < 1 || world_size > 8) return GS_EINVAL;
+  gs_ctx* c = new gs_ctx();
+  c->device = device;
+  c->world = world_size;
+  c->emulated = true;
+  int rc = init_common(c, device);
+  c->local.resize(world_size);
+  for (int r = 0; r < world_size; ++r) c->local[r].rank = r;
+  *out = c;
+  return rc;
+}
+
+void gs_destroy(gs_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->reqs)
+    for (auto& s : kv.second->shards)
+      if (s.z) cudaFree(s.z);
+  for (auto& m : c->models)
+    for (void* p : m->allocs) cudaFree(p);
+  for (auto& A : c->local) {
+    DevBuf* bufs[] = {&A.x, &A.a, &A.qkv, &A.qs, &A.ks, &A.vs, &A.qr, &A.kr, &A.vr, &A.o, &A.orecv,
+                      &A.ostage, &A.h, &A.zpack, &A.zb, &A.e0, &A.e, &A.temb, &A.row_req, &A.row_tok,
+                      &A.req_grid};
+    for (DevBuf* b : bufs)
+      if (b->p) cudaFree(b->p);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
+  if (c->d_flag) cudaFree(c->d_flag);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* gs_last_error(gs_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int gs_info(gs_ctx* c, int* num_sms, int* world_size, int* nlocal) {
+  if (!c) return GS_EINVAL;
+  if (num_sms) *num_sms = c->num_sms;
+  if (world_size) *world_size = c->world;
+  if (nlocal) *nlocal = static_cast<int>(c->local.size());
+  return GS_OK;
+}
+
+int gs_model_create(gs_ctx* c, const gs_model_desc* d, int* model_id) {
+  if (!c || !d || !model_id) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  if (d->dim <= 0 || d->heads <= 0 || d->dim % d->heads || d->dim % 64 || d->dim > 8192 || d->ffn % 256 ||
+      d->layers < 1 || d->lat != 64 || d->freq_dim % 2 || d->freq_dim % 64)
+    return fail(c, GS_EINVAL, "unsupported model shape (dim %d heads %d ffn %d lat %d)", d->dim, d->heads, d->ffn, d->lat);
+  const int hd = d->dim / d->heads;
+  if (hd != 64 && hd != 128) return fail(c, GS_EUNSUPPORTED, "head dim %d not in {64, 128}", hd);
+  auto m = std::make_unique<Model>();
+  m->desc = *d;
+  m->hd = hd;
+  m->blocks.resize(d->layers);
+  for (int l = 0; l < d->layers; ++l)
+    for (const WSpec& s : block_specs(*d)) RET(gen(c, *m, block_slot(m->blocks[l], s.name), s, d->weight_seed + l));
+  for (const WSpec& s : global_specs(*d)) RET(gen(c, *m, global_slot(*m, s.name), s, d->weight_seed + 1000000ull));
+  // RoPE table (reading 1 / SURVEY.md §8(c) step 4): slots [d/2 - 2 floor(d/6), floor(d/6), floor(d/6)]
+  const int half = hd / 2, s3 = hd / 6;
+  const int slots[3] = {half - 2 * s3, s3, s3};
+  std::vector<int> axis(half);
+  std::vector<double> freq(half);
+  int k = 0;
+  for (int a = 0; a < 3; ++a)
+    for (int j = 0; j < slots[a]; ++j, ++k) {
+      axis[k] = a;
+      freq[k] = std::pow(static_cast<double>(d->rope_theta), -2.0 * j / (2.0 * slots[a]));
+    }
+  std::vector<float2> tab(static_cast<size_t>(m->p_max) * half);
+  for (int p = 0; p < m->p_max; ++p)
+    for (int s = 0; s < half; ++s) {
+      const double ang = p * freq[s];
+      tab[static_cast<size_t>(p) * half + s] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+    }
+  void *pt = nullptr, *pa = nullptr;
+  CK(cudaMalloc(&pt, tab.size() * sizeof(float2)));
+  m->allocs.push_back(pt);
+  CK(cudaMalloc(&pa, axis.size() * 4));
+  m->allocs.push_back(pa);
+  CK(cudaMemcpy(pt, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(pa, axis.data(), axis.size() * 4, cudaMemcpyHostToDevice));
+  m->cs_tab = static_cast<float2*>(pt);
+  m->slot_axis = static_cast<int*>(pa);
+  CK(cudaStreamSynchronize(c->stream));
+  c->models.push_back(std::move(m));
+  *model_id = static_cast<int>(c->models.size()) - 1;
+  return GS_OK;
+}
+
+int gs_get_weight(gs_ctx* c, int model, int layer, const char* name, void* host, size_t bytes) {
+  if (!c || !name || !host) return GS_EINVAL;
+  if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
+  Model& m = *c->models[model];
+  const auto specs = layer < 0 ? global_specs(m.desc) : block_specs(m.desc);
+  if (layer >= m.desc.layers) return fail(c, GS_EINVAL, "bad layer");
+  for (const WSpec& s : specs) {
+    if (strcmp(s.name, name)) continue;
+    const size_t want = s.rows * s.cols * (s.kind == RNG_F32_SCALED ? 4 : 2);
+    if (bytes != want) return fail(c, GS_EINVAL, "%s is %zu bytes, got %zu", name, want, bytes);
+    void** slot = layer < 0 ? global_slot(m, name) : block_slot(m.blocks[layer], name);
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpy(host, *slot, bytes, cudaMemcpyDeviceToHost));
+    return GS_OK;
+  }
+  return fail(c, GS_EINVAL, "unknown tensor %s", name);
+}
+
+int gs_submit(gs_ctx* c, int model, int width, int height, int frames, int steps, uint64_t noise_seed,
+              const float* init_latent, const int* ranks, int nranks, gs_req* out) {
+  if (!c || !out) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
+  if (width <= 0 || height <= 0 || width % 16 || height % 16 || frames < 1 || (frames - 1) % 4 || steps < 1)
+    return fail(c, GS_EINVAL, "bad request shape %dx%d frames %d steps %d", width, height, frames, steps);
+  RET(check_ranks(c, ranks, nranks));
+  Model& m = *c->models[model];
+  auto q = std::make_unique<Request>();
+  q->model = model;
+  q->grid[0] = 1 + (frames - 1) / 4;
+  q->grid[1] = height / 16;
+  q->grid[2] = width / 16;
+  if (q->grid[0] > m.p_max || q->grid[1] > m.p_max || q->grid[2] > m.p_max)
+    return fail(c, GS_EINVAL, "token grid exceeds RoPE table (%d)", m.p_max);
+  q->n = q->grid[0] * q->grid[1] * q->grid[2];
+  q->steps = steps;
+  q->ranks.assign(ranks, ranks + nranks);
+  q->shards.resize(nranks);
+  for (int i = 0; i < nranks; ++i) {
+    Shard& s = q->shards[i];
+    s.rank = ranks[i];
+    shard_bounds(q->n, nranks, i, &s.lo, &s.hi);
+    if (local_index(c, s.rank) < 0) continue;
+    RET(alloc_shard(c, s, m.desc.lat));
+    if (init_latent)
+      CK(cudaMemcpyAsync(s.z, init_latent + static_cast<size_t>(s.lo) * m.desc.lat,
+                         static_cast<size_t>(s.hi - s.lo) * m.desc.lat * 4, cudaMemcpyHostToDevice, c->stream));
+    else
+      CK(rng_noise(s.z, s.lo, s.hi - s.lo, m.desc.lat, noise_seed, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  std::lock_guard<std::mutex> g2(c->table_mu);
+  q->id = c->next_req++;
+  *out = q->id;
+  c->reqs[q->id] = std::move(q);
+  return GS_OK;
+}
+
+int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int nranks, int k, int* steps_run) {
+  if (!c || !ids) return GS_EINVAL;
+  if (steps_run) *steps_run = 0;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  if (nreq < 1 || nreq > MAX_BATCH) return fail(c, GS_EINVAL, "batch of %d requests (1..%d)", nreq, MAX_BATCH);
+  RET(check_ranks(c, ranks, nranks));
+  std::vector<Request*> reqs;
+  for (int r = 0; r < nreq; ++r) {
+    Request* q = find_req(c, ids[r]);
+    if (!q) return fail(c, GS_EINVAL, "unknown request %llu", (unsigned long long)ids[r]);
+    for (Request* o : reqs)
+      if (o == q) return fail(c, GS_EINVAL, "request listed twice");
+    if (q->state != GS_REQ_PLACED) return fail(c, GS_ESTATE, "request %llu is not runnable (state %d)", (unsigned long long)q->id, q->state);
+    if (!reqs.empty() && q->model != reqs[0]->model) return fail(c, GS_ESTATE, "batch mixes models");
+    if (static_cast<int>(q->ranks.size()) != nranks || !std::equal(q->ranks.begin(), q->ranks.end(), ranks))
+      return fail(c, GS_ESTATE, "request %llu is not placed on the given ranks", (unsigned long long)q->id);
+    if (k < 0 || q->step_idx + k > q->steps) return fail(c, GS_EINVAL, "k=%d exceeds remaining steps", k);
+    reqs.push_back(q);
+  }
+  Model* m = c->models[reqs[0]->model].get();
+  Plan P;
+  make_plan(P, m, reqs, ranks, nranks);
+  const std::vector<int> mine = local_positions(c, P);
+  for (int i : mine) {
+    RankArena& A = c->local[local_index(c, P.ranks[i])];
+    RET(prepare_rank(c, P, i, A));
+    RET(move_latent(c, P, i, A, 0));
+  }
+  for (Request* q : reqs) q->state = GS_REQ_RUNNING;
+  int done = 0, rc = GS_OK;
+  for (int s = 0; s < k; ++s) {
+    int flag = 0;
+    for (Request* q : reqs) flag |= q->preempt.load();
+    int stop = 0;
+    rc = agree_stop(c, P, flag, &stop);
+    if (rc != GS_OK || stop) break;
+    rc = run_one_step(c, P, mine);
+    if (rc != GS_OK) break;
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+      rc = fail(c, GS_ECUDA, "step failed: %s", cudaGetErrorString(e));
+      break;
+    }
+    prof_flush(c);
+    for (Request* q : reqs) ++q->step_idx;
+    ++done;
+  }
+  for (int i : mine) {
+    int r2 = move_latent(c, P, i, c->local[local_index(c, P.ranks[i])], 1);
+    if (rc == GS_OK) rc = r2;
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (rc == GS_OK && e != cudaSuccess) rc = fail(c, GS_ECUDA, "%s", cudaGetErrorString(e));
+  for (Request* q : reqs) {
+    if (q->preempt.load()) {
+      q->state = GS_REQ_PAUSED;
+      q->preempt.store(0);
+    } else {
+      q->state = q->step_idx >= q->steps ? GS_REQ_DONE : GS_REQ_PLACED;
+    }
+  }
+  if (steps_run) *steps_run = done;
+  return rc;
+}
+
+int gs_preempt(gs_ctx* c, gs_req id, int* steps_done_out) {
+  if (!c) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->table_mu);
+  auto it = c->reqs.find(id);
+  if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request");
+  Request* q = it->second.get();
+  if (q->state == GS_REQ_DONE) return fail(c, GS_ESTATE, "request already finished");
+  if (q->state == GS_REQ_RUNNING)
+    q->preempt.store(1);
+  else
+    q->state = GS_REQ_PAUSED;
+  if (steps_done_out) *steps_done_out = q->step_idx;
+  return GS_OK;
+}
+
+int gs_resume(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
+  if (!c) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  Request* q = find_req(c, id);
+  if (!q) return fail(c, GS_EINVAL, "unknown request");
+  if (q->state != GS_REQ_PAUSED && q->state != GS_REQ_PLACED)
+    return fail(c, GS_ESTATE, "resume needs a paused or placed request (state %d)", q->state);
+  RET(check_ranks(c, ranks, nranks));
+  const int lat = c->models[q->model]->desc.lat;
+  std::vector<Shard> ns(nranks);
+  for (int i = 0; i < nranks; ++i) {
+    ns[i].rank = ranks[i];
+    shard_bounds(q->n, nranks, i, &ns[i].lo, &ns[i].hi);
+    if (local_index(c, ns[i].rank) >= 0) RET(alloc_shard(c, ns[i], lat));
+  }
+  // interval intersections old x new: pure copies
+  bool nccl_open = false;
+  if (!c->emulated && c->world > 1) {
+    NK(ncclGroupStart());
+    nccl_open = true;
+  }
+  for (const Shard& o : q->shards)
+    for (const Shard& n : ns) {
+      const int lo = std::max(o.lo, n.lo), hi = std::min(o.hi, n.hi);
+      if (lo >= hi) continue;
+      const size_t bytes = static_cast<size_t>(hi - lo) * lat * 4;
+      const bool have_o = local_index(c, o.rank) >= 0, have_n = local_index(c, n.rank) >= 0;
+      float* src = have_o ? o.z + static_cast<size_t>(lo - o.lo) * lat : nullptr;
+      float* dst = have_n ? n.z + static_cast<size_t>(lo - n.lo) * lat : nullptr;
+      if (have_o && have_n) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+      } else if (have_o) {
+        NK(ncclSend(src, bytes, ncclUint8, n.rank, c->comm, c->stream));
+      } else if (have_n) {
+        NK(ncclRecv(dst, bytes, ncclUint8, o.rank, c->comm, c->stream));
+      }
+    }
+  if (nccl_open) NK(ncclGroupEnd());
+  CK(cudaStreamSynchronize(c->stream));
+  for (Shard& o : q->shards)
+    if (o.z) cudaFree(o.z);
+  q->shards = ns;
+  q->ranks.assign(ranks, ranks + nranks);
+  q->state = q->step_idx >= q->steps ? GS_REQ_DONE : GS_REQ_PLACED;
+  return GS_OK;
+}
+
+int gs_query(gs_ctx* c, gs_req id, int* steps_done, int* steps_total, int* nranks, int* ranks_out, int* state,
+             int* n_tokens) {
+  if (!c) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->table_mu);
+  auto it = c->reqs.find(id);
+  if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request");
+  Request* q = it->second.get();
+  if (steps_done) *steps_done = q->step_idx;
+  if (steps_total) *steps_total = q->steps;
+  if (nranks) *nranks = static_cast<int>(q->ranks.size());
+  if (ranks_out)
+    for (size_t i = 0; i < q->ranks.size(); ++i) ranks_out[i] = q->ranks[i];
+  if (state) *state = q->state;
+  if (n_tokens) *n_tokens = q->n;
+  return GS_OK;
+}
+
+int gs_read_latent(gs_ctx* c, gs_req id, float* host, size_t nfloats) {
+  if (!c || !host) return GS_EINVAL;
+  Request* q = find_req(c, id);
+  if (!q) return fail(c, GS_EINVAL, "unknown request");
+  if (q->state == GS_REQ_RUNNING) return fail(c, GS_ESTATE, "request is running");
+  const int lat = c->models[q->model]->desc.lat;
+  if (nfloats != static_cast<size_t>(q->n) * lat) return fail(c, GS_EINVAL, "latent has %d x %d floats", q->n, lat);
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  for (const Shard& s : q->shards)
+    if (s.z && s.hi > s.lo)
+      CK(cudaMemcpy(host + static_cast<size_t>(s.lo) * lat, s.z, static_cast<size_t>(s.hi - s.lo) * lat * 4,
+                    cudaMemcpyDeviceToHost));
+  return GS_OK;
+}
+
+int gs_release(gs_ctx* c, gs_req id) {
+  if (!c) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->table_mu);
+  auto it = c->reqs.find(id);
+  if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request");
+  if (it->second->state == GS_REQ_RUNNING) return fail(c, GS_ESTATE, "request is running");
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& s : it->second->shards)
+    if (s.z) cudaFree(s.z);
+  c->reqs.erase(it);
+  return GS_OK;
+}
+
+int gs_profile(gs_ctx* c, int enable, int reset) {
+  if (!c) return GS_EINVAL;
+  c->prof = enable != 0;
+  if (reset) {
+    c->prof_tab.clear();
+    c->launches = 0;
+  }
+  return GS_OK;
+}
+
+int gs_stats(gs_ctx* c, char* json, size_t len) {
+  if (!c || !json || len == 0) return GS_EINVAL;
+  std::string s = "{";
+  for (auto& kv : c->prof_tab) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "\"%s\": {\"ms\": %.6f, \"n\": %lld}, ", kv.first.c_str(), kv.second.ms, kv.second.n);
+    s += buf;
+  }
+  char buf[64];
+  snprintf(buf, sizeof buf, "\"launches\": %lld}", c->launches);
+  s += buf;
+  if (s.size() + 1 > len) return fail(c, GS_EINVAL, "stats buffer too small (%zu)", s.size() + 1);
+  memcpy(json, s.c_str(), s.size() + 1);
+  return GS_OK;
+}
+
+int gs_stream(gs_ctx* c, int rank, void** stream_out) {
+  if (!c || !stream_out) return GS_EINVAL;
+  if (local_index(c, rank) < 0) return fail(c, GS_EINVAL, "rank %d not owned by this process", rank);
+  *stream_out = c->stream;
+  return GS_OK;
+}
+
+// ------------------------------------------------------------------ debug entry points
+int gs_debug_gemm(gs_ctx* c, int e, int M, int N, int K, const void* A, const void* W, const void* bias, void* out,
+                  const float* gate_a, const float* gate_b, int gate_b_stride, const int* row_req,
+                  const float* dsig_host) {
+  if (!c) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  EpiParams ep{};
+  ep.out = out;
+  ep.ldo = N;
+  ep.bias = static_cast<const bf16*>(bias);
+  ep.gate_a = gate_a;
+  ep.gate_b = gate_b;
+  ep.gate_b_stride = gate_b_stride;
+  ep.row_req = row_req;
+  if (dsig_host)
+    for (int i = 0; i < 8; ++i) ep.dsig[i] = dsig_host[i];
+  cudaError_t err = gemm_bf16_tc(e, M, N, K, A, K, W, K, ep, c->num_sms, c->stream);
+  if (err != cudaSuccess) return fail(c, err == cudaErrorInvalidValue ? GS_EINVAL : GS_ECUDA, "gemm: %s", cudaGetErrorString(err));
+  CK(cudaStreamSynchronize(c->stream));
+  return GS_OK;
+}
+
+int gs_debug_attention(gs_ctx* c, const void* q, const void* k, const void* v, void* o, int heads, int d, int q_rs,
+                       int kv_rs, int o_rs, const int* seq_off, const int* seq_len, int nreq) {
+  if (!c || !seq_off || !seq_len) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  cudaError_t err = attention_tc(q, k, v, o, heads, d, q_rs, kv_rs, o_rs, seq_off, seq_len, nreq, c->num_sms, c->stream);
+  if (err != cudaSuccess) return fail(c, err == cudaErrorInvalidValue ? GS_EINVAL : GS_ECUDA, "attention: %s", cudaGetErrorString(err));
+  CK(cudaStreamSynchronize(c->stream));
+  return GS_OK;
+}
+
+int gs_debug_time_embed(gs_ctx* c, int model, int nreq, const float* t, float* e0, float* e) {
+  if (!c || !t || !e0 || !e) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
+  if (nreq < 1 || nreq > MAX_BATCH) return fail(c, GS_EINVAL, "nreq");
+  Model* m = c->models[model].get();
+  RankArena& A = c->local[0];
+  const int D = m->desc.dim;
+  RET(ensure(c, A.e0, MAX_BATCH * D * 4));
+  RET(ensure(c, A.e, MAX_BATCH * 6 * D * 4));
+  RET(ensure(c, A.temb, (MAX_BATCH * m->desc.freq_dim + 2 * MAX_BATCH * D) * 4));
+  TimeEmbedW tw{m->w_t1, m->b_t1, m->w_t2, m->b_t2, m->w_tp, m->b_tp, D, m->desc.freq_dim};
+  CK(time_embed(tw, nreq, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), c->stream));
+  CK(cudaMemcpyAsync(e0, A.e0.p, static_cast<size_t>(nreq) * D * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(e, A.e.p, static_cast<size_t>(nreq) * 6 * D * 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return GS_OK;
+}
+
+int gs_debug_block(gs_ctx* c, int model, int layer, float* x, int nreq, const int* grids, const int* tok_lo,
+                   const int* n_rows, const float* t) {
+  if (!c || !x || !grids || !tok_lo || !n_rows || !t) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->run_mu);
+  CK(cudaSetDevice(c->device));
+  if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
+  Model* m = c->models[model].get();
+  if (layer < 0 || layer >= m->desc.layers) return fail(c, GS_EINVAL, "bad layer");
+  if (nreq < 1 || nreq > MAX_BATCH) return fail(c, GS_EINVAL, "nreq");
+  // A p = 1 plan over segments [tok_lo, tok_lo + n_rows) of each request; attention runs over
+  // the segment only (pass full requests, tok_lo = 0, for the block of the method).
+  std::vector<std::unique_ptr<Request>> own(nreq);
+  std::vector<Request*> reqs(nreq);
+  for (int r = 0; r < nreq; ++r) {
+    own[r] = std::make_unique<Request>();
+    for (int a = 0; a < 3; ++a) own[r]->grid[a] = grids[3 * r + a];
+    own[r]->n = n_rows[r];
+    own[r]->steps = 1;
+    reqs[r] = own[r].get();
+  }
+  int rank0 = c->local[0].rank;
+  Plan P;
+  make_plan(P, m, reqs, &rank0, 1);
+  RankArena& A = c->local[0];
+  RET(prepare_rank(c, P, 0, A));
+  // row_tok = tok_lo + local index
+  {
+    std::vector<int> rt(P.rows[0]);
+    for (int r = 0; r < nreq; ++r)
+      for (int i = 0; i < n_rows[r]; ++i) rt[P.loff[0][r] + i] = tok_lo[r] + i;
+    CK(cudaMemcpyAsync(A.row_tok.p, rt.data(), rt.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  const int D = m->desc.dim;
+  TimeEmbedW tw{m->w_t1, m->b_t1, m->w_t2, m->b_t2, m->w_tp, m->b_tp, D, m->desc.freq_dim};
+  CK(time_embed(tw, nreq, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), c->stream));
+  const size_t xbytes = static_cast<size_t>(P.rows[0]) * D * 4;
+  CK(cudaMemcpyAsync(A.x.p, x, xbytes, cudaMemcpyHostToDevice, c->stream));
+  RET(block_pre(c, P, 0, A, layer));
+  RET(block_attn(c, P, 0, A));
+  RET(block_post(c, P, 0, A, layer));
+  CK(cudaMemcpyAsync(x, A.x.p, xbytes, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  prof_flush(c);
+  return GS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Host-side launchers of the sm_100a kernels (internal to libgs.so; not part of the C-ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gs {
+
+// ----------------------------------------------------------------- GEMM (gemm.cu)
+// C[M,N] = A[M,K] (bf16, row-major, K contiguous) x W[N,K]^T (bf16, row-major) + epilogue.
+// Requirements: K % 64 == 0, N % 32 == 0, lda/ldw multiples of 8 elements, 16-B aligned bases.
+enum EpiKind : int {
+  EPI_BF16 = 0,        // out bf16 [M, ldo] = acc + bias
+  EPI_GELU_BF16 = 1,   // out bf16 = GELU_tanh(acc + bias)
+  EPI_F32 = 2,         // out fp32 = acc + bias
+  EPI_RESID_F32 = 3,   // out fp32 += (gate_a[n] + gate_b[req(m)*gate_b_stride + n]) * (acc + bias)
+  EPI_EULER_F32 = 4,   // out fp32 += dsig[req(m)] * (acc + bias)
+};
+
+struct EpiParams {
+  void* out;
+  int ldo;                    // elements
+  const __nv_bfloat16* bias;  // [N] or null
+  const float* gate_a;        // [N]
+  const float* gate_b;        // [B, stride]
+  int gate_b_stride;
+  const int* row_req;         // [M] request index of each row
+  float dsig[8];              // per-request sigma_{i+1} - sigma_i
+};
+
+// Returns cudaError_t; builds the TMA descriptors on the host.
+cudaError_t gemm_bf16_tc(int epi, int M, int N, int K, const void* A, int lda, const void* W,
+                         int ldw, const EpiParams& ep, int num_sms, cudaStream_t stream);
+
+// ----------------------------------------------------------------- attention (attention.cu)
+// O[r, h, :] = softmax(Q_h K_h^T / sqrt(d)) V_h over each request's own rows (block-diagonal).
+// Q/K/V/O: bf16 [rows, heads, d] with row strides (elements) *_rs; seq_off/seq_len per request
+// (host arrays, nreq <= 64).
+cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
+                         int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
+                         int nreq, int num_sms, cudaStream_t stream);
+
+// ----------------------------------------------------------------- element-wise (elementwise.cu)
+// out[m, :] = LN(x[m, :]) * (1 + sc) + sh, sh = sh_a + sh_b[req(m)*b_stride], same for sc.
+cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const float* sh_b,
+                        const float* sc_a, const float* sc_b, int b_stride, const int* row_req,
+                        float eps, __nv_bfloat16* out, cudaStream_t stream);
+
+// qk-RMSNorm over D, 3-axis RoPE, and pack of q/k/v into the per-destination send layout
+// [dest j][row][H_j][d] (dest_off[j] = element offset of chunk j, heads split contiguously).
+struct RopeParams {
+  const int* row_req;    // [M]
+  const int* row_tok;    // [M] request-local token index
+  const int* req_grid;   // [B * 3] (F_t, H_t, W_t)
+  const float2* cs_tab;  // [P_MAX][d/2] (cos, sin) of pos * freq(slot)
+  const int* slot_axis;  // [d/2] axis (0 = f, 1 = h, 2 = w) of each pair slot
+  int p_max;
+};
+struct PackParams {
+  int ndest;
+  int head_off[9];       // head_off[j]..head_off[j+1]: heads of destination j
+  long long dest_off[8]; // element offset of destination chunk j in each send buffer
+  int rows;              // M (local rows; chunk j is [rows][H_j][d])
+};
+cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
+                              const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,
+                              const RopeParams& rp, const PackParams& pk, __nv_bfloat16* q_out,
+                              __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream);
+
+// Time embedding for B requests: e0 = W_t2 SiLU(W_t1 s(t) + b) + b, e = W_tp SiLU(e0) + b.
+struct TimeEmbedW {
+  const __nv_bfloat16 *w_t1, *b_t1, *w_t2, *b_t2, *w_tp, *b_tp;
+  int D, freq_dim;
+};
+cudaError_t time_embed(const TimeEmbedW& w, int B, const float* t_host /*B*/, float* scratch,
+                       float* e0, float* e, cudaStream_t stream);
+
+cudaError_t f32_to_bf16(const float* in, __nv_bfloat16* out, long long n, cudaStream_t stream);
+
+// ----------------------------------------------------------------- RNG (rng.cu)
+// Counter RNG of DESIGN.md "Input recipe" (independent re-implementation of synth/rng.py).
+enum RngKind : int { RNG_BF16_SCALED = 0, RNG_BF16_GAIN = 1, RNG_F32_SCALED = 2 };
+cudaError_t rng_fill(void* out, long long n, uint64_t seed, uint32_t tensor_id, int kind,
+                     float scale, cudaStream_t stream);
+// z[i, c] for tokens [tok_lo, tok_lo + ntok) of a request's [n, 64] noise latent.
+cudaError_t rng_noise(float* out, long long tok_lo, long long ntok, int channels, uint64_t seed,
+                      cudaStream_t stream);
+
+}  // namespace gs

@@ -1,0 +1,102 @@
+// Internal runtime structures of libgs.so (context, models, requests, per-rank arenas).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <atomic>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/gs.h"
+#include "kernels.h"
+
+namespace gs {
+
+using bf16 = __nv_bfloat16;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+struct BlockW {
+  bf16 *w_qkv, *b_qkv, *g_q, *g_k, *w_o, *b_o, *w_1, *b_1, *w_2, *b_2;
+  float* mod;  // [6, D]
+};
+
+struct Model {
+  gs_model_desc desc{};
+  int hd = 0;  // head dim
+  std::vector<BlockW> blocks;
+  bf16 *w_pe, *b_pe, *w_t1, *b_t1, *w_t2, *b_t2, *w_tp, *b_tp, *w_head, *b_head;
+  float* mod_head;     // [2, D]
+  float2* cs_tab;      // [p_max, hd/2]
+  int* slot_axis;      // [hd/2]
+  int p_max = 1024;
+  std::vector<void*> allocs;
+};
+
+struct Shard {
+  int rank = -1;
+  int lo = 0, hi = 0;  // token range
+  float* z = nullptr;  // device [hi-lo, lat] fp32 if this process owns `rank`
+};
+
+struct Request {
+  gs_req id = 0;
+  int model = 0;
+  int grid[3] = {1, 1, 1};
+  int n = 0;
+  int steps = 0;
+  int step_idx = 0;
+  int state = GS_REQ_PLACED;
+  std::vector<int> ranks;
+  std::vector<Shard> shards;  // one per SP position
+  std::atomic<int> preempt{0};
+};
+
+// Per-local-rank arena (grow-only device buffers).
+struct RankArena {
+  int rank = 0;
+  DevBuf x, a, qkv, qs, ks, vs, qr, kr, vr, o, orecv, ostage, h, zpack, zb, e0, e, temb, row_req,
+      row_tok, req_grid;
+};
+
+struct Prof {
+  double ms = 0;
+  long long n = 0;
+};
+
+}  // namespace gs
+
+struct gs_ctx {
+  int device = 0;
+  int world = 1;
+  int my_rank = 0;   // real mode
+  bool emulated = false;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  std::vector<gs::RankArena> local;  // emulated: world entries; real: 1 entry
+  std::vector<std::unique_ptr<gs::Model>> models;
+  std::map<gs_req, std::unique_ptr<gs::Request>> reqs;
+  gs_req next_req = 1;
+  std::string err;
+  std::mutex table_mu;  // guards reqs
+  std::mutex run_mu;    // one run / resume at a time
+  // measurement
+  bool prof = false;
+  std::map<std::string, gs::Prof> prof_tab;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+  std::vector<cudaEvent_t> event_pool;
+  long long launches = 0;
+  // pinned scratch for preemption agreement
+  int* h_flag = nullptr;
+  int* d_flag = nullptr;
+};

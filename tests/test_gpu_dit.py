@@ -1,0 +1,220 @@
+"""Block / step parity against the fp64 oracle (rung T3) and GPU-vs-GPU bit-exactness (rung T4):
+SP degree 1/2/4/8, batch composition, preempt -> re-shard -> resume.  Multi-rank cases use the
+emulated context (W virtual ranks on the one GPU, exchanges as device copies; same kernels and
+shard shapes as the NCCL path)."""
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import dit
+from synth import models as sm
+from synth import rng
+from tests.gpu_util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2  # BASELINE.json north_star: relative L2 vs the CPU oracle (bf16 storage, fp32 acc)
+
+
+@pytest.fixture(scope="module")
+def gs():
+    import paper_2604_04335_b200 as m
+    m.load()
+    return m
+
+
+def _mk(ctx, shape):
+    return ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed)
+
+
+def _block_case(ctx, shape, grids, ts, seed=11):
+    """x_in random fp32 per request; returns (x_in, gpu_out, oracle_out)."""
+    mid = _mk(ctx, shape)
+    g = np.random.default_rng(seed)
+    ns = [int(np.prod(gr)) for gr in grids]
+    x = g.standard_normal((sum(ns), shape.dim)).astype(np.float32)
+    out = ctx.debug_block(mid, 0, x, grids, [0] * len(ns), ns, ts)
+    glob = sm.as_f64(sm.global_params(shape))
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    e_req = np.stack([dit.time_embedding(np.float64(np.float32(t)), glob)[1] for t in ts])
+    offs = np.cumsum([0] + ns[:-1])
+    ref = dit.dit_block(x.astype(np.float64), blk, e_req,
+                        [(int(o), n, gr) for o, n, gr in zip(offs, ns, grids)], shape.heads)
+    return x, out, ref
+
+
+def test_block_config1_tiny(gs):
+    ctx = gs.Context(device=0)
+    x, out, ref = _block_case(ctx, sm.TINY, [sm.token_grid(256, 256)], [860.5])
+    err = rel_l2(out.astype(np.float64) - x, ref - x)
+    ctx.close()
+    assert err < TOL, err
+
+
+def test_block_config2_wan13b_varlen(gs):
+    # config 2b: varlen 4-image batch {1024^2, 1280x768, 768x1280, 1152x896}, Wan-1.3B block
+    grids = [sm.token_grid(1024, 1024), sm.token_grid(1280, 768), sm.token_grid(768, 1280),
+             sm.token_grid(1152, 896)]
+    ctx = gs.Context(device=0)
+    x, out, ref = _block_case(ctx, sm.WAN_1_3B.with_layers(1), grids, [999.0, 800.0, 500.0, 37.5])
+    ctx.close()
+    offs = np.cumsum([0] + [int(np.prod(g)) for g in grids])
+    for a, b in zip(offs[:-1], offs[1:]):
+        err = rel_l2(out[a:b].astype(np.float64) - x[a:b], ref[a:b] - x[a:b])
+        assert err < TOL, err
+
+
+def test_step_config1_tiny_12_layers(gs):
+    shape = sm.TINY.with_layers(12)
+    ctx = gs.Context(device=0)
+    mid = _mk(ctx, shape)
+    req = ctx.submit(mid, 256, 256, 1, 50, 1000, [0])
+    z0 = ctx.read_latent(req)
+    ctx.run_steps([req], [0], 1)
+    ctx.run_steps([req], [0], 1)
+    z2 = ctx.read_latent(req)
+    ctx.close()
+    glob = sm.as_f64(sm.global_params(shape))
+    blocks = [sm.as_f64(sm.block_params(shape, l)) for l in range(12)]
+    ref = dit.dit_steps([z0.astype(np.float64)], [(1, 16, 16)], [0], 50, 2, glob, blocks,
+                        shape.heads)[0]
+    err = rel_l2(z2.astype(np.float64) - z0, ref - z0)
+    assert err < TOL, err
+
+
+def test_step_batched_varlen_images_match_oracle(gs):
+    shape = sm.TINY.with_layers(2)
+    ctx = gs.Context(device=0)
+    mid = _mk(ctx, shape)
+    sizes = [(256, 256), (512, 256), (256, 384)]
+    reqs = [ctx.submit(mid, w, h, 1, 30, 1000 + i, [0]) for i, (w, h) in enumerate(sizes)]
+    # put the requests at different timesteps first
+    ctx.run_steps([reqs[1]], [0], 3)
+    z0 = [ctx.read_latent(r) for r in reqs]
+    ctx.run_steps(reqs, [0], 1)
+    z1 = [ctx.read_latent(r) for r in reqs]
+    ctx.close()
+    glob = sm.as_f64(sm.global_params(shape))
+    blocks = [sm.as_f64(sm.block_params(shape, l)) for l in range(2)]
+    grids = [sm.token_grid(w, h) for w, h in sizes]
+    ref = dit.dit_steps([z.astype(np.float64) for z in z0], grids, [0, 3, 0], 30, 1, glob, blocks,
+                        shape.heads)
+    for a, b, r in zip(z0, z1, ref):
+        assert rel_l2(b.astype(np.float64) - a, r - a) < TOL
+
+
+# ----------------------------------------------------------------------------- T4 bit-exactness
+def _run_sp(gs, shape, width, height, frames, p, k, steps=50, seed=1000):
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    mid = _mk(ctx, shape)
+    ranks = list(range(p))
+    req = ctx.submit(mid, width, height, frames, steps, seed, ranks)
+    assert ctx.run_steps([req], ranks, k) == k
+    z = ctx.read_latent(req)
+    ctx.close()
+    return z
+
+
+@pytest.mark.parametrize("shape,w,h,f", [(sm.TINY.with_layers(2), 256, 256, 1),
+                                         (sm.WAN_1_3B.with_layers(1), 416, 240, 5)])
+def test_bit_exact_across_sp_degree(gs, shape, w, h, f):
+    ref = _run_sp(gs, shape, w, h, f, 1, 2)
+    for p in (2, 4, 8):
+        z = _run_sp(gs, shape, w, h, f, p, 2)
+        assert np.array_equal(z.view(np.uint32), ref.view(np.uint32)), f"p={p}"
+
+
+def test_bit_exact_across_batch_composition(gs):
+    shape = sm.TINY.with_layers(2)
+    ctx = gs.Context(device=0)
+    mid = _mk(ctx, shape)
+    alone = ctx.submit(mid, 256, 256, 1, 50, 1000, [0])
+    ctx.run_steps([alone], [0], 2)
+    za = ctx.read_latent(alone)
+    a = ctx.submit(mid, 512, 256, 1, 50, 1001, [0])
+    b = ctx.submit(mid, 256, 256, 1, 50, 1000, [0])
+    c = ctx.submit(mid, 384, 384, 1, 50, 1002, [0])
+    ctx.run_steps([a, b, c], [0], 2)
+    zb = ctx.read_latent(b)
+    ctx.close()
+    assert np.array_equal(za.view(np.uint32), zb.view(np.uint32))
+
+
+def test_preempt_reshard_resume_bit_exact(gs):
+    shape = sm.WAN_1_3B.with_layers(1)
+    w, h, f = 416, 240, 5
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    mid = _mk(ctx, shape)
+    straight = ctx.submit(mid, w, h, f, 50, 1000, [0, 1, 2, 3])
+    ctx.run_steps([straight], [0, 1, 2, 3], 3)
+    z_ref = ctx.read_latent(straight)
+
+    req = ctx.submit(mid, w, h, f, 50, 1000, [0, 1, 2, 3])
+    assert ctx.run_steps([req], [0, 1, 2, 3], 1) == 1
+    assert ctx.preempt(req) == 1
+    assert ctx.query(req)["state"] == gs.REQ_PAUSED
+    with pytest.raises(gs.GsError):
+        ctx.run_steps([req], [0, 1, 2, 3], 1)          # paused: contract violation
+    before = ctx.read_latent(req)
+    ctx.resume(req, [6, 7])                             # SP 4 -> 2 on a different GPU set
+    np.testing.assert_array_equal(ctx.read_latent(req), before)   # re-shard is a pure copy
+    assert ctx.run_steps([req], [6, 7], 1) == 1
+    ctx.resume(req, [0, 2, 4, 5, 1, 3, 6, 7])           # SP 2 -> 8, permuted set
+    assert ctx.run_steps([req], [0, 2, 4, 5, 1, 3, 6, 7], 1) == 1
+    z = ctx.read_latent(req)
+    q = ctx.query(req)
+    ctx.close()
+    assert q["steps_done"] == 3
+    assert np.array_equal(z.view(np.uint32), z_ref.view(np.uint32))
+
+
+def test_preempt_from_another_thread_stops_at_step_boundary(gs):
+    shape = sm.TINY.with_layers(12)
+    ctx = gs.Context(device=0)
+    mid = _mk(ctx, shape)
+    req = ctx.submit(mid, 512, 512, 1, 1000, 1000, [0])
+    done = {}
+
+    def run():
+        done["n"] = ctx.run_steps([req], [0], 900)
+
+    th = threading.Thread(target=run)
+    th.start()
+    import time
+    time.sleep(0.3)
+    ctx.preempt(req)
+    th.join()
+    q = ctx.query(req)
+    assert q["state"] == gs.REQ_PAUSED
+    assert q["steps_done"] == done["n"] < 900
+    # progress is never lost and the run continues exactly from the boundary
+    ctx.resume(req, [0])
+    ctx.run_steps([req], [0], 900 - done["n"])
+    z = ctx.read_latent(req)
+    ref = ctx.submit(mid, 512, 512, 1, 1000, 1000, [0])
+    ctx.run_steps([ref], [0], 900)
+    zr = ctx.read_latent(ref)
+    ctx.close()
+    assert np.array_equal(z.view(np.uint32), zr.view(np.uint32))
+
+
+def test_contract_errors(gs):
+    ctx = gs.Context(device=0, world_size=4, emulated=True)
+    mid = _mk(ctx, sm.TINY)
+    with pytest.raises(gs.GsError) as e:
+        ctx.submit(mid, 250, 256, 1, 50, 1, [0])
+    assert e.value.code == gs.GS_EINVAL
+    with pytest.raises(gs.GsError):
+        ctx.submit(mid, 256, 256, 1, 50, 1, [0, 1, 2])       # p = 3
+    with pytest.raises(gs.GsError):
+        ctx.submit(mid, 256, 256, 1, 50, 1, [1, 1])          # duplicate GPU
+    r = ctx.submit(mid, 256, 256, 1, 2, 1, [0, 1])
+    with pytest.raises(gs.GsError) as e:
+        ctx.run_steps([r], [0], 1)                            # wrong placement
+    assert e.value.code == gs.GS_ESTATE
+    with pytest.raises(gs.GsError):
+        ctx.run_steps([r], [0, 1], 3)                         # k > remaining
+    assert ctx.run_steps([r], [0, 1], 2) == 2
+    assert ctx.query(r)["state"] == gs.REQ_DONE
+    ctx.close()
