@@ -1,0 +1,393 @@
+"""bench.py — DiT denoising-step benchmark of the GenServe hot path on B200.
+
+Contract (task statement / DESIGN.md "Measurement"):
+  python bench.py --gpus N --steps K --warmup W [--workload W] [--impl reference]
+prints ONE JSON line on rank 0.  Under torchrun (N > 1) every rank owns one GPU; the request is
+token-sharded over all N ranks (Ulysses SP degree p = N) and the exchanges run over NCCL.
+
+A "step" is one whole pass of the hot path: time embedding, patch
+embed, L DiT blocks (LN+mod, QKV GEMM, qk-RMSNorm+RoPE+pack, a2a, flash attention, a2a, O GEMM +
+gated residual, LN+mod, MLP up+GELU, MLP down + gated residual), head + Euler update, for one
+batch of synthetic input.  Workloads (BASELINE.json configs):
+  t2v720  (default) config 4: 720x1280, 81 frames -> 75,600 tokens, Wan-14B-shaped (D 5120,
+          40x128 heads, F 13824, L 40), one request at SP = N  ("scaling": "strong")
+  t2v480  config 3: 480x832, 81 frames -> 32,760 tokens, Wan-1.3B-shaped, SP = N (strong)
+  t2i1024 config 2: 4 x 1024^2 images (4 x 4096 tokens), Wan-1.3B-shaped, SP = 1 per rank;
+          N > 1 runs N independent image batches (replicas, "scaling": "weak")
+The metric is BASELINE.json's "DiT step ms & attn TFLOPS (% BF16 peak)": `value` is the DiT
+step time (ms, device-timed with CUDA events on the context's stream, max over ranks);
+attention TFLOPS and its fraction of the measured BF16 peak ride in `roofline`.
+Inputs are far larger than L2 (weights 19.7 GB / 2.6 GB, activations > 1 GB), so no explicit
+L2 flush is needed between timed steps ("l2": "inputs larger than L2" in config).
+
+`--impl reference` is the base contract's reference arm for this tier: the fp64 CPU oracle
+(oracle/dit.py) timed as it stands on the host cores on a bounded sample of the same workload.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_2604_04335_b200 import costmodel  # noqa: E402  (work accounting, no method arithmetic)
+from synth import models as sm  # noqa: E402
+
+METRIC = "DiT step ms & attn TFLOPS (% BF16 peak) at SP=1/2/4/8, 720p T2V + 1024px T2I"
+
+WORKLOADS = {
+    # name: (model shape, [(width, height, frames)], sp_over_ranks)
+    "t2v720": (sm.WAN_14B, [(1280, 720, 81)], True),
+    "t2v480": (sm.WAN_1_3B, [(832, 480, 81)], True),
+    "t2i1024": (sm.WAN_1_3B, [(1024, 1024, 1)] * 4, False),
+}
+CONFIG_NAME = {
+    "t2v720": "config4: 720x1280 81f T2V (75600 tok), Wan-14B-shaped DiT step",
+    "t2v480": "config3: 480x832 81f T2V (32760 tok), Wan-1.3B-shaped DiT step",
+    "t2i1024": "config2: 4 x 1024px T2I (4 x 4096 tok) batch, Wan-1.3B-shaped DiT step",
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm": p["hbm_gbs"], "bf16": p["bf16_tflops"],
+                "bf16_sustained": p["bf16_tflops_sustained"], "src": "measured"}
+    except Exception:
+        # /opt/skills/guides/B200_PROFILING.md fallback figures
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "src": "fallback"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sms, maxs, reasons = [], [], set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sms.append(float(f[1]))
+                maxs.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(self.REASONS, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sms:
+            return None
+        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": max(maxs),
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ----------------------------------------------------------------------------- oracle sample
+def oracle_sample(workload, reps=1, budget_tokens=None):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: one full DiT
+    block of layer 0 on a single-latent-frame request of the workload's resolution (fewer
+    tokens, same model dims), then extrapolate to one full step by the paper's FLOP model
+    (PAPER.md Tab. arithmetic_intensity; costmodel.py).  Returns (ms_per_full_step, info)."""
+    from oracle import dit
+    shape, reqs, _ = WORKLOADS[workload]
+    w, h, _f = reqs[0]
+    grid = sm.token_grid(w, h, 1)
+    if budget_tokens is not None and grid[1] * grid[2] > budget_tokens:
+        rows = max(1, budget_tokens // grid[2])
+        grid = (1, rows, grid[2])
+    n = grid[0] * grid[1] * grid[2]
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    g = np.random.default_rng(5)
+    x = g.standard_normal((n, shape.dim))
+    e_req = g.uniform(-0.5, 0.5, (1, 6, shape.dim))
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        dit.dit_block(x, blk, e_req, [(0, n, grid)], shape.heads)
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    f_sample = costmodel.flops_per_block([n], shape.dim, shape.ffn)
+    full_seqs = [sm.token_grid(*r) for r in reqs]
+    full_n = [a * b * c for a, b, c in full_seqs]
+    f_step = shape.layers * costmodel.flops_per_block(full_n, shape.dim, shape.ffn)
+    ms_step = t * 1e3 * f_step / f_sample
+    info = {"sample": (f"oracle dit_block (fp64 numpy) layer 0 of {shape.name} on a {grid} "
+                       f"token grid ({n} tokens, {f_sample / 1e9:.1f} GFLOP) in {t:.2f} s; "
+                       f"extrapolated by FLOPs to one full {shape.layers}-layer step of "
+                       f"{sum(full_n)} tokens ({f_step / 1e12:.1f} TFLOP)"),
+            "sample_s": t, "gflops_fp64": f_sample / t / 1e9}
+    return ms_step, info
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    times, info = [], None
+    for i in range(args.warmup + args.steps):
+        ms, info = oracle_sample(args.workload, reps=1, budget_tokens=args.ref_tokens)
+        if i >= args.warmup:
+            times.append(ms)
+    v = float(np.mean(times))
+    shape, reqs, _ = WORKLOADS[args.workload]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": v, "higher_is_better": False,
+            "scaling": "strong" if WORKLOADS[args.workload][2] else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64)",
+            "config": {"workload": CONFIG_NAME[args.workload], "sp": 1},
+            "cpu_baseline": {"value": v, "unit": "ms", "cores": host_cores(), "kind": "oracle",
+                             "sample": info["sample"]},
+            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def attn_flops_per_launch(shape, seqlens, heads_local):
+    return 4 * shape.head_dim * heads_local * sum(n * n for n in seqlens)
+
+
+def head_split(H, p, j):
+    return (j + 1) * (H // p) + min(j + 1, H % p) - (j * (H // p) + min(j, H % p))
+
+
+def load_traffic(workload, p):
+    """dram bytes per attention launch from a committed ncu --set full capture, if any."""
+    path = os.path.join(ROOT, "profiles", "attention_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(f"{workload}_sp{p}")
+    except Exception:
+        return None
+
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import paper_2604_04335_b200 as gs
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        uid = [gs.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = gs.Context(device=local_rank, world_size=world, rank=rank, nccl_uid=uid[0])
+    else:
+        torch.cuda.set_device(local_rank)
+        ctx = gs.Context(device=local_rank)
+
+    shape, reqs_spec, sp_over_ranks = WORKLOADS[args.workload]
+    ranks = list(range(world)) if sp_over_ranks else [rank]
+    p = len(ranks)
+    if not sp_over_ranks and world > 1:
+        # replicas: every rank owns its own single-rank placement (images use <= 1 GPU)
+        pass
+    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed)
+    total_steps = max(50, args.warmup + args.steps + 1)
+
+    def submit_all(init=None):
+        out = []
+        for r, (w, h, f) in enumerate(reqs_spec):
+            lat = None if init is None else init[r]
+            out.append(ctx.submit(mid, w, h, f, total_steps, 1000 + r, ranks, init_latent=lat))
+        return out
+
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(rank))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # -------------------------------------------------------------- device-timed steps
+    reqs = submit_all()
+    if args.warmup:
+        ctx.run_steps(reqs, ranks, args.warmup)
+    ctx.profile(True, True)
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    barrier()
+    if clocks:
+        clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    done = ctx.run_steps(reqs, ranks, args.steps)
+    ev1.record(stream)
+    barrier()
+    clk = clocks.stop() if clocks else None
+    assert done == args.steps, f"ran {done} of {args.steps} steps"
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_step = ms_total / args.steps
+    st = ctx.stats()
+    ctx.profile(False, False)
+    for q in reqs:
+        ctx.release(q)
+
+    # -------------------------------------------------------------- end to end (host buffers)
+    seqlens = [int(np.prod(sm.token_grid(*r))) for r in reqs_spec]
+    host_z = [np.ascontiguousarray(np.random.default_rng(40 + i).standard_normal((n, 64)),
+                                   dtype=np.float32) for i, n in enumerate(seqlens)]
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    e2e_ms = []
+    out = None
+    for _ in range(e2e_steps):
+        barrier()
+        t0 = time.perf_counter()
+        rq = submit_all(host_z)                       # H2D of the step's input latents
+        ctx.run_steps(rq, ranks, 1)
+        out = [ctx.read_latent(q, n) for q, n in zip(rq, seqlens)]   # D2H of the result
+        for q in rq:
+            ctx.release(q)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_v = max_over_ranks(float(np.median(e2e_ms)))
+    lat_bytes = sum(seqlens) * 64 * 4
+    # each rank copies its own shard in and out
+    h2d = lat_bytes if not sp_over_ranks else lat_bytes  # whole-job bytes per step
+    assert out is not None and all(np.isfinite(o).all() for o in out)
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        ctx.close()
+        return
+
+    # -------------------------------------------------------------- roofline (attention)
+    pk = peaks()
+    H_loc = head_split(shape.heads, p, 0)  # rank 0 carries the most heads
+    attn = st.get("attention", {"ms": 0.0, "n": 0})
+    attn_avg_ms = attn["ms"] / max(attn["n"], 1)
+    af = attn_flops_per_launch(shape, seqlens, H_loc)
+    achieved = af / (attn_avg_ms * 1e-3) / 1e12 if attn_avg_ms > 0 else 0.0
+    peak = pk["bf16_sustained"]
+    traffic = load_traffic(args.workload, p)
+    gemm_ms = sum(v["ms"] for k, v in st.items() if isinstance(v, dict) and k.startswith("gemm"))
+    gemm_flops = shape.layers * costmodel.gemm_flops_per_block(sum(seqlens) / p, shape.dim, shape.ffn)
+    gemm_tflops = gemm_flops * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    step_flops = shape.layers * (costmodel.gemm_flops_per_block(sum(seqlens) / p, shape.dim, shape.ffn)
+                                 + af)
+    breakdown = {k: round(v["ms"] / args.steps, 3) for k, v in st.items() if isinstance(v, dict)}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        ms_cpu, info = oracle_sample(args.workload, reps=1, budget_tokens=args.ref_tokens)
+        cpu = {"value": ms_cpu, "unit": "ms", "cores": host_cores(), "kind": "oracle",
+               "sample": info["sample"], "gflops_fp64": round(info["gflops_fp64"], 2)}
+
+    line = {
+        "metric": METRIC, "value": round(ms_step, 3), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+        "higher_is_better": False, "scaling": "strong" if sp_over_ranks else "weak",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded splitmix64 latents, random-init weights of the shape)",
+        "config": {"workload": CONFIG_NAME[args.workload], "sp": p,
+                   "tokens": seqlens, "layers": shape.layers, "dim": shape.dim,
+                   "heads": shape.heads, "ffn": shape.ffn,
+                   "parallelism": f"ulysses_sp{p}" if sp_over_ranks else f"replicas{world}",
+                   "l2": "inputs larger than L2 (no flush)"},
+        "roofline": {"bound": "tensor", "kernel": "attention (attn_tc_kernel<128>)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_src": f"{pk['src']} bf16 sustained (kernel timed inside a long step)",
+                     "frac_of_burst": round(achieved / pk["bf16"], 4),
+                     "flops_per_launch": af, "avg_launch_ms": round(attn_avg_ms, 4)},
+        "attn_tflops": round(achieved, 1),
+        "gemm_tflops": round(gemm_tflops, 1),
+        "step_tflops": round(step_flops / (ms_step * 1e-3) / 1e12, 1),
+        "breakdown_ms_per_step": breakdown,
+        "gpu_launches": int(st.get("launches", 0)),
+        "e2e": {"value": round(e2e_v, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": lat_bytes, "steps": e2e_steps,
+                "how": "wall clock around gs_submit(host latent) + gs_run_steps(k=1) + "
+                       "gs_read_latent + gs_release"},
+        "clocks": clk,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="t2v720", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-tokens", type=int, default=1200,
+                    help="token budget of the oracle sample (bounded CPU time)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            sys.exit("bench.py --gpus N>1 must be launched under torchrun (one rank per GPU)")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_gpu(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()
