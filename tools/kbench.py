@@ -60,6 +60,7 @@ def main():
     ap.add_argument("--gemm", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--torch", action="store_true", help="also time torch SDPA / matmul yardsticks")
+    ap.add_argument("--only", default=None, help="substring filter on the case label")
     a = ap.parse_args()
     if not (a.attn or a.gemm):
         a.attn = a.gemm = True
@@ -67,6 +68,8 @@ def main():
     res = {}
     if a.attn:
         for label, seqs, H, d in ATTN:
+            if a.only and a.only not in label:
+                continue
             N = sum(seqs)
             q = torch.randn(N, H, d, device="cuda").to(torch.bfloat16)
             k = torch.randn(N, H, d, device="cuda").to(torch.bfloat16)
@@ -97,6 +100,8 @@ def main():
             del q, k, v, o
     if a.gemm:
         for label, M, N, K in GEMM:
+            if a.only and a.only not in label:
+                continue
             A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
             b = torch.zeros(N, device="cuda").to(torch.bfloat16)
