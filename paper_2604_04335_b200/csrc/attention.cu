@@ -20,13 +20,18 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
 #include "tma.h"
 
 namespace gs {
+// Development trace (GS_ATTN_TRACE=1): clock64 stamps of CTA (0,0) for the first 32 KV tiles.
+__device__ unsigned long long g_attn_trace[16 * 64];
 namespace {
+#define TRACE_EV(ev, w, j) \
+  if (TRACE && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 32) g_attn_trace[((ev) * 32 + (j)) * 2 + (w)] = clock64()
 
 constexpr int MAX_REQ = 64;
 constexpr int THREADS = 384;
@@ -42,15 +47,56 @@ template <int HD>
 struct Cfg {
   static constexpr int BOXES = HD / 64;                  // 64-element (128 B) column boxes
   static constexpr int TILE_BYTES = 128 * HD * 2;        // one 128-row tile
-  static constexpr int ST = HD == 128 ? 2 : 4;           // KV stages
+  // K ring deeper than V: a K slot frees after both S MMAs, a V slot only after both PV MMAs
+  static constexpr int KST = HD == 128 ? 3 : 4;          // K stages
+  static constexpr int VST = HD == 128 ? 2 : 4;          // V stages
   static constexpr int Q_OFF = 0;
-  static constexpr int KV_OFF = 2 * TILE_BYTES;
-  static constexpr int STAGE_BYTES = 2 * TILE_BYTES;     // K + V
-  static constexpr int BAR_OFF = KV_OFF + ST * STAGE_BYTES;
+  static constexpr int K_OFF = 2 * TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + KST * TILE_BYTES;
+  static constexpr int BAR_OFF = V_OFF + VST * TILE_BYTES;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
 };
 
-template <int HD>
+
+// P = exp2(S * scale - m) for the 128 columns of this thread's row, packed to bf16 pairs and
+// stored over the S columns [0, 64) in TMEM (P aliases S).  Returns the fp32 partial row sums.
+// FULL = false is the last (partial) KV tile of a request: masked columns get p = 0 exactly.
+template <int POLY8, bool FULL>
+__device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[128], float2 sc2, float2 nm2,
+                                                 int kv_valid, uint32_t tS) {
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int col = c * 32 + 2 * i;
+      const float2 x =
+          __ffma2_rn(make_float2(__uint_as_float(v[col]), __uint_as_float(v[col + 1])), sc2, nm2);
+      // exp2: MUFU for most pairs, FMA-pipe polynomial for POLY8 of every 8 pairs (reading 18)
+      float2 p;
+      if ((i & 7) >= 8 - POLY8) {
+        p = exp2_poly2(x);
+      } else {
+        p.x = ex2_approx(x.x);
+        p.y = ex2_approx(x.y);
+      }
+      if (!FULL) {
+        p.x = col < kv_valid ? p.x : 0.f;
+        p.y = col + 1 < kv_valid ? p.y : 0.f;
+      }
+      if (i & 1)
+        acc1 = __fadd2_rn(acc1, p);
+      else
+        acc0 = __fadd2_rn(acc0, p);
+      pk[i] = pack_bf16x2(p.x, p.y);
+    }
+    GS_TMEM_ST16(tS + c * 16, pk);
+  }
+  return __fadd2_rn(acc0, acc1);
+}
+
+template <int HD, int POLY8, bool TRACE = false>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
@@ -60,10 +106,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* q_full = bars;
-  uint64_t* kfull = bars + 1;
-  uint64_t* vfull = kfull + C::ST;
-  uint64_t* kvempty = vfull + C::ST;
-  uint64_t* sfull = kvempty + C::ST;  // [2]
+  uint64_t* kfull = bars + 1;           // [KST]
+  uint64_t* kempty = kfull + C::KST;    // [KST]
+  uint64_t* vfull = kempty + C::KST;    // [VST]
+  uint64_t* vempty = vfull + C::VST;    // [VST]
+  uint64_t* sfull = vempty + C::VST;    // [2]
   uint64_t* pfull = sfull + 2;        // [2]
   uint64_t* ofull = pfull + 2;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 2);
@@ -82,10 +129,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < C::ST; ++s) {
+    for (int s = 0; s < C::KST; ++s) {
       mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
       mbar_init(&vfull[s], 1);
-      mbar_init(&kvempty[s], 1);
+      mbar_init(&vempty[s], 1);
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&sfull[w], 1);
@@ -105,6 +155,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // register split: producer / MMA warpgroup shrinks, the two softmax warpgroups grow.  The CTA
+  // pool is 384 x 168 (launch allocation): 4 warps x 32 x (168 - 80) = 11264 freed >= 8 warps x
+  // 32 x (208 - 168) = 10240 requested (an unsatisfiable .inc would block forever).
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
   if (warp == 0) {
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
@@ -113,17 +168,19 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_3d(&tmQ, q_full, smem + C::Q_OFF + w * C::TILE_BYTES + b * 16384, b * 64, head,
                       q_row0 + w * 128);
       for (int j = 0; j < nkv; ++j) {
-        const int s = j % C::ST;
-        const uint32_t ph = (j / C::ST) & 1;
-        mbar_wait(&kvempty[s], ph ^ 1);
-        uint8_t* sk = smem + C::KV_OFF + s * C::STAGE_BYTES;
-        uint8_t* sv = sk + C::TILE_BYTES;
-        mbar_arrive_expect_tx(&kfull[s], C::TILE_BYTES);
+        const int ks = j % C::KST, vs = j % C::VST;
+        mbar_wait(&kempty[ks], ((j / C::KST) & 1) ^ 1);
+        uint8_t* sk = smem + C::K_OFF + ks * C::TILE_BYTES;
+        TRACE_EV(8, 0, j);
+        mbar_arrive_expect_tx(&kfull[ks], C::TILE_BYTES);
         for (int b = 0; b < C::BOXES; ++b)
-          tma_load_3d(&tmK, &kfull[s], sk + b * 16384, b * 64, head, kv_off + j * 128);
-        mbar_arrive_expect_tx(&vfull[s], C::TILE_BYTES);
+          tma_load_3d(&tmK, &kfull[ks], sk + b * 16384, b * 64, head, kv_off + j * 128);
+        mbar_wait(&vempty[vs], ((j / C::VST) & 1) ^ 1);
+        uint8_t* sv = smem + C::V_OFF + vs * C::TILE_BYTES;
+        TRACE_EV(9, 0, j);
+        mbar_arrive_expect_tx(&vfull[vs], C::TILE_BYTES);
         for (int b = 0; b < C::BOXES; ++b)
-          tma_load_3d(&tmV, &vfull[s], sv + b * 16384, b * 64, head, kv_off + j * 128);
+          tma_load_3d(&tmV, &vfull[vs], sv + b * 16384, b * 64, head, kv_off + j * 128);
       }
     }
   } else if (warp == 1) {
@@ -131,14 +188,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
       const uint32_t sq = smem_u32(smem + C::Q_OFF);
-      const uint32_t skv = smem_u32(smem + C::KV_OFF);
+      const uint32_t sk0 = smem_u32(smem + C::K_OFF);
+      const uint32_t sv0 = smem_u32(smem + C::V_OFF);
       mbar_wait(q_full, 0);
       auto issue_s = [&](int w, int j) {
-        const int s = j % C::ST;
-        mbar_wait(&kfull[s], (j / C::ST) & 1);
+        const int s = j % C::KST;
+        mbar_wait(&kfull[s], (j / C::KST) & 1);
         tc_fence_after();
+        TRACE_EV(0, w, j);
         const uint32_t qa = sq + w * C::TILE_BYTES;
-        const uint32_t kb = skv + s * C::STAGE_BYTES;
+        const uint32_t kb = sk0 + s * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -148,11 +207,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         mma_commit(&sfull[w]);
       };
       auto issue_pv = [&](int w, int j) {
-        const int s = j % C::ST;
+        const int s = j % C::VST;
+        mbar_wait(&vfull[s], (j / C::VST) & 1);  // normally long complete: check it first
         mbar_wait(&pfull[w], j & 1);
-        mbar_wait(&vfull[s], (j / C::ST) & 1);
+        TRACE_EV(10, w, j);
         tc_fence_after();
-        const uint32_t vb = skv + s * C::STAGE_BYTES + C::TILE_BYTES;
+        TRACE_EV(1, w, j);
+        const uint32_t vb = sv0 + s * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           mma_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
@@ -161,74 +222,86 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       issue_s(0, 0);
       issue_s(1, 0);
+      mma_commit(&kempty[0]);
       for (int j = 0; j < nkv; ++j) {
         issue_pv(0, j);
         if (j + 1 < nkv) issue_s(0, j + 1);
         issue_pv(1, j);
-        mma_commit(&kvempty[j % C::ST]);
-        if (j + 1 < nkv) issue_s(1, j + 1);
+        mma_commit(&vempty[j % C::VST]);
+        if (j + 1 < nkv) {
+          issue_s(1, j + 1);
+          mma_commit(&kempty[(j + 1) % C::KST]);
+        }
       }
       mma_commit(&ofull[0]);
       mma_commit(&ofull[1]);
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
     const int w = (warp - 4) >> 2;  // softmax warpgroup
     const int quarter = warp & 3;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tS = tmem + lane_base + w * 128;
     const uint32_t tO = tmem + lane_base + 256 + w * 128;
+    const float2 sc2 = make_float2(scale_log2, scale_log2);
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(&sfull[w], j & 1);
       tc_fence_after();
+      if (quarter == 0 && lane == 0) TRACE_EV(2, w, j);
       const int kv_valid = min(128, kv_len - j * 128);
-      float mx = -INFINITY;
+      // whole S row of this thread (128 fp32) in registers: one TMEM round trip per tile
+      uint32_t v[128];
+      GS_TMEM_LD32(tS + 0, (*reinterpret_cast<uint32_t(*)[32]>(v + 0)));
+      GS_TMEM_LD32(tS + 32, (*reinterpret_cast<uint32_t(*)[32]>(v + 32)));
+      GS_TMEM_LD32(tS + 64, (*reinterpret_cast<uint32_t(*)[32]>(v + 64)));
+      GS_TMEM_LD32(tS + 96, (*reinterpret_cast<uint32_t(*)[32]>(v + 96)));
+      tmem_ld_wait();
+      if (quarter == 0 && lane == 0) TRACE_EV(3, w, j);
+      const bool full = kv_valid == 128;  // warp-uniform: only a request's last tile is partial
+      if (!full) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        GS_TMEM_LD32(tS + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < kv_valid) mx = fmaxf(mx, __uint_as_float(v[i]));
+        for (int i = 0; i < 128; ++i)
+          if (i >= kv_valid) v[i] = __float_as_uint(-INFINITY);
       }
-      const float m_tile = mx * scale_log2;
+      // row max: 4 independent FMNMX3 chains
+      float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
+      float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
+#pragma unroll
+      for (int i = 4; i < 128; i += 8) {
+        mx0 = fmax3(mx0, __uint_as_float(v[i + 0]), __uint_as_float(v[i + 1]));
+        mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+        mx2 = fmax3(mx2, __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
+        mx3 = fmax3(mx3, __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
+      }
+      const float m_tile = fmax3(mx0, mx1, fmaxf(mx2, mx3)) * scale_log2;
+      // lazy rescale: move the reference max only when it grows by more than 2^8
       const bool need = m_tile > m_run + 8.0f;
       const float alpha = need ? ex2_approx(m_run - m_tile) : 1.0f;
       if (need) m_run = m_tile;
       if (j > 0 && __any_sync(0xffffffffu, need)) {
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
-          uint32_t v[32];
-          GS_TMEM_LD32(tO + c * 32, v);
+          uint32_t o[32];
+          GS_TMEM_LD32(tO + c * 32, o);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-          GS_TMEM_ST32(tO + c * 32, v);
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          GS_TMEM_ST32(tO + c * 32, o);
         }
       }
       l_run *= alpha;
-      float sum = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        GS_TMEM_LD32(tS + c * 32, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int col = c * 32 + 2 * i;
-          const float p0 = col < kv_valid ? ex2_approx(fmaf(__uint_as_float(v[2 * i]), scale_log2, -m_run)) : 0.f;
-          const float p1 = col + 1 < kv_valid ? ex2_approx(fmaf(__uint_as_float(v[2 * i + 1]), scale_log2, -m_run)) : 0.f;
-          sum += p0 + p1;
-          pk[i] = pack_bf16x2(p0, p1);
-        }
-        GS_TMEM_ST16(tS + c * 16, pk);
-      }
-      l_run += sum;
+      float2 acc;
+      if (full)
+        acc = exp_pack_store<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
+      else
+        acc = exp_pack_store<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
+      l_run += acc.x + acc.y;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
+      if (lane == 0) TRACE_EV(4 + quarter, w, j);
       if (lane == 0) mbar_arrive(&pfull[w]);
     }
     // epilogue: O / l -> bf16 -> global
@@ -262,8 +335,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int HD>
-cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
+template <int HD, int POLY8>
+cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
                    int kv_rs, int o_rs, const SeqTable& tab, int total_rows, cudaStream_t stream) {
   using C = Cfg<HD>;
   CUtensorMap tq, tk, tv;
@@ -271,13 +344,37 @@ cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int hea
       !make_tma_3d_bf16(&tk, K, HD, heads, total_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128) ||
       !make_tma_3d_bf16(&tv, V, HD, heads, total_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
+  auto kern = trace ? attn_tc_kernel<HD, POLY8, true> : attn_tc_kernel<HD, POLY8, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
   dim3 grid(tab.tile_start[tab.nreq], heads);
-  attn_tc_kernel<HD><<<grid, THREADS, C::SMEM, stream>>>(tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs,
+  kern<<<grid, THREADS, C::SMEM, stream>>>(tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs,
                                                           tab, scale_log2);
   return cudaGetLastError();
+}
+
+// Fraction of exp2 pairs (in eighths) computed by the FMA-pipe polynomial.  Default from the
+// tuning sweep in profiles/; GS_ATTN_POLY8 overrides it (development aid).
+int poly8_setting() {
+  static int v = [] {
+    const char* e = getenv("GS_ATTN_POLY8");
+    int x = e ? atoi(e) : 0;
+    return (x == 0 || x == 2 || x == 3 || x == 4) ? x : 0;
+  }();
+  return v;
+}
+
+template <int HD>
+cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
+                   int kv_rs, int o_rs, const SeqTable& tab, int total_rows, cudaStream_t stream) {
+  switch (poly8_setting()) {
+    case 2: return launch_t<HD, 2>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
+    case 4: return launch_t<HD, 4>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
+    case 3: return launch_t<HD, 3>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
+    default: return launch_t<HD, 0>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
+  }
 }
 }  // namespace
 
@@ -302,3 +399,8 @@ cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, i
 }
 
 }  // namespace gs
+
+extern "C" int gs_debug_attention_trace(unsigned long long* host, size_t n) {
+  if (!host || n > sizeof(gs::g_attn_trace) / 8) return -1;
+  return cudaMemcpyFromSymbol(host, gs::g_attn_trace, n * 8) == cudaSuccess ? 0 : -4;
+}

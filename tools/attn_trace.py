@@ -1,0 +1,42 @@
+"""Per-tile timeline of the first attention CTA (GS_ATTN_TRACE=1): MMA issue, softmax wake/load/done."""
+import ctypes
+import os
+import sys
+
+os.environ["GS_ATTN_TRACE"] = "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2604_04335_b200 as gs  # noqa: E402
+
+lib = gs.load()
+lib.gs_debug_attention_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+ctx = gs.Context(device=0)
+N, H, d = 75600, 5, 128
+q, k, v = (torch.randn(N, H, d, device="cuda").to(torch.bfloat16) for _ in range(3))
+o = torch.empty_like(q)
+for _ in range(2):
+    ctx.debug_attention(q, k, v, o, H, d, [0], [N])
+buf = np.zeros(16 * 64, dtype=np.uint64)
+assert lib.gs_debug_attention_trace(buf.ctypes.data, buf.size) == 0
+t = buf.reshape(16, 32, 2).astype(np.int64)
+t0 = t[t > 0].min()
+names = ["issue_S", "issue_PV", "sm_wake", "sm_loaded", "Pdone_q0", "Pdone_q1", "Pdone_q2", "Pdone_q3"]
+print("tile  " + "  ".join(f"{n}{w:>1d}".rjust(11) for n in names for w in range(2)))
+for j in range(32):
+    print(f"{j:4d}  " + "  ".join(f"{(t[e, j, w] - t0) if t[e, j, w] else -1:11d}" for e in range(8) for w in range(2)))
+d_ = np.diff(t[2, 4:30, 0])
+print("WG0 period (cycles) median", np.median(d_))
+print("softmax T_s (wake->Pdone) median", np.median(t[4, 4:30, 0] - t[2, 4:30, 0]),
+      "load", np.median(t[3, 4:30, 0] - t[2, 4:30, 0]))
+print("Pdone -> issue_PV median", np.median(t[1, 4:30, 0] - t[4, 4:30, 0]))
+for q in range(4):
+    print(f"WG0 q{q} T_s median", np.median(t[4 + q, 4:30, 0] - t[2, 4:30, 0]),
+          f"WG1 q{q} T_s median", np.median(t[4 + q, 4:30, 1] - t[2, 4:30, 1]))
+print("issue_S(j+1) -> wake(j+1) median", np.median(t[2, 5:30, 0] - t[0, 5:30, 0]))
+for j in range(20, 26):
+    print(f"tile {j}: K issued {t[8, j, 0] - t0}  V issued {t[9, j, 0] - t0}  MMA pfull0-ok {t[10, j, 0] - t0} "
+          f"PV0 issued {t[1, j, 0] - t0}  pfull1-ok {t[10, j, 1] - t0} PV1 issued {t[1, j, 1] - t0}")
+ctx.close()
