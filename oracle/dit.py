@@ -123,9 +123,9 @@ def softmax(s, axis=-1):
 def attention(q, k, v):
     """Full non-causal attention of one request: q [nq, H, d], k/v [n, H, d] -> [nq, H, d]."""
     d = q.shape[-1]
-    s = np.einsum("qhd,khd->hqk", q, k) / math.sqrt(d)
+    s = np.matmul(q.transpose(1, 0, 2), k.transpose(1, 2, 0)) / math.sqrt(d)   # [H, nq, n]
     p = softmax(s, axis=-1)
-    return np.einsum("hqk,khd->qhd", p, v)
+    return np.matmul(p, v.transpose(1, 0, 2)).transpose(1, 0, 2)              # [nq, H, d]
 
 
 # --------------------------------------------------------------------------------------
