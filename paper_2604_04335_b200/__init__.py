@@ -58,6 +58,7 @@ _SIG = {
     "gs_debug_attention": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _IP, _IP, _I],
     "gs_debug_block": [_P, _I, _I, _FP, _I, _IP, _IP, _IP, _FP],
     "gs_debug_time_embed": [_P, _I, _I, _FP, _FP, _FP],
+    "gs_debug_attention_trace": [_P, ctypes.c_size_t],
 }
 _lib = None
 
@@ -241,6 +242,12 @@ class Context:
         self._ck(self._lib.gs_debug_block(self._h, model, layer, x.ctypes.data_as(_FP), len(n_rows),
                                           _ints(flat), _ints(tok_lo), _ints(n_rows), _fl(t)))
         return x
+
+    def debug_attention_trace(self):
+        """clock64 stamps of the first attention CTA (needs GS_ATTN_TRACE=1 at process start)."""
+        buf = np.zeros(16 * 64, dtype=np.uint64)
+        self._ck(self._lib.gs_debug_attention_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.size))
+        return buf.reshape(16, 32, 2)
 
     def debug_time_embed(self, model, t, dim):
         e0 = np.zeros((len(t), dim), np.float32)

@@ -1,5 +1,4 @@
 """Per-tile timeline of the first attention CTA (GS_ATTN_TRACE=1): MMA issue, softmax wake/load/done."""
-import ctypes
 import os
 import sys
 
@@ -11,17 +10,13 @@ import torch  # noqa: E402
 
 import paper_2604_04335_b200 as gs  # noqa: E402
 
-lib = gs.load()
-lib.gs_debug_attention_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 ctx = gs.Context(device=0)
 N, H, d = 75600, 5, 128
 q, k, v = (torch.randn(N, H, d, device="cuda").to(torch.bfloat16) for _ in range(3))
 o = torch.empty_like(q)
 for _ in range(2):
     ctx.debug_attention(q, k, v, o, H, d, [0], [N])
-buf = np.zeros(16 * 64, dtype=np.uint64)
-assert lib.gs_debug_attention_trace(buf.ctypes.data, buf.size) == 0
-t = buf.reshape(16, 32, 2).astype(np.int64)
+t = ctx.debug_attention_trace().astype(np.int64)
 t0 = t[t > 0].min()
 names = ["issue_S", "issue_PV", "sm_wake", "sm_loaded", "Pdone_q0", "Pdone_q1", "Pdone_q2", "Pdone_q3"]
 print("tile  " + "  ".join(f"{n}{w:>1d}".rjust(11) for n in names for w in range(2)))
