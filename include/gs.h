@@ -128,8 +128,46 @@ int gs_stats(gs_ctx* ctx, char* json, size_t len);
 /* The CUDA stream (cudaStream_t) the context launches rank `rank`'s work on, as a pointer. */
 int gs_stream(gs_ctx* ctx, int rank, void** stream_out);
 
+/* ------------------------------------------------------------------ exchange plans (host only)
+ * The SP data movement of one DiT block (Ulysses seq->head of
+ * Q,K,V and head->seq of O) and of a resume (row a17: latent re-shard p -> p') as transfer lists
+ * for one participant.  Pure host computation (no GPU, no context): the NCCL executor, the
+ * emulated executor and the CPU multi-process tests all run these plans.  Messages between a
+ * pair of participants are matched in list order (NCCL point-to-point semantics).
+ * Offsets / sizes are in elements of the named buffers (bf16 for a2a, fp32 for the latent):
+ *   a2a kind 0 (Q,K,V; apply to each): SEND buffer [dest j][rows_me][H_j][d] (pack-kernel layout),
+ *     RECV buffer [rows of the whole batch][H_me][d];
+ *   a2a kind 1 (O): O buffer [rows of the batch][H_me][d] (attention output), STAGE buffer
+ *     (*stage_elems elements), ORECV buffer [rows_me][heads * d]; COPY entries (2-D blocks) run
+ *     after all sends/recvs completed;
+ *   reshard: OLD shard [old rows][lat], NEW shard [new rows][lat]; peers are global ranks.
+ * Token shard i of p is [floor(i n/p), floor((i+1) n/p)) (reading 10); heads split
+ * contiguously with positions < H mod p holding ceil(H/p) (reading 9). */
+enum { GS_XFER_SEND = 0, GS_XFER_RECV = 1, GS_XFER_COPY = 2 };
+enum { GS_BUF_SEND = 0, GS_BUF_RECV = 1, GS_BUF_O = 2, GS_BUF_STAGE = 3, GS_BUF_ORECV = 4,
+       GS_BUF_OLD = 5, GS_BUF_NEW = 6 };
+typedef struct {
+  int op;                  /* GS_XFER_*                                                    */
+  int peer;                /* SP position (a2a) or global rank (reshard); -1 for COPY       */
+  int src_buf, dst_buf;    /* GS_BUF_* (-1 where unused)                                   */
+  long long src_off, dst_off;
+  long long rows, width;   /* a rows x width block                                         */
+  long long src_pitch, dst_pitch;
+} gs_xfer;
+/* kind 0 = seq->head (Q,K,V), 1 = head->seq (O) for SP position `me` of p over a batch of nreq
+ * requests with n_tokens[r] tokens.  out may be NULL to query *n_out; GS_EINVAL if max_out is
+ * too small or an argument is out of range. */
+int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
+                gs_xfer* out, int max_out, int* n_out, long long* stage_elems);
+/* Re-shard of a request's latent [n_tokens, lat] from old_ranks (old_p) to new_ranks (new_p), as
+ * seen by global rank `me` (which may be in either set, both or none). */
+int gs_plan_reshard(int n_tokens, int lat, const int* old_ranks, int old_p, const int* new_ranks,
+                    int new_p, int me, gs_xfer* out, int max_out, int* n_out);
+
 /* ------------------------------------------------------------------ parity / debug entry points
- * Single device, rank-independent, caller-owned buffers. */
+ * Single device, rank-independent, caller-owned buffers.  The launch is ordered after all work
+ * previously submitted to the legacy default stream (where torch writes the caller's inputs)
+ * and the call returns after the kernel completed. */
 /* GEMM C = A W^T with epilogue epi (0 bf16, 1 GELU-bf16, 2 fp32, 3 gated-residual fp32,
  * 4 Euler fp32; see csrc/kernels.h).  A [M,K] bf16, W [N,K] bf16, bias [N] bf16 (or NULL),
  * out [M,N] (bf16 or fp32), gate_a [N] fp32, gate_b [B,gate_b_stride] fp32, row_req [M] int32,

@@ -30,6 +30,18 @@ class ModelDesc(ctypes.Structure):
                 ("flow_shift", ctypes.c_float), ("weight_seed", ctypes.c_uint64)]
 
 
+class Xfer(ctypes.Structure):
+    """gs_xfer (include/gs.h): one transfer of an exchange plan."""
+    _fields_ = [("op", ctypes.c_int), ("peer", ctypes.c_int), ("src_buf", ctypes.c_int),
+                ("dst_buf", ctypes.c_int), ("src_off", ctypes.c_longlong),
+                ("dst_off", ctypes.c_longlong), ("rows", ctypes.c_longlong),
+                ("width", ctypes.c_longlong), ("src_pitch", ctypes.c_longlong),
+                ("dst_pitch", ctypes.c_longlong)]
+
+
+XFER_SEND, XFER_RECV, XFER_COPY = 0, 1, 2
+BUF_SEND, BUF_RECV, BUF_O, BUF_STAGE, BUF_ORECV, BUF_OLD, BUF_NEW = range(7)
+
 _P = ctypes.c_void_p
 _I = ctypes.c_int
 _IP = ctypes.POINTER(ctypes.c_int)
@@ -59,6 +71,9 @@ _SIG = {
     "gs_debug_block": [_P, _I, _I, _FP, _I, _IP, _IP, _IP, _FP],
     "gs_debug_time_embed": [_P, _I, _I, _FP, _FP, _FP],
     "gs_debug_attention_trace": [_P, ctypes.c_size_t],
+    "gs_plan_a2a": [_I, _I, _I, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP,
+                    ctypes.POINTER(ctypes.c_longlong)],
+    "gs_plan_reshard": [_I, _I, _IP, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP],
 }
 _lib = None
 
@@ -103,6 +118,36 @@ def nccl_unique_id():
     if rc != GS_OK:
         raise GsError(rc, "ncclGetUniqueId failed")
     return buf.raw
+
+
+def _xfers(call):
+    n = ctypes.c_int()
+    rc = call(None, 0, ctypes.byref(n))
+    if rc != GS_OK:
+        raise GsError(rc, "plan arguments rejected")
+    arr = (Xfer * max(n.value, 1))()
+    rc = call(arr, n.value, ctypes.byref(n))
+    if rc != GS_OK:
+        raise GsError(rc, "plan failed")
+    return [{f: getattr(arr[i], f) for f, _t in Xfer._fields_} for i in range(n.value)]
+
+
+def plan_a2a(kind, p, me, n_tokens, heads, head_dim):
+    """Host-only Ulysses exchange plan of SP position `me` (kind 0: Q/K/V seq->head, 1: O
+    head->seq).  Returns (list of transfer dicts, staging elements)."""
+    lib = load()
+    stage = ctypes.c_longlong()
+    xs = _xfers(lambda out, mx, n: lib.gs_plan_a2a(kind, p, me, len(n_tokens), _ints(n_tokens),
+                                                   heads, head_dim, out, mx, n, ctypes.byref(stage)))
+    return xs, stage.value
+
+
+def plan_reshard(n_tokens, lat, old_ranks, new_ranks, me):
+    """Host-only latent re-shard plan of global rank `me`."""
+    lib = load()
+    return _xfers(lambda out, mx, n: lib.gs_plan_reshard(n_tokens, lat, _ints(old_ranks),
+                                                         len(old_ranks), _ints(new_ranks),
+                                                         len(new_ranks), me, out, mx, n))
 
 
 class Context:

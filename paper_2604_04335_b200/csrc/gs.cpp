@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 
+#include "plan.h"
 #include "runtime.h"
 
 using namespace gs;
@@ -121,15 +122,6 @@ int local_index(gs_ctx* c, int rank) {
   if (c->emulated) return (rank >= 0 && rank < c->world) ? rank : -1;
   return rank == c->my_rank ? 0 : -1;
 }
-
-// Contiguous shard i of n tokens over p ranks (reading 10).
-inline void shard_bounds(int n, int p, int i, int* lo, int* hi) {
-  *lo = static_cast<int>((static_cast<long long>(i) * n) / p);
-  *hi = static_cast<int>((static_cast<long long>(i + 1) * n) / p);
-}
-
-// Contiguous head split: positions < H mod p get ceil(H/p) heads (reading 9).
-inline int head_off(int H, int p, int j) { return j * (H / p) + std::min(j, H % p); }
 
 double sigma_at(int i, int S, double shift) {
   const double u = 1.0 - static_cast<double>(i) / S;
@@ -237,50 +229,22 @@ void** global_slot(Model& m, const char* name) {
 }
 
 // ------------------------------------------------------------------ batch plan
-struct Plan {
-  int p = 1, B = 0, D = 0, H = 0, hd = 0, F = 0;
+struct Plan : A2aGeometry {
+  int D = 0, F = 0;
   Model* m = nullptr;
   std::vector<Request*> reqs;
   std::vector<int> ranks;
-  std::vector<int> hoff;      // p + 1
-  std::vector<int> off_full;  // B
-  int rows_full = 0;
-  std::vector<std::vector<int>> lo, hi, loff;  // [pos][req]
-  std::vector<int> rows;                        // [pos]
-  int H_loc(int j) const { return hoff[j + 1] - hoff[j]; }
 };
 
 void make_plan(Plan& P, Model* m, const std::vector<Request*>& reqs, const int* ranks, int p) {
+  std::vector<int> n(reqs.size());
+  for (size_t r = 0; r < reqs.size(); ++r) n[r] = reqs[r]->n;
+  P.init(p, n.data(), static_cast<int>(n.size()), m->desc.heads, m->hd);
   P.m = m;
-  P.p = p;
-  P.B = static_cast<int>(reqs.size());
   P.D = m->desc.dim;
-  P.H = m->desc.heads;
-  P.hd = m->hd;
   P.F = m->desc.ffn;
   P.reqs = reqs;
   P.ranks.assign(ranks, ranks + p);
-  P.hoff.resize(p + 1);
-  for (int j = 0; j <= p; ++j) P.hoff[j] = head_off(P.H, p, j);
-  P.off_full.resize(P.B);
-  P.rows_full = 0;
-  for (int r = 0; r < P.B; ++r) {
-    P.off_full[r] = P.rows_full;
-    P.rows_full += reqs[r]->n;
-  }
-  P.lo.assign(p, std::vector<int>(P.B));
-  P.hi.assign(p, std::vector<int>(P.B));
-  P.loff.assign(p, std::vector<int>(P.B));
-  P.rows.assign(p, 0);
-  for (int i = 0; i < p; ++i) {
-    int acc = 0;
-    for (int r = 0; r < P.B; ++r) {
-      shard_bounds(reqs[r]->n, p, i, &P.lo[i][r], &P.hi[i][r]);
-      P.loff[i][r] = acc;
-      acc += P.hi[i][r] - P.lo[i][r];
-    }
-    P.rows[i] = acc;
-  }
 }
 
 // Size the arena of position i and upload its row maps.
@@ -347,135 +311,120 @@ int move_latent(gs_ctx* c, const Plan& P, int i, RankArena& A, int dir) {
 }
 
 // ------------------------------------------------------------------ exchanges
+// Executors of the host plans (plan.cpp).  NCCL mode: this process is one SP position; sends and
+// recvs of the plan go into one NCCL group on the context stream (NVLink / NVSwitch), local
+// copies are device copies.  Emulated mode: every position is local; the n-th send of i to j is
+// the n-th recv of j from i (the NCCL matching rule), executed as a device copy.
+int my_position(gs_ctx* c, const Plan& P) {
+  for (int i = 0; i < P.p; ++i)
+    if (P.ranks[i] == c->my_rank) return i;
+  return -1;
+}
+
+int copy_block(gs_ctx* c, void* dst, const void* src, const gs_xfer& x, size_t esz) {
+  if (x.rows == 1 || (x.src_pitch == x.width && x.dst_pitch == x.width))
+    CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(x.rows * x.width) * esz, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    CK(cudaMemcpy2DAsync(dst, x.dst_pitch * esz, src, x.src_pitch * esz, x.width * esz, x.rows,
+                         cudaMemcpyDeviceToDevice, c->stream));
+  return GS_OK;
+}
+
+// bufs(pos, id) -> base pointer of buffer id of position pos (nullptr if not applicable)
+template <class BufFn>
+int run_emulated(gs_ctx* c, const std::vector<std::vector<gs_xfer>>& plans, BufFn bufs, size_t esz) {
+  const int p = static_cast<int>(plans.size());
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) {
+      if (i == j) continue;
+      std::vector<const gs_xfer*> snd, rcv;
+      for (const gs_xfer& x : plans[i])
+        if (x.op == GS_XFER_SEND && x.peer == j) snd.push_back(&x);
+      for (const gs_xfer& x : plans[j])
+        if (x.op == GS_XFER_RECV && x.peer == i) rcv.push_back(&x);
+      if (snd.size() != rcv.size()) return fail(c, GS_ESTATE, "exchange plan mismatch %d -> %d", i, j);
+      for (size_t k = 0; k < snd.size(); ++k) {
+        if (snd[k]->width != rcv[k]->width) return fail(c, GS_ESTATE, "exchange size mismatch %d -> %d", i, j);
+        char* dst = static_cast<char*>(bufs(j, rcv[k]->dst_buf)) + rcv[k]->dst_off * esz;
+        const char* src = static_cast<const char*>(bufs(i, snd[k]->src_buf)) + snd[k]->src_off * esz;
+        CK(cudaMemcpyAsync(dst, src, snd[k]->width * esz, cudaMemcpyDeviceToDevice, c->stream));
+      }
+    }
+  for (int i = 0; i < p; ++i)
+    for (const gs_xfer& x : plans[i])
+      if (x.op == GS_XFER_COPY)
+        RET(copy_block(c, static_cast<char*>(bufs(i, x.dst_buf)) + x.dst_off * esz,
+                       static_cast<const char*>(bufs(i, x.src_buf)) + x.src_off * esz, x, esz));
+  return GS_OK;
+}
+
 // seq -> head: Q/K/V chunk j of position i (rows of i, heads of j) -> recv buffers of j.
 int exchange_qkv(gs_ctx* c, const Plan& P) {
   Scope sc(c, "a2a_qkv", 0);
-  const size_t d = P.hd;
   if (c->emulated) {
-    for (int i = 0; i < P.p; ++i) {
-      RankArena& S = c->local[P.ranks[i]];
-      for (int j = 0; j < P.p; ++j) {
-        RankArena& R = c->local[P.ranks[j]];
-        const size_t Hj = P.H_loc(j);
-        const size_t chunk = static_cast<size_t>(P.rows[i]) * P.hoff[j] * d;
-        for (int r = 0; r < P.B; ++r) {
-          const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * Hj * d;
-          if (!cnt) continue;
-          const size_t so = chunk + static_cast<size_t>(P.loff[i][r]) * Hj * d;
-          const size_t ro = static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * Hj * d;
-          CK(cudaMemcpyAsync(R.qr.as<bf16>() + ro, S.qs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
-          CK(cudaMemcpyAsync(R.kr.as<bf16>() + ro, S.ks.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
-          CK(cudaMemcpyAsync(R.vr.as<bf16>() + ro, S.vs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
-        }
-      }
+    std::vector<std::vector<gs_xfer>> plans(P.p);
+    for (int i = 0; i < P.p; ++i) plan_qkv(P, i, plans[i]);
+    for (int t = 0; t < 3; ++t) {
+      auto bufs = [&](int pos, int id) -> void* {
+        RankArena& A = c->local[P.ranks[pos]];
+        if (id == GS_BUF_SEND) return t == 0 ? A.qs.p : t == 1 ? A.ks.p : A.vs.p;
+        return t == 0 ? A.qr.p : t == 1 ? A.kr.p : A.vr.p;
+      };
+      RET(run_emulated(c, plans, bufs, 2));
     }
     return GS_OK;
   }
-  int me = -1;
-  for (int i = 0; i < P.p; ++i)
-    if (P.ranks[i] == c->my_rank) me = i;
+  const int me = my_position(c, P);
+  std::vector<gs_xfer> plan;
+  plan_qkv(P, me, plan);
   RankArena& A = c->local[0];
+  bf16* snd[3] = {A.qs.as<bf16>(), A.ks.as<bf16>(), A.vs.as<bf16>()};
+  bf16* rcv[3] = {A.qr.as<bf16>(), A.kr.as<bf16>(), A.vr.as<bf16>()};
   NK(ncclGroupStart());
-  for (int j = 0; j < P.p; ++j) {  // my rows -> j
-    const size_t Hj = P.H_loc(j);
-    const size_t chunk = static_cast<size_t>(P.rows[me]) * P.hoff[j] * d;
-    for (int r = 0; r < P.B; ++r) {
-      const size_t cnt = static_cast<size_t>(P.hi[me][r] - P.lo[me][r]) * Hj * d;
-      if (!cnt) continue;
-      const size_t so = chunk + static_cast<size_t>(P.loff[me][r]) * Hj * d;
-      if (j == me) {
-        const size_t ro = static_cast<size_t>(P.off_full[r] + P.lo[me][r]) * Hj * d;
-        CK(cudaMemcpyAsync(A.qr.as<bf16>() + ro, A.qs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(A.kr.as<bf16>() + ro, A.ks.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(A.vr.as<bf16>() + ro, A.vs.as<bf16>() + so, cnt * 2, cudaMemcpyDeviceToDevice, c->stream));
-      } else {
-        NK(ncclSend(A.qs.as<bf16>() + so, cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
-        NK(ncclSend(A.ks.as<bf16>() + so, cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
-        NK(ncclSend(A.vs.as<bf16>() + so, cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
-      }
+  for (const gs_xfer& x : plan)
+    for (int t = 0; t < 3; ++t) {
+      if (x.op == GS_XFER_SEND)
+        NK(ncclSend(snd[t] + x.src_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, c->stream));
+      else if (x.op == GS_XFER_RECV)
+        NK(ncclRecv(rcv[t] + x.dst_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, c->stream));
     }
-  }
-  const size_t Hm = P.H_loc(me);
-  for (int i = 0; i < P.p; ++i) {  // rows of i, my heads
-    if (i == me) continue;
-    for (int r = 0; r < P.B; ++r) {
-      const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * Hm * d;
-      if (!cnt) continue;
-      const size_t ro = static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * Hm * d;
-      NK(ncclRecv(A.qr.as<bf16>() + ro, cnt * 2, ncclUint8, P.ranks[i], c->comm, c->stream));
-      NK(ncclRecv(A.kr.as<bf16>() + ro, cnt * 2, ncclUint8, P.ranks[i], c->comm, c->stream));
-      NK(ncclRecv(A.vr.as<bf16>() + ro, cnt * 2, ncclUint8, P.ranks[i], c->comm, c->stream));
-    }
-  }
   NK(ncclGroupEnd());
+  for (const gs_xfer& x : plan)
+    if (x.op == GS_XFER_COPY)
+      for (int t = 0; t < 3; ++t) RET(copy_block(c, rcv[t] + x.dst_off, snd[t] + x.src_off, x, 2));
   return GS_OK;
 }
 
 // head -> seq: attention output of position j (all rows, heads of j) -> rows' owners.
 int exchange_o(gs_ctx* c, const Plan& P) {
   Scope sc(c, "a2a_o", 0);
-  const size_t d = P.hd, D = P.D;
+  auto arena_buf = [&](RankArena& A, int id) -> void* {
+    return id == GS_BUF_O ? A.o.p : id == GS_BUF_STAGE ? A.ostage.p : A.orecv.p;
+  };
   if (c->emulated) {
-    for (int j = 0; j < P.p; ++j) {
-      RankArena& S = c->local[P.ranks[j]];
-      const size_t w = static_cast<size_t>(P.H_loc(j)) * d;
-      for (int i = 0; i < P.p; ++i) {
-        RankArena& R = c->local[P.ranks[i]];
-        for (int r = 0; r < P.B; ++r) {
-          const size_t cnt = P.hi[i][r] - P.lo[i][r];
-          if (!cnt) continue;
-          CK(cudaMemcpy2DAsync(R.orecv.as<bf16>() + static_cast<size_t>(P.loff[i][r]) * D + P.hoff[j] * d, D * 2,
-                               S.o.as<bf16>() + static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * w, w * 2, w * 2, cnt,
-                               cudaMemcpyDeviceToDevice, c->stream));
-        }
-      }
-    }
-    return GS_OK;
+    std::vector<std::vector<gs_xfer>> plans(P.p);
+    for (int i = 0; i < P.p; ++i) plan_o(P, i, plans[i], nullptr);
+    auto bufs = [&](int pos, int id) -> void* { return arena_buf(c->local[P.ranks[pos]], id); };
+    return run_emulated(c, plans, bufs, 2);
   }
-  int me = -1;
-  for (int i = 0; i < P.p; ++i)
-    if (P.ranks[i] == c->my_rank) me = i;
+  const int me = my_position(c, P);
+  std::vector<gs_xfer> plan;
+  plan_o(P, me, plan, nullptr);
   RankArena& A = c->local[0];
-  const size_t wm = static_cast<size_t>(P.H_loc(me)) * d;
-  // staging layout: [src j][req r][rows][H_j d]
-  std::vector<size_t> stage_off(P.p * P.B);
-  size_t acc = 0;
-  for (int j = 0; j < P.p; ++j)
-    for (int r = 0; r < P.B; ++r) {
-      stage_off[j * P.B + r] = acc;
-      acc += static_cast<size_t>(P.hi[me][r] - P.lo[me][r]) * P.H_loc(j) * d;
-    }
   NK(ncclGroupStart());
-  for (int i = 0; i < P.p; ++i) {
-    if (i == me) continue;
-    for (int r = 0; r < P.B; ++r) {
-      const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * wm;
-      if (!cnt) continue;
-      NK(ncclSend(A.o.as<bf16>() + static_cast<size_t>(P.off_full[r] + P.lo[i][r]) * wm, cnt * 2, ncclUint8,
-                  P.ranks[i], c->comm, c->stream));
-    }
-  }
-  for (int j = 0; j < P.p; ++j) {
-    if (j == me) continue;
-    const size_t wj = static_cast<size_t>(P.H_loc(j)) * d;
-    for (int r = 0; r < P.B; ++r) {
-      const size_t cnt = static_cast<size_t>(P.hi[me][r] - P.lo[me][r]) * wj;
-      if (!cnt) continue;
-      NK(ncclRecv(A.ostage.as<bf16>() + stage_off[j * P.B + r], cnt * 2, ncclUint8, P.ranks[j], c->comm, c->stream));
-    }
+  for (const gs_xfer& x : plan) {
+    if (x.op == GS_XFER_SEND)
+      NK(ncclSend(static_cast<bf16*>(arena_buf(A, x.src_buf)) + x.src_off, x.width * 2, ncclUint8, P.ranks[x.peer],
+                  c->comm, c->stream));
+    else if (x.op == GS_XFER_RECV)
+      NK(ncclRecv(static_cast<bf16*>(arena_buf(A, x.dst_buf)) + x.dst_off, x.width * 2, ncclUint8, P.ranks[x.peer],
+                  c->comm, c->stream));
   }
   NK(ncclGroupEnd());
-  for (int j = 0; j < P.p; ++j) {
-    const size_t wj = static_cast<size_t>(P.H_loc(j)) * d;
-    for (int r = 0; r < P.B; ++r) {
-      const size_t cnt = P.hi[me][r] - P.lo[me][r];
-      if (!cnt) continue;
-      const bf16* src = (j == me) ? A.o.as<bf16>() + static_cast<size_t>(P.off_full[r] + P.lo[me][r]) * wm
-                                  : A.ostage.as<bf16>() + stage_off[j * P.B + r];
-      CK(cudaMemcpy2DAsync(A.orecv.as<bf16>() + static_cast<size_t>(P.loff[me][r]) * D + P.hoff[j] * d, D * 2, src,
-                           wj * 2, wj * 2, cnt, cudaMemcpyDeviceToDevice, c->stream));
-    }
-  }
+  for (const gs_xfer& x : plan)
+    if (x.op == GS_XFER_COPY)
+      RET(copy_block(c, static_cast<bf16*>(arena_buf(A, x.dst_buf)) + x.dst_off,
+                     static_cast<bf16*>(arena_buf(A, x.src_buf)) + x.src_off, x, 2));
   return GS_OK;
 }
 
@@ -752,6 +701,7 @@ void gs_destroy(gs_ctx* c) {
       if (b->p) cudaFree(b->p);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  if (c->ev_order) cudaEventDestroy(c->ev_order);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   if (c->d_flag) cudaFree(c->d_flag);
@@ -974,29 +924,42 @@ int gs_resume(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
     shard_bounds(q->n, nranks, i, &ns[i].lo, &ns[i].hi);
     if (local_index(c, ns[i].rank) >= 0) RET(alloc_shard(c, ns[i], lat));
   }
-  // interval intersections old x new: pure copies
-  bool nccl_open = false;
-  if (!c->emulated && c->world > 1) {
-    NK(ncclGroupStart());
-    nccl_open = true;
-  }
-  for (const Shard& o : q->shards)
-    for (const Shard& n : ns) {
-      const int lo = std::max(o.lo, n.lo), hi = std::min(o.hi, n.hi);
-      if (lo >= hi) continue;
-      const size_t bytes = static_cast<size_t>(hi - lo) * lat * 4;
-      const bool have_o = local_index(c, o.rank) >= 0, have_n = local_index(c, n.rank) >= 0;
-      float* src = have_o ? o.z + static_cast<size_t>(lo - o.lo) * lat : nullptr;
-      float* dst = have_n ? n.z + static_cast<size_t>(lo - n.lo) * lat : nullptr;
-      if (have_o && have_n) {
-        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
-      } else if (have_o) {
-        NK(ncclSend(src, bytes, ncclUint8, n.rank, c->comm, c->stream));
-      } else if (have_n) {
-        NK(ncclRecv(dst, bytes, ncclUint8, o.rank, c->comm, c->stream));
+  // interval intersections old x new: pure copies, planned on the host
+  std::vector<int> old_ranks(q->ranks);
+  auto shard_of = [](std::vector<Shard>& v, int rank) -> float* {
+    for (Shard& s : v)
+      if (s.rank == rank) return s.z;
+    return nullptr;
+  };
+  if (c->emulated) {
+    // every rank is local: pair the n-th send of a with the n-th recv of b
+    std::vector<std::vector<gs_xfer>> plans(c->world);
+    for (int me = 0; me < c->world; ++me)
+      plan_reshard(q->n, lat, old_ranks.data(), static_cast<int>(old_ranks.size()), ranks, nranks, me, plans[me]);
+    auto bufs = [&](int rank, int id) -> void* {
+      return id == GS_BUF_OLD ? shard_of(q->shards, rank) : shard_of(ns, rank);
+    };
+    RET(run_emulated(c, plans, bufs, 4));
+  } else {
+    std::vector<gs_xfer> plan;
+    plan_reshard(q->n, lat, old_ranks.data(), static_cast<int>(old_ranks.size()), ranks, nranks, c->my_rank, plan);
+    float* zo = shard_of(q->shards, c->my_rank);
+    float* zn = shard_of(ns, c->my_rank);
+    bool any_p2p = false;
+    for (const gs_xfer& x : plan) any_p2p |= x.op != GS_XFER_COPY;
+    if (any_p2p) {
+      NK(ncclGroupStart());
+      for (const gs_xfer& x : plan) {
+        if (x.op == GS_XFER_SEND)
+          NK(ncclSend(zo + x.src_off, x.width * 4, ncclUint8, x.peer, c->comm, c->stream));
+        else if (x.op == GS_XFER_RECV)
+          NK(ncclRecv(zn + x.dst_off, x.width * 4, ncclUint8, x.peer, c->comm, c->stream));
       }
+      NK(ncclGroupEnd());
     }
-  if (nccl_open) NK(ncclGroupEnd());
+    for (const gs_xfer& x : plan)
+      if (x.op == GS_XFER_COPY) RET(copy_block(c, zn + x.dst_off, zo + x.src_off, x, 4));
+  }
   CK(cudaStreamSynchronize(c->stream));
   for (Shard& o : q->shards)
     if (o.z) cudaFree(o.z);
@@ -1087,12 +1050,24 @@ int gs_stream(gs_ctx* c, int rank, void** stream_out) {
 }
 
 // ------------------------------------------------------------------ debug entry points
+namespace {
+// Caller-owned device buffers are typically produced on the legacy default stream (e.g. by
+// torch); order the context's non-blocking stream after that work without a host sync.
+int order_after_legacy(gs_ctx* c) {
+  if (!c->ev_order) CK(cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->ev_order, cudaStreamLegacy));
+  CK(cudaStreamWaitEvent(c->stream, c->ev_order, 0));
+  return GS_OK;
+}
+}  // namespace
+
 int gs_debug_gemm(gs_ctx* c, int e, int M, int N, int K, const void* A, const void* W, const void* bias, void* out,
                   const float* gate_a, const float* gate_b, int gate_b_stride, const int* row_req,
                   const float* dsig_host) {
   if (!c) return GS_EINVAL;
   std::lock_guard<std::mutex> g(c->run_mu);
   CK(cudaSetDevice(c->device));
+  RET(order_after_legacy(c));
   EpiParams ep{};
   ep.out = out;
   ep.ldo = N;
@@ -1114,6 +1089,7 @@ int gs_debug_attention(gs_ctx* c, const void* q, const void* k, const void* v, v
   if (!c || !seq_off || !seq_len) return GS_EINVAL;
   std::lock_guard<std::mutex> g(c->run_mu);
   CK(cudaSetDevice(c->device));
+  RET(order_after_legacy(c));
   cudaError_t err = attention_tc(q, k, v, o, heads, d, q_rs, kv_rs, o_rs, seq_off, seq_len, nreq, c->num_sms, c->stream);
   if (err != cudaSuccess) return fail(c, err == cudaErrorInvalidValue ? GS_EINVAL : GS_ECUDA, "attention: %s", cudaGetErrorString(err));
   CK(cudaStreamSynchronize(c->stream));

@@ -96,6 +96,7 @@ struct gs_ctx {
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
   std::vector<cudaEvent_t> event_pool;
   long long launches = 0;
+  cudaEvent_t ev_order = nullptr;   // debug entry points: order after the legacy stream
   // pinned scratch for preemption agreement
   int* h_flag = nullptr;
   int* d_flag = nullptr;

@@ -1,0 +1,167 @@
+"""Parity at BASELINE.json's full sizes, in the launch configurations bench.py times (SURVEY.md §8(c)
+"Large configs"): the GPU kernels run on the whole 32,760- / 75,600-token requests and the fp64 oracle
+checks sampled output rows it can compute one by one (row-sampled attention and DiT block, oracle
+`dit_block_rows`).  Exactness properties that hold at any size (SP degree, preempt -> re-shard ->
+resume) are checked GPU-vs-GPU bitwise on the full 720p grid with a 1-layer Wan-14B-shaped model.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import dit
+from synth import models as sm
+from synth import rng
+from tests.gpu_util import from_dev_bf16, rel_l2, to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2        # BASELINE.json north_star: relative L2 vs the CPU oracle
+TOL_ATTN = 6e-3   # identical bf16 inputs: P and O rounded to bf16
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def gs():
+    import paper_2604_04335_b200 as m
+    m.load()
+    return m
+
+
+def sample_rows(n, k=40, seed=0):
+    """First / last rows, 128-row tile boundaries, the last partial tile, and random rows."""
+    g = np.random.default_rng(seed)
+    fixed = [0, 1, 127, 128, 129, 255, 256, 257, n // 2, n - 129, n - 128, n - 2, n - 1,
+             (n // 128) * 128 - 1, (n // 128) * 128]
+    rows = [r for r in fixed if 0 <= r < n] + g.integers(0, n, k).tolist()
+    return np.unique(rows)
+
+
+# ----------------------------------------------------------------------------- attention
+ATTN_CASES = [
+    ("c4 720p sp1 (40 heads)", [75600], 40),
+    ("c4 720p sp8 (5 heads)", [75600], 5),
+    ("c3 480p sp1 (12 heads)", [32760], 12),
+    ("c3 480p sp8 (2 heads, uneven split)", [32760], 2),
+    ("c2 4 x 1024^2 (12 heads)", [4096] * 4, 12),
+    ("c2b varlen 4 images", [4096, 3840, 3840, 4032], 12),
+]
+
+
+@pytest.mark.parametrize("label,seqlens,H", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
+def test_attention_fullsize_sampled_rows(gs, label, seqlens, H):
+    import torch
+    d = 128
+    ctx = gs.Context(device=0)
+    g = torch.Generator(device="cuda").manual_seed(len(label))
+    N = sum(seqlens)
+    q, k, v = (torch.randn(N, H, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    o = torch.zeros_like(q)
+    off = np.cumsum([0] + seqlens[:-1]).tolist()
+    ctx.debug_attention(q, k, v, o, H, d, off, seqlens)
+    ctx.close()
+    got = from_dev_bf16(o)
+    qf, kf, vf = (from_dev_bf16(t) for t in (q, k, v))
+    for r, (o_, n) in enumerate(zip(off, seqlens)):
+        rows = sample_rows(n, k=24 if n > 10000 else 16, seed=r)
+        ref = dit.attention(qf[o_ + rows], kf[o_:o_ + n], vf[o_:o_ + n])
+        err = rel_l2(got[o_ + rows], ref)
+        assert err < TOL_ATTN, (label, r, err)
+
+
+POLY_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2604_04335_b200 as gs
+from oracle import dit
+from tests.gpu_util import from_dev_bf16, rel_l2
+ctx = gs.Context(device=0)
+H, d, seqlens = 3, 128, [1000, 129, 4096]
+g = torch.Generator(device="cuda").manual_seed(3)
+N = sum(seqlens)
+q, k, v = (torch.randn(N, H, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+q = q * 3
+o = torch.zeros_like(q)
+off = np.cumsum([0] + seqlens[:-1]).tolist()
+ctx.debug_attention(q, k, v, o, H, d, off, seqlens)
+got = from_dev_bf16(o); qf, kf, vf = (from_dev_bf16(t) for t in (q, k, v))
+for o_, n in zip(off, seqlens):
+    ref = dit.attention(qf[o_:o_ + n], kf[o_:o_ + n], vf[o_:o_ + n])
+    e = rel_l2(got[o_:o_ + n], ref)
+    assert e < 6e-3, e
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("poly8", [2, 3, 4])
+def test_attention_poly_exp2_variants(poly8):
+    """The FMA-pipe exp2 polynomial (reading 18) at each offload fraction."""
+    env = dict(os.environ, GS_ATTN_POLY8=str(poly8))
+    r = subprocess.run([sys.executable, "-c", POLY_SCRIPT.format(root=ROOT)], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+# ----------------------------------------------------------------------------- DiT block
+def _block_rows_case(gs, shape, width, height, frames, t, nrows=24):
+    ctx = gs.Context(device=0)
+    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, 1, shape.weight_seed)
+    grid = sm.token_grid(width, height, frames)
+    n = int(np.prod(grid))
+    g = np.random.default_rng(21)
+    x = g.standard_normal((n, shape.dim)).astype(np.float32)
+    out = ctx.debug_block(mid, 0, x, [grid], [0], [n], [t])
+    ctx.close()
+    glob = sm.as_f64(sm.global_params(shape))
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    e = dit.time_embedding(np.float64(np.float32(t)), glob)[1]
+    rows = sample_rows(n, k=nrows)
+    ref = dit.dit_block_rows(x.astype(np.float64), blk, e, grid, shape.heads, rows)
+    return x[rows].astype(np.float64), out[rows].astype(np.float64), ref
+
+
+def test_block_config3_fullsize_row_sampled(gs):
+    """Config 3: 480x832, 81 frames (32,760 tokens), Wan-1.3B-shaped block at SP=1."""
+    x, out, ref = _block_rows_case(gs, sm.WAN_1_3B, 832, 480, 81, 871.25)
+    err = rel_l2(out - x, ref - x)
+    assert err < TOL, err
+
+
+@pytest.mark.slow
+def test_block_config4_fullsize_row_sampled(gs):
+    """Config 4: 720x1280, 81 frames (75,600 tokens), Wan-14B-shaped block at SP=1 (the bench's
+    N=1 launch configuration).  The oracle computes LN1 and K/V for all tokens (7.9 TFLOP fp64)."""
+    x, out, ref = _block_rows_case(gs, sm.WAN_14B, 1280, 720, 81, 999.0, nrows=16)
+    err = rel_l2(out - x, ref - x)
+    assert err < TOL, err
+
+
+# ----------------------------------------------------------------------------- exactness, 720p
+def _steps(gs, ctx, mid, placements, k_each):
+    """Run a 720p/81f request through a sequence of (ranks, k) placements with preempt+resume."""
+    req = ctx.submit(mid, 1280, 720, 81, 50, 1000, placements[0])
+    for i, (ranks, k) in enumerate(zip(placements, k_each)):
+        if i:
+            ctx.preempt(req)
+            ctx.resume(req, ranks)
+        assert ctx.run_steps([req], ranks, k) == k
+    z = ctx.read_latent(req)
+    ctx.release(req)
+    return z
+
+
+def test_config4_sp8_preempt_resume_sp2_bit_exact_fullsize(gs):
+    """Config 4's scenario on the full 75,600-token grid (1-layer Wan-14B-shaped model): SP=8,
+    preempt, re-shard and resume at SP=2 on GPUs {0,1} equals the uninterrupted SP=1 run bitwise."""
+    shape = sm.WAN_14B
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, 1, shape.weight_seed)
+    z_sp1 = _steps(gs, ctx, mid, [[0]], [2])
+    z_sp8 = _steps(gs, ctx, mid, [list(range(8))], [2])
+    z_pre = _steps(gs, ctx, mid, [list(range(8)), [0, 1]], [1, 1])
+    ctx.close()
+    assert np.array_equal(z_sp8.view(np.uint32), z_sp1.view(np.uint32))
+    assert np.array_equal(z_pre.view(np.uint32), z_sp1.view(np.uint32))
+    assert np.isfinite(z_sp1).all()

@@ -1,0 +1,236 @@
+"""N>1 host logic of the SP path on CPU (no GPU): the exchange plans libgs.so computes for the
+Ulysses all-to-alls and the resume re-shard (row a17) are executed
+(1) for all positions in one process with NCCL's matching rule and (2) by two real processes over
+torch.distributed `gloo` (world_size 2), and the resulting buffers are checked against the
+layouts include/gs.h defines, re-derived here from the partition readings (readings 9,
+10): token shard i of p = [i n // p, (i+1) n // p), contiguous head split with positions < H mod p
+holding ceil(H/p) heads."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2604_04335_b200 as gs
+
+
+def shards(n, p):
+    return [(i * n // p, (i + 1) * n // p) for i in range(p)]
+
+
+def head_offsets(H, p):
+    return [j * (H // p) + min(j, H % p) for j in range(p + 1)]
+
+
+# ----------------------------------------------------------------------------- reference layouts
+def send_buffer(q, ns, p, i, H, d):
+    """Pack layout of position i: [dest j][rows_i][H_j][d] (rows_i = its shards of each request)."""
+    hoff = head_offsets(H, p)
+    offs = np.cumsum([0] + ns[:-1])
+    rows = np.concatenate([q[o + lo:o + hi] for o, n in zip(offs, ns) for lo, hi in [shards(n, p)[i]]])
+    return np.concatenate([rows[:, hoff[j]:hoff[j + 1], :].ravel() for j in range(p)])
+
+
+def execute(plans, bufs):
+    """Run per-position plans: n-th send of a to b matched with n-th recv of b from a, then copies."""
+    P = len(plans)
+    for a in range(P):
+        for b in range(P):
+            if a == b:
+                continue
+            snd = [x for x in plans[a] if x["op"] == gs.XFER_SEND and x["peer"] == b]
+            rcv = [x for x in plans[b] if x["op"] == gs.XFER_RECV and x["peer"] == a]
+            assert len(snd) == len(rcv)
+            for s, r in zip(snd, rcv):
+                assert s["width"] == r["width"] and s["rows"] == r["rows"] == 1
+                src = bufs[a][s["src_buf"]]
+                bufs[b][r["dst_buf"]][r["dst_off"]:r["dst_off"] + r["width"]] = \
+                    src[s["src_off"]:s["src_off"] + s["width"]]
+    for a in range(P):
+        for x in plans[a]:
+            if x["op"] == gs.XFER_COPY:
+                copy_block(bufs[a], x)
+
+
+def copy_block(bufs, x):
+    src, dst = bufs[x["src_buf"]], bufs[x["dst_buf"]]
+    for r in range(x["rows"]):
+        so = x["src_off"] + r * x["src_pitch"]
+        do = x["dst_off"] + r * x["dst_pitch"]
+        dst[do:do + x["width"]] = src[so:so + x["width"]]
+
+
+CASES = [
+    (1, [256], 6, 4), (2, [4096 // 64], 12, 8), (2, [33, 17, 64], 12, 8), (4, [1001], 40, 4),
+    (8, [75600 // 100], 40, 4), (8, [32760 // 40], 12, 8), (8, [7, 300, 13], 12, 4), (4, [3], 6, 2),
+]
+
+
+@pytest.mark.parametrize("p,ns,H,d", CASES)
+def test_a2a_plans_realise_ulysses_layouts(p, ns, H, d):
+    g = np.random.default_rng(p * 1000 + H)
+    N = sum(ns)
+    q = g.integers(-1000, 1000, (N, H, d)).astype(np.int64)
+    o = g.integers(-1000, 1000, (N, H, d)).astype(np.int64)
+    hoff = head_offsets(H, p)
+    offs = np.cumsum([0] + ns[:-1])
+    # seq -> head
+    plans = [gs.plan_a2a(0, p, i, ns, H, d)[0] for i in range(p)]
+    bufs = [{gs.BUF_SEND: send_buffer(q, ns, p, i, H, d),
+             gs.BUF_RECV: np.full(N * (hoff[i + 1] - hoff[i]) * d, -7, np.int64)} for i in range(p)]
+    execute(plans, bufs)
+    for j in range(p):
+        want = q[:, hoff[j]:hoff[j + 1], :].ravel()
+        np.testing.assert_array_equal(bufs[j][gs.BUF_RECV], want)
+    # head -> seq
+    plans, stages = zip(*[gs.plan_a2a(1, p, i, ns, H, d) for i in range(p)])
+    bufs = []
+    for i in range(p):
+        rows_i = sum(hi - lo for n in ns for lo, hi in [shards(n, p)[i]])
+        bufs.append({gs.BUF_O: o[:, hoff[i]:hoff[i + 1], :].ravel().copy(),
+                     gs.BUF_STAGE: np.full(max(stages[i], 1), -9, np.int64),
+                     gs.BUF_ORECV: np.full(rows_i * H * d, -5, np.int64)})
+    execute(plans, bufs)
+    for i in range(p):
+        want = np.concatenate([o[of + lo:of + hi] for of, n in zip(offs, ns)
+                               for lo, hi in [shards(n, p)[i]]]).ravel()
+        np.testing.assert_array_equal(bufs[i][gs.BUF_ORECV], want)
+
+
+RESHARD = [([0], [0]), ([0, 1, 2, 3, 4, 5, 6, 7], [0, 1]), ([0, 1, 2, 3], [4, 5, 6, 7]),
+           ([0, 1], [2, 3, 4, 5]), ([4, 5, 6, 7], [0, 1, 2, 3, 4, 5, 6, 7]), ([1, 0], [0, 1]),
+           ([3], [0, 1, 2, 3]), ([6, 7], [6])]
+
+
+@pytest.mark.parametrize("old,new", RESHARD)
+@pytest.mark.parametrize("n", [75600 // 50, 1001, 5])
+def test_reshard_plans_move_exact_token_ranges(old, new, n):
+    lat = 3
+    z = np.arange(n * lat, dtype=np.int64)
+    plans, bufs = [], []
+    for me in range(8):
+        plans.append(gs.plan_reshard(n, lat, old, new, me))
+        b = {}
+        if me in old:
+            lo, hi = shards(n, len(old))[old.index(me)]
+            b[gs.BUF_OLD] = z[lo * lat:hi * lat].copy()
+        if me in new:
+            lo, hi = shards(n, len(new))[new.index(me)]
+            b[gs.BUF_NEW] = np.full((hi - lo) * lat, -1, np.int64)
+        bufs.append(b)
+        if me not in old and me not in new:
+            assert plans[-1] == []
+    execute(plans, bufs)
+    for b, me in enumerate(new):
+        lo, hi = shards(n, len(new))[b]
+        np.testing.assert_array_equal(bufs[me][gs.BUF_NEW], z[lo * lat:hi * lat])
+
+
+def test_plan_rejects_bad_arguments():
+    with pytest.raises(gs.GsError):
+        gs.plan_a2a(0, 2, 2, [10], 12, 8)
+    with pytest.raises(gs.GsError):
+        gs.plan_a2a(5, 2, 0, [10], 12, 8)
+
+
+# ----------------------------------------------------------------------------- gloo, 2 processes
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run_plan_dist(dist, torch, plan, bufs):
+    """Execute one participant's plan over torch.distributed (tag = message index per peer)."""
+    reqs, nsent, nrecv = [], {}, {}
+    for x in plan:
+        if x["op"] == gs.XFER_SEND:
+            k = nsent.get(x["peer"], 0)
+            nsent[x["peer"]] = k + 1
+            t = torch.from_numpy(bufs[x["src_buf"]][x["src_off"]:x["src_off"] + x["width"]].copy())
+            reqs.append(dist.isend(t, dst=x["peer"], tag=k))
+        elif x["op"] == gs.XFER_RECV:
+            k = nrecv.get(x["peer"], 0)
+            nrecv[x["peer"]] = k + 1
+            t = torch.empty(x["width"], dtype=torch.int64)
+            reqs.append((dist.irecv(t, src=x["peer"], tag=k), t, x))
+    for r in reqs:
+        if isinstance(r, tuple):
+            r[0].wait()
+            x = r[2]
+            bufs[x["dst_buf"]][x["dst_off"]:x["dst_off"] + x["width"]] = r[1].numpy()
+        else:
+            r.wait()
+    for x in plan:
+        if x["op"] == gs.XFER_COPY:
+            copy_block(bufs, x)
+
+
+def _worker(rank, world, port, errq):
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        p, ns, H, d = 2, [37, 64, 5], 12, 4
+        N = sum(ns)
+        g = np.random.default_rng(7)      # same seed: every rank knows the global tensors
+        q = g.integers(-99, 99, (N, H, d)).astype(np.int64)
+        o = g.integers(-99, 99, (N, H, d)).astype(np.int64)
+        hoff = head_offsets(H, p)
+        offs = np.cumsum([0] + ns[:-1])
+        me = rank
+        plan, _ = gs.plan_a2a(0, p, me, ns, H, d)
+        bufs = {gs.BUF_SEND: send_buffer(q, ns, p, me, H, d),
+                gs.BUF_RECV: np.full(N * (hoff[me + 1] - hoff[me]) * d, -7, np.int64)}
+        _run_plan_dist(dist, torch, plan, bufs)
+        np.testing.assert_array_equal(bufs[gs.BUF_RECV], q[:, hoff[me]:hoff[me + 1], :].ravel())
+        plan, stage = gs.plan_a2a(1, p, me, ns, H, d)
+        rows_me = sum(hi - lo for n in ns for lo, hi in [shards(n, p)[me]])
+        bufs = {gs.BUF_O: o[:, hoff[me]:hoff[me + 1], :].ravel().copy(),
+                gs.BUF_STAGE: np.zeros(max(stage, 1), np.int64),
+                gs.BUF_ORECV: np.zeros(rows_me * H * d, np.int64)}
+        _run_plan_dist(dist, torch, plan, bufs)
+        want = np.concatenate([o[of + lo:of + hi] for of, n in zip(offs, ns)
+                               for lo, hi in [shards(n, p)[me]]]).ravel()
+        np.testing.assert_array_equal(bufs[gs.BUF_ORECV], want)
+        # preempt at SP2 {0,1} -> resume at SP1 {1}, then back to SP2 in swapped order {1,0}
+        n, lat = 1001, 4
+        z = np.arange(n * lat, dtype=np.int64)
+        state = {0: z[:500 * lat].copy(), 1: z[500 * lat:].copy()}[me]
+        for old, new in (([0, 1], [1]), ([1], [1, 0]), ([1, 0], [0, 1])):
+            plan = gs.plan_reshard(n, lat, old, new, me)
+            bufs = {}
+            if me in old:
+                bufs[gs.BUF_OLD] = state
+            if me in new:
+                lo, hi = shards(n, len(new))[new.index(me)]
+                bufs[gs.BUF_NEW] = np.full((hi - lo) * lat, -1, np.int64)
+            _run_plan_dist(dist, torch, plan, bufs)
+            state = bufs.get(gs.BUF_NEW)
+            if me in new:
+                lo, hi = shards(n, len(new))[new.index(me)]
+                np.testing.assert_array_equal(state, z[lo * lat:hi * lat])
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        errq.put(f"rank {rank}: {e!r}\n{traceback.format_exc()}")
+
+
+def test_two_process_gloo_exchange_and_reshard():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, errq)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, "\n".join(errs)
+    assert all(pr.exitcode == 0 for pr in procs)
