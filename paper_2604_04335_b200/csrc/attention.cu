@@ -3,9 +3,9 @@
 //
 // Design (B200-first; FlashAttention-4-style structure, written from scratch):
 //   * one CTA = one head x two 128-row Q tiles of one request (256 query rows);
-//   * warp 0: TMA producer (Q once; K_j, V_j into a 2-stage ring, 128B swizzle);
-//   * warp 1: TMEM owner + single-thread tcgen05.mma issuer;
-//   * warps 4..7 / 8..11: softmax warpgroups WG0 / WG1, one thread per query row;
+//   * warps 0..3 / 4..7: softmax warpgroups WG0 / WG1, one thread per query row;
+//   * warp 8: TMA producer (Q once; K_j into a 3-slot ring, V_j into a 2-slot ring, 128B swizzle);
+//   * warp 9: TMEM owner + single-thread tcgen05.mma issuer;
 //   * TMEM (512 cols): S_w = Q_w K_j^T at cols [128w, 128w+128) (fp32), P_w (bf16 pairs)
 //     written over S_w cols [128w, 128w+64), O_w at cols [256+128w, 256+128w+d);
 //   * MMA issue order S0_0, S1_0, {PV0_j, S0_{j+1}, PV1_j, S1_{j+1}}: WG0's softmax of tile j+1
@@ -35,6 +35,10 @@ namespace {
 
 constexpr int MAX_REQ = 64;
 constexpr int THREADS = 384;
+// Warp roles.  The SMSP arbiter issues highest-warp-id first, so the latency-critical producer
+// and MMA-issuer warps take the highest ids (8, 9) and are never starved by the softmax warps
+// (0-3: Q tile 0, 4-7: Q tile 1) sharing their SMSPs; warps 10, 11 idle.
+constexpr int kProducerWarp = 8, kMmaWarp = 9;
 
 struct SeqTable {
   int nreq;
@@ -58,6 +62,16 @@ struct Cfg {
 };
 
 
+// Which of every 8 exp2 pairs go to the FMA-pipe polynomial: spread out so the polynomial's FMA /
+// ALU instructions fill the 8-cycle MUFU issue gaps of the neighbouring pairs.
+template <int POLY8>
+__device__ __forceinline__ constexpr bool poly_pair(int k) {
+  return POLY8 == 0 ? false
+       : POLY8 == 2 ? (k == 2 || k == 6)
+       : POLY8 == 3 ? (k == 1 || k == 4 || k == 6)
+       : (k & 1) == 1;
+}
+
 // P = exp2(S * scale - m) for the 128 columns of this thread's row, packed to bf16 pairs and
 // stored over the S columns [0, 64) in TMEM (P aliases S).  Returns the fp32 partial row sums.
 // FULL = false is the last (partial) KV tile of a request: masked columns get p = 0 exactly.
@@ -75,7 +89,7 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[128], float
           __ffma2_rn(make_float2(__uint_as_float(v[col]), __uint_as_float(v[col + 1])), sc2, nm2);
       // exp2: MUFU for most pairs, FMA-pipe polynomial for POLY8 of every 8 pairs (reading 18)
       float2 p;
-      if ((i & 7) >= 8 - POLY8) {
+      if (poly_pair<POLY8>(i & 7)) {
         p = exp2_poly2(x);
       } else {
         p.x = ex2_approx(x.x);
@@ -144,12 +158,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == kProducerWarp && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -158,9 +172,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   // register split: producer / MMA warpgroup shrinks, the two softmax warpgroups grow.  The CTA
   // pool is 384 x 168 (launch allocation): 4 warps x 32 x (168 - 80) = 11264 freed >= 8 warps x
   // 32 x (208 - 168) = 10240 requested (an unsatisfiable .inc would block forever).
-  if (warp < 4) {
+  if (warp >= 8) {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
-  if (warp == 0) {
+  if (warp == kProducerWarp) {
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
       for (int w = 0; w < 2; ++w)
@@ -183,7 +197,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           tma_load_3d(&tmV, &vfull[vs], sv + b * 16384, b * 64, head, kv_off + j * 128);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
+    // Single MMA issuer.  Its fixed order PV0_j, S0_j+1, PV1_j, S1_j+1 keeps the two softmax
+    // warpgroups half a period apart (ping-pong: one group's exp work overlaps the other's MMAs);
+    // independent per-group issuers were measured to fall into lock-step (profiles/r01_notes.md).
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
@@ -191,13 +208,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t sk0 = smem_u32(smem + C::K_OFF);
       const uint32_t sv0 = smem_u32(smem + C::V_OFF);
       mbar_wait(q_full, 0);
-      auto issue_s = [&](int w, int j) {
-        const int s = j % C::KST;
-        mbar_wait(&kfull[s], (j / C::KST) & 1);
-        tc_fence_after();
+      // issue without waiting: callers wait for K_j (kfull) / V_j (vfull) + P (pfull) first
+      auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T -> TMEM cols [128 w, 128 w + 128)
         TRACE_EV(0, w, j);
         const uint32_t qa = sq + w * C::TILE_BYTES;
-        const uint32_t kb = sk0 + s * C::TILE_BYTES;
+        const uint32_t kb = sk0 + (j % C::KST) * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
@@ -205,30 +220,43 @@ __global__ void __launch_bounds__(THREADS, 1)
                  idesc_s, kk > 0);
         }
         mma_commit(&sfull[w]);
+        TRACE_EV(13, w, j);
       };
-      auto issue_pv = [&](int w, int j) {
-        const int s = j % C::VST;
-        mbar_wait(&vfull[s], (j / C::VST) & 1);  // normally long complete: check it first
-        mbar_wait(&pfull[w], j & 1);
-        TRACE_EV(10, w, j);
-        tc_fence_after();
+      auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j, P_w read from TMEM (bf16 over S_w)
         TRACE_EV(1, w, j);
-        const uint32_t vb = sv0 + s * C::TILE_BYTES;
+        const uint32_t vb = sv0 + (j % C::VST) * C::TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           mma_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
                  idesc_o, (j > 0) || (kk > 0));
         }
+        TRACE_EV(14, w, j);
       };
+      auto wait_p = [&](int w, int j) {
+        TRACE_EV(12, w, j);
+        mbar_wait_spin(&pfull[w], j & 1);
+        TRACE_EV(10, w, j);
+        tc_fence_after();
+      };
+      mbar_wait_spin(&kfull[0], 0);
+      tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
       mma_commit(&kempty[0]);
       for (int j = 0; j < nkv; ++j) {
+        const bool more = j + 1 < nkv;
+        // V_j and K_{j+1} landed long ago in steady state: check them before waiting on P
+        TRACE_EV(15, 0, j);
+        mbar_wait_spin(&vfull[j % C::VST], (j / C::VST) & 1);
+        if (more) mbar_wait_spin(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
+        TRACE_EV(11, 0, j);
+        wait_p(0, j);
         issue_pv(0, j);
-        if (j + 1 < nkv) issue_s(0, j + 1);
+        if (more) issue_s(0, j + 1);
+        wait_p(1, j);
         issue_pv(1, j);
         mma_commit(&vempty[j % C::VST]);
-        if (j + 1 < nkv) {
+        if (more) {
           issue_s(1, j + 1);
           mma_commit(&kempty[(j + 1) % C::KST]);
         }
@@ -239,7 +267,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
-    const int w = (warp - 4) >> 2;  // softmax warpgroup
+    const int w = warp >> 2;  // softmax warpgroup
     const int quarter = warp & 3;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     const uint32_t tS = tmem + lane_base + w * 128;
@@ -265,17 +293,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < 128; ++i)
           if (i >= kv_valid) v[i] = __float_as_uint(-INFINITY);
       }
-      // row max: 4 independent FMNMX3 chains
-      float mx0 = __uint_as_float(v[0]), mx1 = __uint_as_float(v[1]);
-      float mx2 = __uint_as_float(v[2]), mx3 = __uint_as_float(v[3]);
+      // row max: 8 independent FMNMX3 chains (a 3-level tree over 128 values)
+      float mx[8];
 #pragma unroll
-      for (int i = 4; i < 128; i += 8) {
-        mx0 = fmax3(mx0, __uint_as_float(v[i + 0]), __uint_as_float(v[i + 1]));
-        mx1 = fmax3(mx1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
-        mx2 = fmax3(mx2, __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
-        mx3 = fmax3(mx3, __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
-      }
-      const float m_tile = fmax3(mx0, mx1, fmaxf(mx2, mx3)) * scale_log2;
+      for (int c = 0; c < 8; ++c) mx[c] = fmax3(__uint_as_float(v[16 * c]), __uint_as_float(v[16 * c + 1]),
+                                                __uint_as_float(v[16 * c + 2]));
+#pragma unroll
+      for (int i = 3; i < 15; i += 2)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          mx[c] = fmax3(mx[c], __uint_as_float(v[16 * c + i]), __uint_as_float(v[16 * c + i + 1]));
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mx[c] = fmaxf(mx[c], __uint_as_float(v[16 * c + 15]));
+      const float m_tile =
+          fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * scale_log2;
       // lazy rescale: move the reference max only when it grows by more than 2^8
       const bool need = m_tile > m_run + 8.0f;
       const float alpha = need ? ex2_approx(m_run - m_tile) : 1.0f;
@@ -301,8 +332,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) TRACE_EV(4 + quarter, w, j);
+      const long long t_done = TRACE ? clock64() : 0;
       if (lane == 0) mbar_arrive(&pfull[w]);
+      if (TRACE && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && j < 32)
+        g_attn_trace[((4 + quarter) * 32 + j) * 2 + w] = t_done;
     }
     // epilogue: O / l -> bf16 -> global
     mbar_wait(&ofull[w], 0);
@@ -328,7 +361,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
   }
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     __syncwarp();
     tc_fence_after();
     tmem_dealloc(tmem, 512);

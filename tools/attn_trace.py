@@ -31,6 +31,22 @@ for q in range(4):
     print(f"WG0 q{q} T_s median", np.median(t[4 + q, 4:30, 0] - t[2, 4:30, 0]),
           f"WG1 q{q} T_s median", np.median(t[4 + q, 4:30, 1] - t[2, 4:30, 1]))
 print("issue_S(j+1) -> wake(j+1) median", np.median(t[2, 5:30, 0] - t[0, 5:30, 0]))
+print("issue_S: kfull wait (cycles) median", np.median(t[0, 4:30, 0] - t[11, 4:30, 0]), np.median(t[0, 4:30, 1] - t[11, 4:30, 1]))
+print("issue_PV: vfull+pfull wait median", np.median(t[10, 4:30, 0] - t[12, 4:30, 0]), np.median(t[10, 4:30, 1] - t[12, 4:30, 1]))
+print("PV0 issue -> S0(j+1) pre-wait median", np.median(t[11, 5:30, 0] - t[1, 4:29, 0]))
+print("timeline (cycles rel. to issue_PV0(j) start), WG0 then WG1:")
+for j in range(20, 24):
+    for w in range(2):
+        b = t[1, j, w]
+        ev = [("PV_issue_end", t[14, j, w]), ("S(j+1)_issue", t[0, j + 1, w]), ("S(j+1)_issue_end", t[13, j + 1, w]),
+              ("wake(j+1)", t[2, j + 1, w]), ("loaded", t[3, j + 1, w]),
+              ("Pdone q0..q3", max(t[4 + q, j + 1, w] for q in range(4))), ("pfull_ok", t[10, j + 1, w]),
+              ("PV(j+1)_issue", t[1, j + 1, w])]
+        print(f" j={j} WG{w}: " + ", ".join(f"{n} {v - b:+d}" for n, v in ev))
+for j in range(20, 24):
+    b = t[1, j, 0]
+    print(f" loop head j={j}: start {t[15, j, 0] - b:+d} kv-ok {t[11, j, 0] - b:+d} "
+          f"pfull0-ok {t[10, j, 0] - b:+d}  (prev S0 issue end {t[13, j, 0] - b:+d})")
 for j in range(20, 26):
     print(f"tile {j}: K issued {t[8, j, 0] - t0}  V issued {t[9, j, 0] - t0}  MMA pfull0-ok {t[10, j, 0] - t0} "
           f"PV0 issued {t[1, j, 0] - t0}  pfull1-ok {t[10, j, 1] - t0} PV1 issued {t[1, j, 1] - t0}")
