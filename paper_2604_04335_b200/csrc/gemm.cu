@@ -107,6 +107,18 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int row,
   }
 }
 
+// Tile rasterisation: bands of GROUP_M M-tiles, N-major inside a band, so the ~148 tiles in
+// flight cover a GROUP_M x (148 / GROUP_M) block whose A and W panels stay resident in L2.
+constexpr int GROUP_M = 16;
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
+  const int per_group = GROUP_M * num_n;
+  const int g = t / per_group, r = t - g * per_group;
+  const int m0 = g * GROUP_M;
+  const int gm = min(GROUP_M, num_m - m0);
+  mb = m0 + r % gm;
+  nb = r / gm;
+}
+
 template <int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -150,7 +162,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int mb = t % num_m, nb = t / num_m;
+        int mb, nb;
+        tile_coords(t, num_m, num_n, mb, nb);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -195,7 +208,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int quarter = warp & 3;
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
-      const int mb = t % num_m, nb = t / num_m;
+      int mb, nb;
+      tile_coords(t, num_m, num_n, mb, nb);
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
