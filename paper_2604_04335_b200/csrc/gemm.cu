@@ -22,13 +22,19 @@
 namespace gs {
 
 namespace {
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+// CTA-pair (cta_group::2) tiles: the pair computes 256 x 256 outputs with M=256 N=256 K=16 MMAs
+// issued by the leader CTA; each CTA stages its 128 A rows and its 128-row half of W per stage,
+// and holds its 128 output rows x 256 fp32 columns in its own TMEM.
+constexpr int BM = 128;                     // output rows per CTA (pair tile: 256)
+constexpr int BN = 256;                     // output columns per pair tile
+constexpr int PM = 2 * BM;                  // pair tile rows
+constexpr int BK = 64, STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;        // 16 KB
+constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB: this CTA's half of the W tile
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 192;
-constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t TMEM_COLS = 512;         // 2 accumulators x 256 columns
 
 __device__ __forceinline__ float gelu_tanh_f(float u) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -120,30 +126,32 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, const __grid_constant__ EpiParams ep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* full = bars;                 // [STAGES]
-  uint64_t* empty = bars + STAGES;       // [STAGES]
-  uint64_t* tfull = bars + 2 * STAGES;   // [2]
-  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
+  uint64_t* full = bars;                     // [STAGES] (leader's are used: both CTAs' bytes)
+  uint64_t* empty = bars + STAGES;           // [STAGES] per CTA (multicast commit)
+  uint64_t* tfull = bars + 2 * STAGES;       // [2] per CTA (multicast commit)
+  uint64_t* tempty = bars + 2 * STAGES + 2;  // [2] leader's: 4 epilogue warps x 2 CTAs
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int num_m = (M + BM - 1) / BM, num_n = (N + BN - 1) / BN;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int num_m = (M + PM - 1) / PM, num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n, num_k = K / BK;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 128);
+      mbar_init(&tempty[s], 8);
     }
     fence_barrier_init();
   }
@@ -151,36 +159,36 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0) {  // producer (both CTAs): this CTA's A rows and W half, bytes counted by the leader
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = pair; t < num_tiles; t += npairs) {
         int mb, nb;
         tile_coords(t, num_m, num_n, mb, nb);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(&tmA, &full[stage], sa, kb * BK, mb * BM);
-          tma_load_2d(&tmB, &full[stage], sa + A_BYTES, kb * BK, nb * BN);
+          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&full[stage]), 0), STAGE_BYTES);
+          tma_load_2d_2sm(&tmA, &full[stage], sa, kb * BK, mb * PM + rank * BM);
+          tma_load_2d_2sm(&tmB, &full[stage], sa + A_BYTES, kb * BK, nb * BN + rank * (BN / 2));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(BM, BN, 0, 0);
+    if (lane == 0 && rank == 0) {  // MMA issuer: leader CTA only
+      constexpr uint32_t idesc = idesc_bf16(PM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      for (int t = pair; t < num_tiles; t += npairs, ++it) {
         const int as = it & 1;
         const uint32_t aphase = (it >> 1) & 1;
         mbar_wait(&tempty[as], aphase ^ 1);
@@ -192,29 +200,28 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = sdesc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t bd = sdesc_sw128(sb + kk * 32, 16, 1024);
-            mma_ss(d_tmem, ad, bd, idesc, (kb | kk) != 0);
-          }
-          mma_commit(&empty[stage]);
+          for (int kk = 0; kk < BK / 16; ++kk)
+            mma_ss_2sm(d_tmem, sdesc_sw128(sa + kk * 32, 16, 1024), sdesc_sw128(sb + kk * 32, 16, 1024), idesc,
+                       (kb | kk) != 0);
+          mma_commit_2sm_mc(&empty[stage], 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[as]);
+        mma_commit_2sm_mc(&tfull[as], 0x3);
       }
     }
   } else {
-    // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    // epilogue (both CTAs): warps 2..5 -> TMEM lane quarter (warp % 4) of this CTA's 128 rows
     const int quarter = warp & 3;
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    for (int t = pair; t < num_tiles; t += npairs, ++it) {
       int mb, nb;
       tile_coords(t, num_m, num_n, mb, nb);
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const int row = mb * BM + quarter * 32 + lane;
+      const int row = mb * PM + rank * BM + quarter * 32 + lane;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * BN;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -226,14 +233,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (row < M) epilogue_chunk<EPI>(r, row, col0, ep);
       }
       tc_fence_before();
-      mbar_arrive(&tempty[as]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + as * 8);
     }
   }
+  tc_fence_before();
   __syncthreads();
+  cluster_sync();  // the peer may still read our smem / arrive on our barriers until here
   if (warp == 1) {
-    __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    tmem_dealloc_2sm(tmem_base, TMEM_COLS);
   }
 }
 
@@ -242,15 +251,16 @@ cudaError_t launch(int M, int N, int K, const void* A, int lda, const void* W, i
                    const EpiParams& ep, int num_sms, cudaStream_t stream) {
   CUtensorMap ta, tb;
   if (!make_tma_2d_bf16(&ta, A, K, M, static_cast<uint64_t>(lda) * 2, BK, BM)) return cudaErrorInvalidValue;
-  if (!make_tma_2d_bf16(&tb, W, K, N, static_cast<uint64_t>(ldw) * 2, BK, BN)) return cudaErrorInvalidValue;
+  if (!make_tma_2d_bf16(&tb, W, K, N, static_cast<uint64_t>(ldw) * 2, BK, BN / 2)) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
+  const int tiles = ((M + PM - 1) / PM) * ((N + BN - 1) / BN);
+  const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
+  const int grid = 2 * pairs;  // clusters of 2 (CTA pairs on one TPC)
   gemm_tc_kernel<EPI><<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
   return cudaGetLastError();
 }
