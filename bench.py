@@ -345,7 +345,10 @@ def run_gpu(args, rank, world, local_rank):
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "peak_src": f"{pk['src']} bf16 sustained (kernel timed inside a long step)",
                      "frac_of_burst": round(achieved / pk["bf16"], 4),
-                     "flops_per_launch": af, "avg_launch_ms": round(attn_avg_ms, 4)},
+                     "flops_per_launch": af, "avg_launch_ms": round(attn_avg_ms, 4),
+                     "algorithmic_bytes_per_launch": 4 * sum(seqlens) * H_loc * shape.head_dim * 2,
+                     "traffic_src": "profiles/attention_traffic.json (ncu --set full, dram read+write "
+                                    "per launch at this shape)"},
         "attn_tflops": round(achieved, 1),
         "gemm_tflops": round(gemm_tflops, 1),
         "step_tflops": round(step_flops / (ms_step * 1e-3) / 1e12, 1),

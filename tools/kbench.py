@@ -28,6 +28,7 @@ ATTN = [
     ("c3 480p sp8 2h", [32760], 2, 128),
     ("c4 720p sp8 5h", [75600], 5, 128),
     ("c4 720p sp2 20h", [75600], 20, 128),
+    ("c4 720p sp1 40h", [75600], 40, 128),
 ]
 # (label, M, N, K)
 GEMM = [
