@@ -165,3 +165,53 @@ def test_config4_sp8_preempt_resume_sp2_bit_exact_fullsize(gs):
     assert np.array_equal(z_sp8.view(np.uint32), z_sp1.view(np.uint32))
     assert np.array_equal(z_pre.view(np.uint32), z_sp1.view(np.uint32))
     assert np.isfinite(z_sp1).all()
+
+
+def test_config5_mixed_coserving_trace_bit_exact(gs):
+    """Config 5 (BASELINE.json): 2 x 720p/81f videos (Wan-14B-shaped) + 6 x 1024^2 images
+    (Wan-1.3B-shaped) on 8 GPUs with SP switching and image batching, following SURVEY.md §8(d)'s
+    script (1-layer models keep it fast; every step still runs the full kernels at full token
+    counts).  Every request must end bitwise equal to running it alone, uninterrupted, at SP=1."""
+    vs, isz = sm.WAN_14B, sm.WAN_1_3B
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    mv = ctx.model_create(vs.dim, vs.heads, vs.ffn, 1, vs.weight_seed)
+    mi = ctx.model_create(isz.dim, isz.heads, isz.ffn, 1, isz.weight_seed)
+    V1 = ctx.submit(mv, 1280, 720, 81, 50, 2001, [0, 1, 2, 3])
+    V2 = ctx.submit(mv, 1280, 720, 81, 50, 2002, [4, 5, 6, 7])
+    # R0: both videos at SP4 for 2 steps
+    assert ctx.run_steps([V1], [0, 1, 2, 3], 2) == 2
+    assert ctx.run_steps([V2], [4, 5, 6, 7], 2) == 2
+    # R1: preempt V2; V1 4 -> 2 on {0,1}; three 2-image batches on GPUs 2, 3, 4 for 4 steps
+    ctx.preempt(V2)
+    ctx.resume(V1, [0, 1])
+    imgs = [ctx.submit(mi, 1024, 1024, 1, 50, 3000 + i, [2 + i // 2]) for i in range(6)]
+    for b in range(3):
+        assert ctx.run_steps(imgs[2 * b:2 * b + 2], [2 + b], 4) == 4
+    assert ctx.run_steps([V1], [0, 1], 4) == 4
+    # R2: V2 resumes at SP2 on {6,7} (re-shard 4 -> 2 across sets); V1 2 -> 4 on {0..3}
+    ctx.resume(V2, [6, 7])
+    ctx.resume(V1, [0, 1, 2, 3])
+    assert ctx.run_steps([V1], [0, 1, 2, 3], 2) == 2
+    assert ctx.run_steps([V2], [6, 7], 2) == 2
+    # R3: V2 pauses again; V1 4 -> 8
+    ctx.preempt(V2)
+    ctx.resume(V1, list(range(8)))
+    assert ctx.run_steps([V1], list(range(8)), 2) == 2
+    got = {"V1": ctx.read_latent(V1), "V2": ctx.read_latent(V2)}
+    got.update({f"I{i}": ctx.read_latent(r) for i, r in enumerate(imgs)})
+    assert ctx.query(V1)["steps_done"] == 10 and ctx.query(V2)["steps_done"] == 4
+    assert ctx.query(V2)["state"] == gs.REQ_PAUSED
+    # references: each request alone, uninterrupted, SP=1 on GPU 0
+    for name, seed, k in (("V1", 2001, 10), ("V2", 2002, 4)):
+        r = ctx.submit(mv, 1280, 720, 81, 50, seed, [0])
+        ctx.run_steps([r], [0], k)
+        ref = ctx.read_latent(r)
+        ctx.release(r)
+        assert np.array_equal(got[name].view(np.uint32), ref.view(np.uint32)), name
+    for i in range(6):
+        r = ctx.submit(mi, 1024, 1024, 1, 50, 3000 + i, [0])
+        ctx.run_steps([r], [0], 4)
+        ref = ctx.read_latent(r)
+        ctx.release(r)
+        assert np.array_equal(got[f"I{i}"].view(np.uint32), ref.view(np.uint32)), f"I{i}"
+    ctx.close()
