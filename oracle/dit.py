@@ -26,6 +26,14 @@ e = W_p SiLU(e0) + b_p; L blocks; head v = (LN(x)(1+hsc)+hsh) W_head^T + b_head 
 (hsh, hsc) = M_head + e0; Euler z <- z + (sigma_{i+1} - sigma_i) v;
 sigma_i = s u_i / (1 + (s-1) u_i), u_i = 1 - i/S, s = 5 (FlowMatch Euler, reading 5).
 
+Text cross-attention + CFG (the paper's blocks have cross-attention,
+P:135 §2.1, and its VideoState carries prompt embeddings, P:759 / Tab. paused_memory; DESIGN.md
+readings 19-21): after the self-attention residual,
+  x <- x + (softmax(q k^T / sqrt d) v) W_co^T + b_co,  q = RMS(LN_aff(x) W_cq^T + b_cq) g_cq,
+  [k|v] = c W_ckv^T + b_ckv, k <- RMS(k) g_ck,  c = W_te2 GELU_tanh(W_te1 emb + b) + b,
+with LN_aff = LN(x) * ln3_w + ln3_b (no modulation, no gate, no RoPE); classifier-free guidance
+v = v_u + g (v_c - v_u) from the forwards with the cond / uncond prompt embeddings.
+
 Parity pins: tests/test_oracle_pins.py (brute force, closed forms, invariants, the
 paper's Tab.3 cost model).  Parity unpinned: agreement with the *trained* Wan/SD3.5
 models (no trained weights exist here).
@@ -129,13 +137,44 @@ def attention(q, k, v):
 
 
 # --------------------------------------------------------------------------------------
+# text cross-attention (NEXT-1)
+# --------------------------------------------------------------------------------------
+def text_embedding(emb, glob):
+    """c = W_te2 GELU_tanh(W_te1 emb + b_te1) + b_te2 for prompt embeddings emb [L, text_dim]."""
+    return linear(gelu_tanh(linear(emb, glob["w_te1"], glob["b_te1"])), glob["w_te2"], glob["b_te2"])
+
+
+def layer_norm_affine(x, w, b, eps=EPS):
+    """LN with elementwise affine (Wan norm3, cross_attn_norm=True [ext])."""
+    return layer_norm(x, eps) * w + b
+
+
+def cross_kv(c, blk, heads):
+    """Per-layer context keys / values of one prompt: k = RMS(c W_ck^T + b) g_ck, v = c W_cv^T + b."""
+    L, D = c.shape
+    kv = linear(c, blk["w_ckv"], blk["b_ckv"])
+    k = rms_norm(kv[:, :D], blk["g_ck"])
+    return k.reshape(L, heads, D // heads), kv[:, D:].reshape(L, heads, D // heads)
+
+
+def cross_attention(x, blk, c, heads):
+    """Cross-attention branch of rows x [n, D] of one request branch against its context c."""
+    n, D = x.shape
+    d = D // heads
+    a = layer_norm_affine(x, blk["ln3_w"], blk["ln3_b"])
+    q = rms_norm(linear(a, blk["w_cq"], blk["b_cq"]), blk["g_cq"]).reshape(n, heads, d)
+    k, v = cross_kv(c, blk, heads)
+    return linear(attention(q, k, v).reshape(n, D), blk["w_co"], blk["b_co"])
+
+
+# --------------------------------------------------------------------------------------
 # block
 # --------------------------------------------------------------------------------------
 def _split_mod(mod_rows):
     return [mod_rows[:, c, :] for c in range(6)]
 
 
-def dit_block(x, blk, e_req, reqs, heads):
+def dit_block(x, blk, e_req, reqs, heads, ctxs=None):
     """One DiT block over a varlen-packed batch.
 
     x      [N, D] fp64, rows of the requests concatenated in `reqs` order
@@ -143,6 +182,7 @@ def dit_block(x, blk, e_req, reqs, heads):
     e_req  [B, 6, D] time-embedding projection e(t_r) per request (M_l added here)
     reqs   list of (offset, n, grid_or_pos) per request; grid = (F_lat, H_t, W_t) or an
            explicit [n, 3] int array of (f, h, w) RoPE positions
+    ctxs   (cross-attention models) per-request text context c [L, D] (text_embedding output)
     """
     N, D = x.shape
     d = D // heads
@@ -165,12 +205,15 @@ def dit_block(x, blk, e_req, reqs, heads):
         vh = v[off:off + n].reshape(n, heads, d)
         o[off:off + n] = attention(qh, kh, vh)
     x = x + g1 * linear(o.reshape(N, D), blk["w_o"], blk["b_o"])
+    if ctxs is not None:
+        for (off, n, _g), c in zip(reqs, ctxs):
+            x[off:off + n] = x[off:off + n] + cross_attention(x[off:off + n], blk, c, heads)
     a2 = modulate(layer_norm(x), sh2, sc2)
     h = gelu_tanh(linear(a2, blk["w_1"], blk["b_1"]))
     return x + g2 * linear(h, blk["w_2"], blk["b_2"])
 
 
-def dit_block_rows(x, blk, e, grid, heads, rows):
+def dit_block_rows(x, blk, e, grid, heads, rows, ctx=None):
     """Row-sampled DiT block of ONE request (SURVEY.md §8(c) 'Large configs').
 
     Computes LN1 and K/V for all n tokens, everything else only for `rows`.
@@ -192,6 +235,8 @@ def dit_block_rows(x, blk, e, grid, heads, rows):
     q = rope_apply(q.reshape(len(rows), heads, d), rope_angles(pos[rows], d))
     o = attention(q, k, v).reshape(len(rows), D)
     xr = x[rows] + g1 * linear(o, blk["w_o"], blk["b_o"])
+    if ctx is not None:
+        xr = xr + cross_attention(xr, blk, ctx, heads)
     a2 = modulate(layer_norm(xr), sh2, sc2)
     return xr + g2 * linear(gelu_tanh(linear(a2, blk["w_1"], blk["b_1"])), blk["w_2"], blk["b_2"])
 
@@ -238,8 +283,8 @@ def euler(z, v, sig_i, sig_next):
     return z + (sig_next - sig_i) * v
 
 
-def dit_velocity(z_list, grids, ts, glob, blocks, heads):
-    """DiT forward of a batch: z_list[r] [n_r, 64], t_r -> velocity list."""
+def dit_velocity(z_list, grids, ts, glob, blocks, heads, ctxs=None):
+    """DiT forward of a batch: z_list[r] [n_r, 64], t_r (and text context c_r) -> velocity list."""
     offs, reqs = 0, []
     for z, g in zip(z_list, grids):
         reqs.append((offs, z.shape[0], g))
@@ -249,21 +294,39 @@ def dit_velocity(z_list, grids, ts, glob, blocks, heads):
     e0s, es = zip(*(time_embedding(t, glob) for t in ts))
     e_req = np.stack(es)
     for blk in blocks:
-        x = dit_block(x, blk, e_req, reqs, heads)
+        x = dit_block(x, blk, e_req, reqs, heads, ctxs)
     e0_rows = np.concatenate([np.broadcast_to(e0s[r], (n, e0s[r].shape[0]))
                               for r, (_o, n, _g) in enumerate(reqs)])
     v = head(x, e0_rows, glob)
     return [v[o:o + n] for o, n, _g in reqs]
 
 
-def dit_steps(z_list, grids, step_idx, n_steps, k, glob, blocks, heads, shift=5.0):
-    """Run k denoising steps of a batch; request r is at step index step_idx[r] of n_steps."""
+def cfg_velocity(v_cond, v_uncond, g):
+    """Classifier-free guidance v = v_u + g (v_c - v_u) (reading 21)."""
+    return v_uncond + g * (v_cond - v_uncond)
+
+
+def dit_steps(z_list, grids, step_idx, n_steps, k, glob, blocks, heads, shift=5.0, prompts=None,
+              cfg=None):
+    """Run k denoising steps of a batch; request r is at step index step_idx[r] of n_steps.
+
+    prompts[r] = (emb_cond, emb_uncond or None) prompt embeddings (cross-attention models);
+    cfg[r] = guidance scale g_r (CFG when emb_uncond is given)."""
     z_list = [np.asarray(z, dtype=np.float64) for z in z_list]
     sig = sigmas(n_steps, shift)
     step_idx = list(step_idx)
+    ctx_c = ctx_u = None
+    if prompts is not None:
+        ctx_c = [text_embedding(pc, glob) for pc, _pu in prompts]
+        ctx_u = [None if pu is None else text_embedding(pu, glob) for _pc, pu in prompts]
     for _ in range(k):
         ts = [1000.0 * sig[i] for i in step_idx]
-        vs = dit_velocity(z_list, grids, ts, glob, blocks, heads)
+        vs = dit_velocity(z_list, grids, ts, glob, blocks, heads, ctx_c)
+        if ctx_u is not None and any(c is not None for c in ctx_u):
+            for r, cu in enumerate(ctx_u):
+                if cu is not None:
+                    vu = dit_velocity([z_list[r]], [grids[r]], [ts[r]], glob, blocks, heads, [cu])[0]
+                    vs[r] = cfg_velocity(vs[r], vu, cfg[r])
         z_list = [euler(z, v, sig[i], sig[i + 1]) for z, v, i in zip(z_list, vs, step_idx)]
         step_idx = [i + 1 for i in step_idx]
     return z_list

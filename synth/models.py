@@ -5,12 +5,12 @@ configs, marked [ext] there).  Token grid: SURVEY.md §8 "Token grids" — Wan2.
 stride (4, 8, 8), patch (1, 2, 2): n = F_lat * (h/16) * (w/16), F_lat = 1 + (frames-1)/4,
 64 latent floats per token.
 """
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 
 from .rng import (GLOBAL_SEED_OFFSET, TID, gain_bf16_bits, linear_weight_bits, modulation_f32,
-                  vector_bf16_bits)
+                  prompt_embeds_bits, vector_bf16_bits)
 
 
 @dataclass(frozen=True)
@@ -23,14 +23,19 @@ class ModelShape:
     lat: int = 64            # P_lat = C * pt * ph * pw = 16 * 1 * 2 * 2
     freq_dim: int = 256      # sinusoidal time-embedding width (Wan [ext])
     weight_seed: int = 1234
+    cross_attn: bool = False  # NEXT-1: text cross-attention in every block (Wan2.1 [ext])
+    text_len: int = 512       # umT5 context length (Wan [ext])
+    text_dim: int = 4096      # umT5 width (Wan [ext])
 
     @property
     def head_dim(self):
         return self.dim // self.heads
 
     def with_layers(self, layers):
-        return ModelShape(self.name, self.dim, self.heads, self.ffn, layers, self.lat,
-                          self.freq_dim, self.weight_seed)
+        return replace(self, layers=layers)
+
+    def with_text(self, text_len=512, text_dim=4096):
+        return replace(self, cross_attn=True, text_len=text_len, text_dim=text_dim)
 
 
 TINY = ModelShape("tiny", 384, 6, 1536, 1)
@@ -67,7 +72,31 @@ def block_params(shape: ModelShape, layer: int):
         "w_2": linear_weight_bits(s, TID["w_2"], D, F),
         "b_2": vector_bf16_bits(s, TID["b_2"], D),
         "mod": modulation_f32(s, TID["mod"], 6, D),
+        **(cross_block_params(shape, layer) if shape.cross_attn else {}),
     }
+
+
+def cross_block_params(shape: ModelShape, layer: int):
+    """Text cross-attention tensors of block `layer` (NEXT-1)."""
+    s = shape.weight_seed + layer
+    D = shape.dim
+    return {
+        "ln3_w": gain_bf16_bits(s, TID["ln3_w"], D),
+        "ln3_b": vector_bf16_bits(s, TID["ln3_b"], D),
+        "w_cq": linear_weight_bits(s, TID["w_cq"], D, D),
+        "b_cq": vector_bf16_bits(s, TID["b_cq"], D),
+        "w_ckv": linear_weight_bits(s, TID["w_ckv"], 2 * D, D),
+        "b_ckv": vector_bf16_bits(s, TID["b_ckv"], 2 * D),
+        "g_cq": gain_bf16_bits(s, TID["g_cq"], D),
+        "g_ck": gain_bf16_bits(s, TID["g_ck"], D),
+        "w_co": linear_weight_bits(s, TID["w_co"], D, D),
+        "b_co": vector_bf16_bits(s, TID["b_co"], D),
+    }
+
+
+def prompt_embeds(shape: ModelShape, prompt_seed: int, branch: int):
+    """Synthetic prompt embeddings [text_len, text_dim] (bf16 bits) of one CFG branch."""
+    return prompt_embeds_bits(prompt_seed, branch, shape.text_len, shape.text_dim)
 
 
 def global_params(shape: ModelShape):
@@ -85,6 +114,10 @@ def global_params(shape: ModelShape):
         "mod_head": modulation_f32(s, TID["mod_head"], 2, D),
         "w_head": linear_weight_bits(s, TID["w_head"], P, D),
         "b_head": vector_bf16_bits(s, TID["b_head"], P),
+        **({"w_te1": linear_weight_bits(s, TID["w_te1"], D, shape.text_dim),
+            "b_te1": vector_bf16_bits(s, TID["b_te1"], D),
+            "w_te2": linear_weight_bits(s, TID["w_te2"], D, D),
+            "b_te2": vector_bf16_bits(s, TID["b_te2"], D)} if shape.cross_attn else {}),
     }
 
 

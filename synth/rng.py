@@ -29,8 +29,13 @@ TID = {
     # global
     "w_pe": 20, "b_pe": 21, "w_t1": 22, "b_t1": 23, "w_t2": 24, "b_t2": 25,
     "w_tp": 26, "b_tp": 27, "mod_head": 28, "w_head": 29, "b_head": 30,
-    # request noise (seed = noise_seed)
-    "noise": 0,
+    # per block, text cross-attention (NEXT-1; Wan2.1 block [ext])
+    "ln3_w": 12, "ln3_b": 13, "w_cq": 14, "b_cq": 15, "w_ckv": 16, "b_ckv": 17, "g_cq": 18,
+    "g_ck": 19, "w_co": 32, "b_co": 33,
+    # global, text embedding MLP (text_dim -> D -> D)
+    "w_te1": 40, "b_te1": 41, "w_te2": 42, "b_te2": 43,
+    # request noise (seed = noise_seed); prompt embeddings (seed = prompt_seed)
+    "noise": 0, "prompt_cond": 50, "prompt_uncond": 51,
 }
 GLOBAL_SEED_OFFSET = 1_000_000
 
@@ -87,6 +92,19 @@ def gain_bf16_bits(seed, tid, n):
 
 def modulation_f32(seed, tid, rows, cols):
     return (uniform_f32(seed, tid, rows * cols) * np.float32(0.5)).reshape(rows, cols)
+
+
+def normal_f32(seed, tensor_id, n):
+    """n standard-normal fp32 values: Irwin-Hall(4) of the counter uniforms, summed in fp64."""
+    u = uniform_f32(seed, tensor_id, 4 * n).astype(np.float64)
+    return (u.reshape(-1, 4).sum(axis=1) * np.sqrt(0.75)).astype(np.float32)
+
+
+def prompt_embeds_bits(prompt_seed, branch, text_len, text_dim):
+    """Synthetic text-encoder output [text_len, text_dim] as bf16 bits (branch 0 = cond,
+    1 = uncond / negative prompt): RNE_bf16 of standard-normal values."""
+    tid = TID["prompt_cond"] if branch == 0 else TID["prompt_uncond"]
+    return f32_to_bf16_bits(normal_f32(prompt_seed, tid, text_len * text_dim)).reshape(text_len, text_dim)
 
 
 def noise_latent_f32(noise_seed, n_tokens, channels=64):

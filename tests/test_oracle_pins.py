@@ -364,3 +364,124 @@ def test_head_closed_form():
     v = dit.head(x, np.broadcast_to(e0, (3, 16)), g)
     np.testing.assert_allclose(v, np.broadcast_to((g["mod_head"][0] + e0) @ g["w_head"].T
                                                   + g["b_head"], (3, 64)), atol=1e-13)
+
+
+# ----------------------------------------------------------------------------- NEXT-1: text cross-attention + CFG
+def _text_shape(D=48, H=3, L=5, T=16):
+    return sm.ModelShape("tx", D, H, 2 * D, 1, weight_seed=91).with_text(L, T)
+
+
+def _fsum_linear(x, w, b):
+    return np.array([[math.fsum(x[i, k] * w[o, k] for k in range(x.shape[1])) + b[o]
+                      for o in range(w.shape[0])] for i in range(x.shape[0])])
+
+
+def test_text_embedding_against_fsum():
+    shape = _text_shape()
+    glob = sm.as_f64(sm.global_params(shape))
+    emb = RNG.standard_normal((shape.text_len, shape.text_dim))
+    h = _fsum_linear(emb, glob["w_te1"], glob["b_te1"])
+    h = 0.5 * h * (1 + np.tanh(math.sqrt(2 / math.pi) * (h + 0.044715 * h ** 3)))
+    ref = _fsum_linear(h, glob["w_te2"], glob["b_te2"])
+    np.testing.assert_allclose(dit.text_embedding(emb, glob), ref, rtol=1e-12, atol=1e-12)
+
+
+def test_layer_norm_affine_constant_row_is_beta():
+    w, b = RNG.standard_normal(8), RNG.standard_normal(8)
+    np.testing.assert_allclose(dit.layer_norm_affine(np.full((2, 8), 3.25), w, b), np.tile(b, (2, 1)),
+                               atol=1e-12)
+
+
+def test_cross_attention_zero_query_is_mean_of_context_values():
+    """W_cq = b_cq = 0 -> q = 0 -> uniform weights over the L context tokens: every row gets
+    mean_L(c W_cv^T + b_cv) W_co^T + b_co."""
+    shape = _text_shape()
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    blk["w_cq"][:] = 0
+    blk["b_cq"][:] = 0
+    D = shape.dim
+    x = RNG.standard_normal((7, D))
+    c = RNG.standard_normal((shape.text_len, D))
+    v = c @ blk["w_ckv"][D:].T + blk["b_ckv"][D:]
+    want = v.mean(axis=0) @ blk["w_co"].T + blk["b_co"]
+    np.testing.assert_allclose(dit.cross_attention(x, blk, c, shape.heads), np.tile(want, (7, 1)),
+                               rtol=1e-10, atol=1e-10)
+
+
+def test_cross_attention_single_context_token_returns_its_value():
+    shape = _text_shape(L=1)
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    D = shape.dim
+    x = RNG.standard_normal((4, D))
+    c = RNG.standard_normal((1, D))
+    want = (c @ blk["w_ckv"][D:].T + blk["b_ckv"][D:]) @ blk["w_co"].T + blk["b_co"]
+    np.testing.assert_allclose(dit.cross_attention(x, blk, c, shape.heads), np.tile(want, (4, 1)),
+                               rtol=1e-10, atol=1e-10)
+
+
+def test_cross_attention_context_permutation_invariant_and_row_wise():
+    shape = _text_shape(L=6)
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    x = RNG.standard_normal((5, shape.dim))
+    c = RNG.standard_normal((6, shape.dim))
+    out = dit.cross_attention(x, blk, c, shape.heads)
+    perm = RNG.permutation(6)
+    np.testing.assert_allclose(dit.cross_attention(x, blk, c[perm], shape.heads), out, rtol=1e-11,
+                               atol=1e-12)
+    np.testing.assert_allclose(dit.cross_attention(x[2:4], blk, c, shape.heads), out[2:4], rtol=1e-12,
+                               atol=1e-13)
+
+
+def test_cross_attention_against_bruteforce_heads():
+    shape = _text_shape(D=12, H=2, L=4)
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    D, H, d = 12, 2, 6
+    x = RNG.standard_normal((3, D))
+    c = RNG.standard_normal((4, D))
+    a = (x - x.mean(1, keepdims=True)) / np.sqrt(x.var(1, keepdims=True) + 1e-6) * blk["ln3_w"] + blk["ln3_b"]
+    q = _fsum_linear(a, blk["w_cq"], blk["b_cq"])
+    q = q / np.sqrt((q * q).mean(1, keepdims=True) + 1e-6) * blk["g_cq"]
+    kv = _fsum_linear(c, blk["w_ckv"], blk["b_ckv"])
+    k = kv[:, :D] / np.sqrt((kv[:, :D] ** 2).mean(1, keepdims=True) + 1e-6) * blk["g_ck"]
+    o = _attention_bruteforce(q.reshape(3, H, d), k.reshape(4, H, d), kv[:, D:].reshape(4, H, d))
+    ref = _fsum_linear(o.reshape(3, D), blk["w_co"], blk["b_co"])
+    np.testing.assert_allclose(dit.cross_attention(x, blk, c, H), ref, rtol=1e-10, atol=1e-12)
+
+
+def test_block_with_cross_attention_reduces_to_self_block_when_w_co_zero():
+    shape = _text_shape()
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    blk["w_co"][:] = 0
+    blk["b_co"][:] = 0
+    grid = (1, 2, 3)
+    x = RNG.standard_normal((6, shape.dim))
+    e = RNG.standard_normal((1, 6, shape.dim)) * 0.1
+    c = RNG.standard_normal((shape.text_len, shape.dim))
+    a = dit.dit_block(x, blk, e, [(0, 6, grid)], shape.heads, [c])
+    b = dit.dit_block(x, blk, e, [(0, 6, grid)], shape.heads)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_cfg_closed_forms():
+    vc, vu = RNG.standard_normal((5, 4)), RNG.standard_normal((5, 4))
+    np.testing.assert_allclose(dit.cfg_velocity(vc, vu, 1.0), vc, rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(dit.cfg_velocity(vc, vu, 0.0), vu)
+    np.testing.assert_allclose(dit.cfg_velocity(vc, vu, 2.5) - dit.cfg_velocity(vc, vu, 1.5), vc - vu,
+                               atol=1e-12)
+
+
+def test_steps_with_cfg_scale_one_equals_cond_only():
+    shape = sm.TINY.with_layers(1).with_text(8, 32)
+    glob = sm.as_f64(sm.global_params(shape))
+    blocks = [sm.as_f64(sm.block_params(shape, 0))]
+    z = RNG.standard_normal((12, 64))
+    pc = sm.as_f64({"p": sm.prompt_embeds(shape, 4, 0)})["p"]
+    pu = sm.as_f64({"p": sm.prompt_embeds(shape, 4, 1)})["p"]
+    a = dit.dit_steps([z], [(1, 3, 4)], [3], 50, 1, glob, blocks, shape.heads, prompts=[(pc, pu)],
+                      cfg=[1.0])[0]
+    b = dit.dit_steps([z], [(1, 3, 4)], [3], 50, 1, glob, blocks, shape.heads, prompts=[(pc, None)])[0]
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-12)
+    c = dit.dit_steps([z], [(1, 3, 4)], [3], 50, 1, glob, blocks, shape.heads, prompts=[(pu, None)])[0]
+    g0 = dit.dit_steps([z], [(1, 3, 4)], [3], 50, 1, glob, blocks, shape.heads, prompts=[(pc, pu)],
+                       cfg=[0.0])[0]
+    np.testing.assert_allclose(g0, c, rtol=0, atol=1e-12)
