@@ -65,6 +65,12 @@ typedef struct {
   float eps;      /* LayerNorm / RMSNorm epsilon (1e-6)                */
   float flow_shift; /* FlowMatch shift s (5.0)                         */
   uint64_t weight_seed;
+  /* Text cross-attention in every block (the paper's DiT blocks "perform N
+   * denoising steps with cross-attention for text alignment", §2.1; Wan2.1 layout, DESIGN.md
+   * reading 19).  0 = the north-star block (self-attention + MLP only). */
+  int cross_attn;
+  int text_len;   /* context tokens (512)                                */
+  int text_dim;   /* prompt-embedding width (4096), multiple of 64       */
 } gs_model_desc;
 
 /* ------------------------------------------------------------------ context */
@@ -86,7 +92,8 @@ int gs_info(gs_ctx* ctx, int* num_sms, int* world_size, int* nlocal);
 int gs_model_create(gs_ctx* ctx, const gs_model_desc* desc, int* model_id);
 /* Copy one weight tensor to host (parity rung T1). layer = -1 for global tensors.
  * name in {w_qkv,b_qkv,g_q,g_k,w_o,b_o,w_1,b_1,w_2,b_2,mod} (block) or
- * {w_pe,b_pe,w_t1,b_t1,w_t2,b_t2,w_tp,b_tp,mod_head,w_head,b_head} (global).
+ * {w_pe,b_pe,w_t1,b_t1,w_t2,b_t2,w_tp,b_tp,mod_head,w_head,b_head} (global); cross-attention
+ * models add {ln3_w,ln3_b,w_cq,b_cq,w_ckv,b_ckv,g_cq,g_ck,w_co,b_co} and {w_te1,b_te1,w_te2,b_te2}.
  * bytes must equal the tensor size (bf16 tensors: 2 B/elem, mod tables fp32). */
 int gs_get_weight(gs_ctx* ctx, int model, int layer, const char* name, void* host, size_t bytes);
 
@@ -99,6 +106,16 @@ int gs_get_weight(gs_ctx* ctx, int model, int layer, const char* name, void* hos
 int gs_submit(gs_ctx* ctx, int model, int width, int height, int frames, int steps,
               uint64_t noise_seed, const float* init_latent, const int* ranks, int nranks,
               gs_req* out);
+/* Submit a request of a cross-attention model with its prompt (P:759 / Tab. paused_memory: the
+ * VideoState keeps the prompt embeddings).  cfg_scale > 0 runs classifier-free guidance with
+ * guidance g = cfg_scale (a cond and an uncond branch per step, v = v_u + g (v_c - v_u), DESIGN.md
+ * reading 21); cfg_scale <= 0 runs the cond branch only.  prompt_embeds: host bf16
+ * [nb][text_len][text_dim] (nb = 2 with CFG: cond, then uncond), or NULL for the synthetic prompt of
+ * prompt_seed.  Other arguments as gs_submit. */
+int gs_submit_text(gs_ctx* ctx, int model, int width, int height, int frames, int steps,
+                   uint64_t noise_seed, uint64_t prompt_seed, float cfg_scale,
+                   const float* init_latent, const void* prompt_embeds, const int* ranks,
+                   int nranks, gs_req* out);
 /* Run k steps of a batch of requests (all placed on exactly `ranks`, same model, not paused,
  * k <= remaining steps of each).  Returns after the last step completed or after the step
  * boundary at which a preemption was requested (steps actually run -> *steps_run).
@@ -182,9 +199,11 @@ int gs_debug_attention(gs_ctx* ctx, const void* q, const void* k, const void* v,
                        int nreq);
 /* One DiT block (model, layer) at p = 1 on host data: x [N, D] fp32 in/out (rows of the nreq
  * requests concatenated), grids [nreq*3] (F_t, H_t, W_t), tok_lo [nreq] first request-local
- * token of each row segment, n_rows [nreq], t [nreq] timesteps (e = time-embedding(t)). */
+ * token of each row segment, n_rows [nreq], t [nreq] timesteps (e = time-embedding(t)).
+ * Cross-attention models: prompts = host bf16 [nreq][text_len][text_dim] (one prompt per row
+ * segment); NULL otherwise. */
 int gs_debug_block(gs_ctx* ctx, int model, int layer, float* x, int nreq, const int* grids,
-                   const int* tok_lo, const int* n_rows, const float* t);
+                   const int* tok_lo, const int* n_rows, const float* t, const void* prompts);
 /* Development aid: clock64 stamps written by the first attention CTA when the environment has
  * GS_ATTN_TRACE=1 (16 events x 32 KV tiles x 2 softmax groups); n <= 1024 entries to host. */
 int gs_debug_attention_trace(unsigned long long* host, size_t n);

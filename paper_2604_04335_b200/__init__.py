@@ -27,7 +27,8 @@ class ModelDesc(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int), ("heads", ctypes.c_int), ("ffn", ctypes.c_int),
                 ("layers", ctypes.c_int), ("lat", ctypes.c_int), ("freq_dim", ctypes.c_int),
                 ("rope_theta", ctypes.c_float), ("eps", ctypes.c_float),
-                ("flow_shift", ctypes.c_float), ("weight_seed", ctypes.c_uint64)]
+                ("flow_shift", ctypes.c_float), ("weight_seed", ctypes.c_uint64),
+                ("cross_attn", ctypes.c_int), ("text_len", ctypes.c_int), ("text_dim", ctypes.c_int)]
 
 
 class Xfer(ctypes.Structure):
@@ -57,6 +58,8 @@ _SIG = {
     "gs_model_create": [_P, ctypes.POINTER(ModelDesc), _IP],
     "gs_get_weight": [_P, _I, _I, ctypes.c_char_p, _P, ctypes.c_size_t],
     "gs_submit": [_P, _I, _I, _I, _I, _I, _U64, _FP, _IP, _I, ctypes.POINTER(_U64)],
+    "gs_submit_text": [_P, _I, _I, _I, _I, _I, _U64, _U64, ctypes.c_float, _FP, _P, _IP, _I,
+                       ctypes.POINTER(_U64)],
     "gs_run_steps": [_P, ctypes.POINTER(_U64), _I, _IP, _I, _I, _IP],
     "gs_preempt": [_P, _U64, _IP],
     "gs_resume": [_P, _U64, _IP, _I],
@@ -68,7 +71,7 @@ _SIG = {
     "gs_stream": [_P, _I, ctypes.POINTER(_P)],
     "gs_debug_gemm": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _FP],
     "gs_debug_attention": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _IP, _IP, _I],
-    "gs_debug_block": [_P, _I, _I, _FP, _I, _IP, _IP, _IP, _FP],
+    "gs_debug_block": [_P, _I, _I, _FP, _I, _IP, _IP, _IP, _FP, _P],
     "gs_debug_time_embed": [_P, _I, _I, _FP, _FP, _FP],
     "gs_debug_attention_trace": [_P, ctypes.c_size_t],
     "gs_plan_a2a": [_I, _I, _I, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP,
@@ -192,8 +195,10 @@ class Context:
 
     # ---------------------------------------------------------------- models
     def model_create(self, dim, heads, ffn, layers, weight_seed=1234, lat=64, freq_dim=256,
-                     rope_theta=10000.0, eps=1e-6, flow_shift=5.0):
-        d = ModelDesc(dim, heads, ffn, layers, lat, freq_dim, rope_theta, eps, flow_shift, weight_seed)
+                     rope_theta=10000.0, eps=1e-6, flow_shift=5.0, cross_attn=False, text_len=512,
+                     text_dim=4096):
+        d = ModelDesc(dim, heads, ffn, layers, lat, freq_dim, rope_theta, eps, flow_shift, weight_seed,
+                      int(cross_attn), text_len, text_dim)
         mid = ctypes.c_int()
         self._ck(self._lib.gs_model_create(self._h, ctypes.byref(d), ctypes.byref(mid)))
         return mid.value
@@ -213,6 +218,24 @@ class Context:
             lat = init_latent.ctypes.data_as(_FP)
         self._ck(self._lib.gs_submit(self._h, model, width, height, frames, steps, noise_seed, lat,
                                      _ints(ranks), len(ranks), ctypes.byref(rid)))
+        return rid.value
+
+    def submit_text(self, model, width, height, frames, steps, noise_seed, ranks, prompt_seed=0,
+                    cfg_scale=0.0, prompt_embeds=None, init_latent=None):
+        """Cross-attention models: prompt_embeds = uint16 (bf16 bits) [nb, text_len, text_dim] or
+        None for the synthetic prompt of prompt_seed; cfg_scale > 0 enables CFG (nb = 2)."""
+        rid = ctypes.c_uint64()
+        lat = None
+        if init_latent is not None:
+            init_latent = np.ascontiguousarray(init_latent, dtype=np.float32)
+            lat = init_latent.ctypes.data_as(_FP)
+        pe = None
+        if prompt_embeds is not None:
+            prompt_embeds = np.ascontiguousarray(prompt_embeds, dtype=np.uint16)
+            pe = prompt_embeds.ctypes.data_as(ctypes.c_void_p)
+        self._ck(self._lib.gs_submit_text(self._h, model, width, height, frames, steps, noise_seed,
+                                          prompt_seed, cfg_scale, lat, pe, _ints(ranks), len(ranks),
+                                          ctypes.byref(rid)))
         return rid.value
 
     def run_steps(self, reqs, ranks, k):
@@ -281,11 +304,16 @@ class Context:
                                               d, q_rs, kv_rs, o_rs, _ints(seq_off),
                                               _ints(seq_len), len(seq_len)))
 
-    def debug_block(self, model, layer, x, grids, tok_lo, n_rows, t):
+    def debug_block(self, model, layer, x, grids, tok_lo, n_rows, t, prompts=None):
+        """prompts (cross-attention models): uint16 bf16 bits [nreq, text_len, text_dim]."""
         x = np.ascontiguousarray(x, dtype=np.float32).copy()
         flat = [g for grid in grids for g in grid]
+        pp = None
+        if prompts is not None:
+            prompts = np.ascontiguousarray(prompts, dtype=np.uint16)
+            pp = prompts.ctypes.data_as(ctypes.c_void_p)
         self._ck(self._lib.gs_debug_block(self._h, model, layer, x.ctypes.data_as(_FP), len(n_rows),
-                                          _ints(flat), _ints(tok_lo), _ints(n_rows), _fl(t)))
+                                          _ints(flat), _ints(tok_lo), _ints(n_rows), _fl(t), pp))
         return x
 
     def debug_attention_trace(self):

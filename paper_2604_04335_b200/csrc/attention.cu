@@ -42,9 +42,9 @@ constexpr int kProducerWarp = 8, kMmaWarp = 9;
 
 struct SeqTable {
   int nreq;
-  int off[MAX_REQ];
-  int len[MAX_REQ];
-  int tile_start[MAX_REQ + 1];  // prefix sum of ceil(len / 256)
+  int q_off[MAX_REQ], q_len[MAX_REQ];    // query rows of segment r
+  int kv_off[MAX_REQ], kv_len[MAX_REQ];  // key / value rows it attends to (= q for self-attention)
+  int tile_start[MAX_REQ + 1];           // prefix sum of ceil(q_len / 256)
 };
 
 template <int HD>
@@ -136,9 +136,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   int r = 0;
   while (r + 1 < tab.nreq && static_cast<int>(blockIdx.x) >= tab.tile_start[r + 1]) ++r;
   const int pair = blockIdx.x - tab.tile_start[r];
-  const int kv_off = tab.off[r], kv_len = tab.len[r];
-  const int q_row0 = kv_off + pair * 256;
-  const int q_rows = min(256, kv_len - pair * 256);
+  const int kv_off = tab.kv_off[r], kv_len = tab.kv_len[r];
+  const int q_row0 = tab.q_off[r] + pair * 256;
+  const int q_rows = min(256, tab.q_len[r] - pair * 256);
   const int nkv = (kv_len + 127) / 128;
 
   if (threadIdx.x == 0) {
@@ -370,12 +370,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 template <int HD, int POLY8>
 cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
-                   int kv_rs, int o_rs, const SeqTable& tab, int total_rows, cudaStream_t stream) {
+                   int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
   using C = Cfg<HD>;
   CUtensorMap tq, tk, tv;
-  if (!make_tma_3d_bf16(&tq, Q, HD, heads, total_rows, HD * 2ull, q_rs * 2ull, 64, 1, 128) ||
-      !make_tma_3d_bf16(&tk, K, HD, heads, total_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128) ||
-      !make_tma_3d_bf16(&tv, V, HD, heads, total_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
+  if (!make_tma_3d_bf16(&tq, Q, HD, heads, q_rows, HD * 2ull, q_rs * 2ull, 64, 1, 128) ||
+      !make_tma_3d_bf16(&tk, K, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128) ||
+      !make_tma_3d_bf16(&tv, V, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
   static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
   auto kern = trace ? attn_tc_kernel<HD, POLY8, true> : attn_tc_kernel<HD, POLY8, false>;
@@ -383,6 +383,7 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
   if (e != cudaSuccess) return e;
   const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
   dim3 grid(tab.tile_start[tab.nreq], heads);
+  if (grid.x == 0) return cudaSuccess;  // no query rows (an empty shard)
   kern<<<grid, THREADS, C::SMEM, stream>>>(tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs,
                                                           tab, scale_log2);
   return cudaGetLastError();
@@ -401,34 +402,46 @@ int poly8_setting() {
 
 template <int HD>
 cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
-                   int kv_rs, int o_rs, const SeqTable& tab, int total_rows, cudaStream_t stream) {
+                   int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
   switch (poly8_setting()) {
-    case 2: return launch_t<HD, 2>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
-    case 4: return launch_t<HD, 4>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
-    case 3: return launch_t<HD, 3>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
-    default: return launch_t<HD, 0>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
+    case 2: return launch_t<HD, 2>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
+    case 4: return launch_t<HD, 4>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
+    case 3: return launch_t<HD, 3>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
+    default: return launch_t<HD, 0>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
   }
 }
 }  // namespace
+
+cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, void* O, int heads, int d,
+                                  int q_rs, int kv_rs, int o_rs, const int* q_off, const int* q_len,
+                                  const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream) {
+  if (nreq < 1 || nreq > MAX_REQ || (d != 64 && d != 128) || heads < 1) return cudaErrorInvalidValue;
+  SeqTable tab{};
+  tab.nreq = nreq;
+  int q_rows = 1, kv_rows = 1;
+  tab.tile_start[0] = 0;
+  for (int r = 0; r < nreq; ++r) {
+    if (q_len[r] < 0 || kv_len[r] < 1) return cudaErrorInvalidValue;
+    tab.q_off[r] = q_off[r];
+    tab.q_len[r] = q_len[r];
+    tab.kv_off[r] = kv_off[r];
+    tab.kv_len[r] = kv_len[r];
+    tab.tile_start[r + 1] = tab.tile_start[r] + (q_len[r] + 255) / 256;
+    q_rows = std::max(q_rows, q_off[r] + q_len[r]);
+    kv_rows = std::max(kv_rows, kv_off[r] + kv_len[r]);
+  }
+  return d == 128 ? launch<128>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream)
+                  : launch<64>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
+}
 
 cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                          int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
                          int nreq, int num_sms, cudaStream_t stream) {
   (void)num_sms;
-  if (nreq < 1 || nreq > MAX_REQ || (d != 64 && d != 128) || heads < 1) return cudaErrorInvalidValue;
-  SeqTable tab{};
-  tab.nreq = nreq;
-  int total_rows = 0;
-  tab.tile_start[0] = 0;
-  for (int r = 0; r < nreq; ++r) {
+  for (int r = 0; r < nreq; ++r)
     if (seq_len[r] < 1) return cudaErrorInvalidValue;
-    tab.off[r] = seq_off[r];
-    tab.len[r] = seq_len[r];
-    tab.tile_start[r + 1] = tab.tile_start[r] + (seq_len[r] + 255) / 256;
-    total_rows = std::max(total_rows, seq_off[r] + seq_len[r]);
-  }
-  return d == 128 ? launch<128>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream)
-                  : launch<64>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, total_rows, stream);
+  return attention_tc_segments(Q, K, V, O, heads, d, q_rs, kv_rs, o_rs, seq_off, seq_len, seq_off, seq_len, nreq,
+                               stream);
 }
 
 }  // namespace gs

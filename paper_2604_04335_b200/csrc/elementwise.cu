@@ -231,7 +231,70 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, __nv_bfloat16* 
   }
 }
 
+__global__ void __launch_bounds__(ROW_THREADS)
+    rmsnorm_rows_kernel(const __nv_bfloat16* __restrict__ in, int ld_in, int D, const __nv_bfloat16* __restrict__ g,
+                        float eps, __nv_bfloat16* __restrict__ out) {
+  __shared__ float red[4];
+  const long long row = blockIdx.x;
+  const int nv = D >> 3;
+  const uint4* src = reinterpret_cast<const uint4*>(in + row * ld_in);
+  uint4 xv[MAXV / 2];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < MAXV / 2; ++i) {
+    const int c = threadIdx.x + i * ROW_THREADS;
+    if (c < nv) {
+      xv[i] = src[c];
+      float f[8];
+      unpack8(xv[i], f);
+      ss += ((f[0] * f[0] + f[1] * f[1]) + (f[2] * f[2] + f[3] * f[3])) +
+            ((f[4] * f[4] + f[5] * f[5]) + (f[6] * f[6] + f[7] * f[7]));
+    }
+  }
+  const float r = rsqrtf(block_sum(ss, red) / D + eps);
+  const uint4* gv = reinterpret_cast<const uint4*>(g);
+  uint4* dst = reinterpret_cast<uint4*>(out + row * D);
+#pragma unroll
+  for (int i = 0; i < MAXV / 2; ++i) {
+    const int c = threadIdx.x + i * ROW_THREADS;
+    if (c < nv) {
+      float f[8], w[8];
+      unpack8(xv[i], f);
+      unpack8(__ldg(gv + c), w);
+      dst[c] = make_uint4(pack_bf16x2(f[0] * r * w[0], f[1] * r * w[1]), pack_bf16x2(f[2] * r * w[2], f[3] * r * w[3]),
+                          pack_bf16x2(f[4] * r * w[4], f[5] * r * w[5]), pack_bf16x2(f[6] * r * w[6], f[7] * r * w[7]));
+    }
+  }
+}
+
+__global__ void cfg_euler_kernel(float* __restrict__ z, float* __restrict__ z2, const float* __restrict__ vc,
+                                 const float* __restrict__ vu, long long n, float dsig, float g) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float v = vu ? vu[i] + g * (vc[i] - vu[i]) : vc[i];
+    const float zn = z[i] + dsig * v;
+    z[i] = zn;
+    if (z2) z2[i] = zn;  // the uncond branch's copy of the shared latent
+  }
+}
+
 }  // namespace
+
+cudaError_t rmsnorm_rows(const __nv_bfloat16* in, int ld_in, int M, int D, const __nv_bfloat16* g, float eps,
+                         __nv_bfloat16* out, cudaStream_t stream) {
+  if (M == 0) return cudaSuccess;
+  if (D % 8 || ld_in % 8 || D > 8 * (MAXV / 2) * ROW_THREADS) return cudaErrorInvalidValue;
+  rmsnorm_rows_kernel<<<M, ROW_THREADS, 0, stream>>>(in, ld_in, D, g, eps, out);
+  return cudaGetLastError();
+}
+
+cudaError_t cfg_euler(float* z, float* z2, const float* vc, const float* vu, long long n, float dsig, float g,
+                      cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  cfg_euler_kernel<<<(int)blocks, 256, 0, stream>>>(z, z2, vc, vu, n, dsig, g);
+  return cudaGetLastError();
+}
 
 cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const float* sh_b,
                         const float* sc_a, const float* sc_b, int b_stride, const int* row_req,

@@ -97,6 +97,18 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int row,
       x.w += (a.w + b.w) * v[4 * q + 3];
       dst[q] = x;
     }
+  } else if constexpr (EPI == EPI_ADD_F32) {
+    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
+                                            static_cast<size_t>(row) * ep.ldo + col0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 x = dst[q];
+      x.x += v[4 * q + 0];
+      x.y += v[4 * q + 1];
+      x.z += v[4 * q + 2];
+      x.w += v[4 * q + 3];
+      dst[q] = x;
+    }
   } else if constexpr (EPI == EPI_EULER_F32) {
     const float ds = ep.dsig[ep.row_req[row]];
     float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
@@ -276,6 +288,7 @@ cudaError_t gemm_bf16_tc(int epi, int M, int N, int K, const void* A, int lda, c
     case EPI_F32: return launch<EPI_F32>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
     case EPI_RESID_F32: return launch<EPI_RESID_F32>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
     case EPI_EULER_F32: return launch<EPI_EULER_F32>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+    case EPI_ADD_F32: return launch<EPI_ADD_F32>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
     default: return cudaErrorInvalidValue;
   }
 }

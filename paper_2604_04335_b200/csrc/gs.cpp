@@ -182,6 +182,37 @@ std::vector<WSpec> block_specs(const gs_model_desc& d) {
       {"mod", 11, RNG_F32_SCALED, 6, D, 0, 0.5f},
   };
 }
+// Text cross-attention tensors (tensor ids as synth/rng.py TID)
+std::vector<WSpec> cross_specs(const gs_model_desc& d) {
+  const long long D = d.dim;
+  return {
+      {"ln3_w", 12, RNG_BF16_GAIN, 1, D, 0, 0},
+      {"ln3_b", 13, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"w_cq", 14, RNG_BF16_SCALED, D, D, (int)D, 0},
+      {"b_cq", 15, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"w_ckv", 16, RNG_BF16_SCALED, 2 * D, D, (int)D, 0},
+      {"b_ckv", 17, RNG_BF16_SCALED, 1, 2 * D, 0, 0.1f},
+      {"g_cq", 18, RNG_BF16_GAIN, 1, D, 0, 0},
+      {"g_ck", 19, RNG_BF16_GAIN, 1, D, 0, 0},
+      {"w_co", 32, RNG_BF16_SCALED, D, D, (int)D, 0},
+      {"b_co", 33, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+  };
+}
+std::vector<WSpec> text_specs(const gs_model_desc& d) {
+  const long long D = d.dim, T = d.text_dim;
+  return {
+      {"w_te1", 40, RNG_BF16_SCALED, D, T, (int)T, 0},
+      {"b_te1", 41, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+      {"w_te2", 42, RNG_BF16_SCALED, D, D, (int)D, 0},
+      {"b_te2", 43, RNG_BF16_SCALED, 1, D, 0, 0.1f},
+  };
+}
+std::vector<WSpec> all_block_specs(const gs_model_desc& d) {
+  auto v = block_specs(d);
+  if (d.cross_attn)
+    for (auto& x : cross_specs(d)) v.push_back(x);
+  return v;
+}
 std::vector<WSpec> global_specs(const gs_model_desc& d) {
   const long long D = d.dim, P = d.lat, T = d.freq_dim;
   return {
@@ -199,6 +230,13 @@ std::vector<WSpec> global_specs(const gs_model_desc& d) {
   };
 }
 
+std::vector<WSpec> all_global_specs(const gs_model_desc& d) {
+  auto v = global_specs(d);
+  if (d.cross_attn)
+    for (auto& x : text_specs(d)) v.push_back(x);
+  return v;
+}
+
 void** block_slot(BlockW& b, const char* name) {
   if (!strcmp(name, "w_qkv")) return (void**)&b.w_qkv;
   if (!strcmp(name, "b_qkv")) return (void**)&b.b_qkv;
@@ -211,6 +249,16 @@ void** block_slot(BlockW& b, const char* name) {
   if (!strcmp(name, "w_2")) return (void**)&b.w_2;
   if (!strcmp(name, "b_2")) return (void**)&b.b_2;
   if (!strcmp(name, "mod")) return (void**)&b.mod;
+  if (!strcmp(name, "ln3_w")) return (void**)&b.ln3_w;
+  if (!strcmp(name, "ln3_b")) return (void**)&b.ln3_b;
+  if (!strcmp(name, "w_cq")) return (void**)&b.w_cq;
+  if (!strcmp(name, "b_cq")) return (void**)&b.b_cq;
+  if (!strcmp(name, "w_ckv")) return (void**)&b.w_ckv;
+  if (!strcmp(name, "b_ckv")) return (void**)&b.b_ckv;
+  if (!strcmp(name, "g_cq")) return (void**)&b.g_cq;
+  if (!strcmp(name, "g_ck")) return (void**)&b.g_ck;
+  if (!strcmp(name, "w_co")) return (void**)&b.w_co;
+  if (!strcmp(name, "b_co")) return (void**)&b.b_co;
   return nullptr;
 }
 void** global_slot(Model& m, const char* name) {
@@ -225,25 +273,47 @@ void** global_slot(Model& m, const char* name) {
   if (!strcmp(name, "mod_head")) return (void**)&m.mod_head;
   if (!strcmp(name, "w_head")) return (void**)&m.w_head;
   if (!strcmp(name, "b_head")) return (void**)&m.b_head;
+  if (!strcmp(name, "w_te1")) return (void**)&m.w_te1;
+  if (!strcmp(name, "b_te1")) return (void**)&m.b_te1;
+  if (!strcmp(name, "w_te2")) return (void**)&m.w_te2;
+  if (!strcmp(name, "b_te2")) return (void**)&m.b_te2;
   return nullptr;
 }
 
 // ------------------------------------------------------------------ batch plan
+// A step's batch.  Rows are laid out per *sequence*: a request, or with classifier-free guidance
+// each of its two branches (cond, uncond), which share the latent and timestep but attend only
+// within their own branch and to their own prompt.  Row maps point at the request (`real`), so
+// time embedding, modulation, gates, RoPE grid and sigma are per request.
 struct Plan : A2aGeometry {
   int D = 0, F = 0;
   Model* m = nullptr;
-  std::vector<Request*> reqs;
+  std::vector<Request*> reqs;    // per sequence
+  std::vector<int> branch;       // CFG branch of each sequence (0 = cond, 1 = uncond)
+  std::vector<int> real;         // index of the sequence's request in ureqs
+  std::vector<Request*> ureqs;   // the batch's requests
   std::vector<int> ranks;
+  bool text = false;
 };
 
-void make_plan(Plan& P, Model* m, const std::vector<Request*>& reqs, const int* ranks, int p) {
-  std::vector<int> n(reqs.size());
-  for (size_t r = 0; r < reqs.size(); ++r) n[r] = reqs[r]->n;
+void make_plan(Plan& P, Model* m, const std::vector<Request*>& ureqs, const int* ranks, int p) {
+  P.text = m->desc.cross_attn != 0;
+  P.ureqs = ureqs;
+  P.reqs.clear();
+  P.branch.clear();
+  P.real.clear();
+  for (size_t r = 0; r < ureqs.size(); ++r)
+    for (int b = 0; b < (P.text ? ureqs[r]->nb : 1); ++b) {
+      P.reqs.push_back(ureqs[r]);
+      P.branch.push_back(b);
+      P.real.push_back(static_cast<int>(r));
+    }
+  std::vector<int> n(P.reqs.size());
+  for (size_t v = 0; v < P.reqs.size(); ++v) n[v] = P.reqs[v]->n;
   P.init(p, n.data(), static_cast<int>(n.size()), m->desc.heads, m->hd);
   P.m = m;
   P.D = m->desc.dim;
   P.F = m->desc.ffn;
-  P.reqs = reqs;
   P.ranks.assign(ranks, ranks + p);
 }
 
@@ -270,6 +340,10 @@ int prepare_rank(gs_ctx* c, const Plan& P, int i, RankArena& A) {
   }
   RET(ensure(c, A.h, rows * F * 2));
   RET(ensure(c, A.zpack, rows * lat * 4));
+  if (P.text) {
+    RET(ensure(c, A.qc, rows * D * 2));
+    RET(ensure(c, A.vbuf, rows * lat * 4));
+  }
   RET(ensure(c, A.zb, rows * lat * 2));
   RET(ensure(c, A.e0, MAX_BATCH * D * 4));
   RET(ensure(c, A.e, MAX_BATCH * 6 * D * 4));
@@ -277,14 +351,14 @@ int prepare_rank(gs_ctx* c, const Plan& P, int i, RankArena& A) {
   RET(ensure(c, A.row_req, rows * 4));
   RET(ensure(c, A.row_tok, rows * 4));
   RET(ensure(c, A.req_grid, MAX_BATCH * 3 * 4));
-  std::vector<int> rr(P.rows[i]), rt(P.rows[i]), grid(P.B * 3);
-  for (int r = 0; r < P.B; ++r) {
+  std::vector<int> rr(P.rows[i]), rt(P.rows[i]), grid(P.ureqs.size() * 3);
+  for (int r = 0; r < P.B; ++r)
     for (int t = P.lo[i][r]; t < P.hi[i][r]; ++t) {
-      rr[P.loff[i][r] + t - P.lo[i][r]] = r;
+      rr[P.loff[i][r] + t - P.lo[i][r]] = P.real[r];
       rt[P.loff[i][r] + t - P.lo[i][r]] = t;
     }
-    for (int a = 0; a < 3; ++a) grid[3 * r + a] = P.reqs[r]->grid[a];
-  }
+  for (size_t r = 0; r < P.ureqs.size(); ++r)
+    for (int a = 0; a < 3; ++a) grid[3 * r + a] = P.ureqs[r]->grid[a];
   if (P.rows[i] > 0) {
     CK(cudaMemcpyAsync(A.row_req.p, rr.data(), rr.size() * 4, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(A.row_tok.p, rt.data(), rt.size() * 4, cudaMemcpyHostToDevice, c->stream));
@@ -299,7 +373,7 @@ int move_latent(gs_ctx* c, const Plan& P, int i, RankArena& A, int dir) {
   const size_t lat = P.m->desc.lat;
   for (int r = 0; r < P.B; ++r) {
     const size_t cnt = static_cast<size_t>(P.hi[i][r] - P.lo[i][r]) * lat * 4;
-    if (!cnt) continue;
+    if (!cnt || (dir == 1 && P.branch[r] != 0)) continue;  // the cond rows carry the CFG update
     float* packed = A.zpack.as<float>() + static_cast<size_t>(P.loff[i][r]) * lat;
     float* shard = P.reqs[r]->shards[i].z;
     if (dir == 0)
@@ -490,6 +564,40 @@ int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
   return GS_OK;
 }
 
+// Text cross-attention (NEXT-1, reading 19): x += CrossAttn(LN_aff(x), context) W_co^T +
+// b_co.  Token-local: each rank's query rows attend to the request's replicated context K/V, so
+// no SP exchange is needed.
+int block_cross(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
+  const int M = P.rows[i], D = P.D, Lt = P.m->desc.text_len, NL = P.m->desc.layers;
+  const BlockW& w = P.m->blocks[l];
+  const float eps = P.m->desc.eps;
+  if (!M) return GS_OK;
+  {
+    Scope sc(c, "ln_mod", 1);
+    CK(ln_modulate(A.x.as<float>(), M, D, w.ln3_shift, P.m->zeros, w.ln3_scale_m1, P.m->zeros, 0,
+                   A.row_req.as<int>(), eps, A.a.as<bf16>(), c->stream));
+  }
+  RET(gemm(c, "gemm_cross_q", EPI_BF16, M, D, D, A.a.p, w.w_cq, epi(A.qc.p, D, w.b_cq)));
+  {
+    Scope sc(c, "rmsnorm", 1);
+    CK(rmsnorm_rows(A.qc.as<bf16>(), D, M, D, w.g_cq, eps, A.qc.as<bf16>(), c->stream));
+  }
+  const int li = local_index(c, P.ranks[i]);
+  for (int v = 0; v < P.B; ++v) {
+    const int cnt = P.hi[i][v] - P.lo[i][v];
+    if (!cnt) continue;
+    Scope sc(c, "attention_cross", 1);
+    const size_t per = static_cast<size_t>(Lt) * D;
+    const bf16* kv = P.reqs[v]->ctx_kv.at(li).as<bf16>() + (static_cast<size_t>(P.branch[v]) * NL + l) * 2 * per;
+    bf16* q = A.qc.as<bf16>() + static_cast<size_t>(P.loff[i][v]) * D;
+    const int zero = 0;
+    // in place: each CTA reads its Q tiles before it writes the same rows / head columns of O
+    CK(attention_tc_segments(q, kv, kv + per, q, P.H, P.hd, D, D, D, &zero, &cnt, &zero, &Lt, 1, c->stream));
+  }
+  RET(gemm(c, "gemm_cross_o", EPI_ADD_F32, M, D, D, A.qc.p, w.w_co, epi(A.x.p, D, w.b_co)));
+  return GS_OK;
+}
+
 int block_post(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
   const int M = P.rows[i], D = P.D, F = P.F;
   const BlockW& w = P.m->blocks[l];
@@ -500,6 +608,7 @@ int block_post(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
   eo.row_req = A.row_req.as<int>();
   const void* oin = P.p == 1 ? A.o.p : A.orecv.p;
   RET(gemm(c, "gemm_o", EPI_RESID_F32, M, D, D, oin, w.w_o, eo));
+  if (P.text) RET(block_cross(c, P, i, A, l));
   {
     Scope sc(c, "ln_mod", 1);
     if (M) CK(ln_modulate(A.x.as<float>(), M, D, w.mod + 3 * D, A.e.as<float>() + 3 * D, w.mod + 4 * D,
@@ -522,7 +631,8 @@ int step_prologue(gs_ctx* c, const Plan& P, int i, RankArena& A, const float* t)
   {
     Scope sc(c, "time_embed", 4);
     TimeEmbedW tw{m->w_t1, m->b_t1, m->w_t2, m->b_t2, m->w_tp, m->b_tp, D, m->desc.freq_dim};
-    CK(time_embed(tw, P.B, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), c->stream));
+    CK(time_embed(tw, static_cast<int>(P.ureqs.size()), t, A.temb.as<float>(), A.e0.as<float>(),
+                  A.e.as<float>(), c->stream));
   }
   {
     Scope sc(c, "patch_embed", 1);
@@ -540,10 +650,32 @@ int step_epilogue(gs_ctx* c, const Plan& P, int i, RankArena& A, const float* ds
     if (M) CK(ln_modulate(A.x.as<float>(), M, D, m->mod_head, A.e0.as<float>(), m->mod_head + D, A.e0.as<float>(), D,
                           A.row_req.as<int>(), m->desc.eps, A.a.as<bf16>(), c->stream));
   }
-  EpiParams eh = epi(A.zpack.p, m->desc.lat, m->b_head);
-  eh.row_req = A.row_req.as<int>();
-  for (int r = 0; r < P.B; ++r) eh.dsig[r] = dsig[r];
-  RET(gemm(c, "head", EPI_EULER_F32, M, m->desc.lat, D, A.a.p, m->w_head, eh));
+  if (!P.text) {
+    EpiParams eh = epi(A.zpack.p, m->desc.lat, m->b_head);
+    eh.row_req = A.row_req.as<int>();
+    for (size_t r = 0; r < P.ureqs.size(); ++r) eh.dsig[r] = dsig[r];
+    RET(gemm(c, "head", EPI_EULER_F32, M, m->desc.lat, D, A.a.p, m->w_head, eh));
+    return GS_OK;
+  }
+  // velocity of every sequence, then classifier-free guidance + Euler on the cond rows
+  RET(gemm(c, "head", EPI_F32, M, m->desc.lat, D, A.a.p, m->w_head, epi(A.vbuf.p, m->desc.lat, m->b_head)));
+  const size_t lat = m->desc.lat;
+  for (int v = 0; v < P.B; ++v) {
+    if (P.branch[v] != 0) continue;
+    const long long cnt = static_cast<long long>(P.hi[i][v] - P.lo[i][v]) * lat;
+    if (!cnt) continue;
+    const float* vu = nullptr;
+    float* zu = nullptr;  // the uncond rows hold a copy of the latent: keep it current across steps
+    for (int u = 0; u < P.B; ++u)
+      if (P.real[u] == P.real[v] && P.branch[u] == 1) {
+        vu = A.vbuf.as<float>() + static_cast<size_t>(P.loff[i][u]) * lat;
+        zu = A.zpack.as<float>() + static_cast<size_t>(P.loff[i][u]) * lat;
+      }
+    Scope sc(c, "cfg_euler", 1);
+    const size_t off = static_cast<size_t>(P.loff[i][v]) * lat;
+    CK(cfg_euler(A.zpack.as<float>() + off, zu, A.vbuf.as<float>() + off, vu, cnt, dsig[P.real[v]], P.reqs[v]->cfg,
+                 c->stream));
+  }
   return GS_OK;
 }
 
@@ -557,8 +689,8 @@ std::vector<int> local_positions(gs_ctx* c, const Plan& P) {
 
 int run_one_step(gs_ctx* c, const Plan& P, const std::vector<int>& mine) {
   float t[MAX_BATCH], dsig[MAX_BATCH];
-  for (int r = 0; r < P.B; ++r) {
-    const Request* q = P.reqs[r];
+  for (size_t r = 0; r < P.ureqs.size(); ++r) {
+    const Request* q = P.ureqs[r];
     const double s0 = sigma_at(q->step_idx, q->steps, P.m->desc.flow_shift);
     const double s1 = sigma_at(q->step_idx + 1, q->steps, P.m->desc.flow_shift);
     t[r] = static_cast<float>(1000.0 * s0);
@@ -617,6 +749,70 @@ int alloc_shard(gs_ctx* c, Shard& s, int lat) {
     return fail(c, GS_ENOMEM, "latent shard alloc failed");
   }
   return GS_OK;
+}
+
+// Context K / V of every layer for a request on local rank li (replicated on every rank of its
+// placement, built on first use there): c = W_te2 GELU(W_te1 emb + b) + b (bf16), then per layer
+// [k|v] = c W_ckv^T + b_ckv, k <- RMSNorm(k) g_ck.  Layout [nb][layers][2][text_len][D] bf16.
+int ensure_text_cache(gs_ctx* c, Model* m, Request* q, int li) {
+  if (!m->desc.cross_attn) return GS_OK;
+  DevBuf& buf = q->ctx_kv[li];
+  if (buf.p) return GS_OK;
+  const int Lt = m->desc.text_len, T = m->desc.text_dim, D = m->desc.dim, NL = m->desc.layers, nb = q->nb;
+  const size_t per = static_cast<size_t>(Lt) * D;
+  RET(ensure(c, buf, static_cast<size_t>(nb) * NL * 2 * per * 2));
+  DevBuf emb, h1, cx, kv;
+  auto cleanup = [&] {
+    cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&emb, &h1, &cx, &kv})
+      if (b->p) cudaFree(b->p);
+  };
+  int rc = GS_OK;
+  do {
+    const size_t rows = static_cast<size_t>(nb) * Lt;
+    if ((rc = ensure(c, emb, rows * T * 2)) != GS_OK) break;
+    if ((rc = ensure(c, h1, rows * D * 2)) != GS_OK) break;
+    if ((rc = ensure(c, cx, rows * D * 2)) != GS_OK) break;
+    if ((rc = ensure(c, kv, rows * 2 * D * 2)) != GS_OK) break;
+    cudaError_t e = cudaSuccess;
+    if (!q->prompt_host.empty())
+      e = cudaMemcpyAsync(emb.p, q->prompt_host.data(), rows * T * 2, cudaMemcpyHostToDevice, c->stream);
+    else
+      for (int b = 0; b < nb && e == cudaSuccess; ++b)
+        e = rng_normal_bf16(emb.as<bf16>() + static_cast<size_t>(b) * Lt * T, static_cast<long long>(Lt) * T,
+                            q->prompt_seed, 50 + b, c->stream);
+    if (e != cudaSuccess) {
+      rc = fail(c, GS_ECUDA, "prompt upload: %s", cudaGetErrorString(e));
+      break;
+    }
+    if ((rc = gemm(c, "text_embed", EPI_GELU_BF16, rows, D, T, emb.p, m->w_te1, epi(h1.p, D, m->b_te1))) != GS_OK) break;
+    if ((rc = gemm(c, "text_embed", EPI_BF16, rows, D, D, h1.p, m->w_te2, epi(cx.p, D, m->b_te2))) != GS_OK) break;
+    for (int l = 0; l < NL && rc == GS_OK; ++l) {
+      const BlockW& w = m->blocks[l];
+      if ((rc = gemm(c, "text_kv", EPI_BF16, rows, 2 * D, D, cx.p, w.w_ckv, epi(kv.p, 2 * D, w.b_ckv))) != GS_OK) break;
+      for (int b = 0; b < nb && rc == GS_OK; ++b) {
+        bf16* dst = buf.as<bf16>() + (static_cast<size_t>(b) * NL + l) * 2 * per;
+        const bf16* src = kv.as<bf16>() + static_cast<size_t>(b) * Lt * 2 * D;
+        e = rmsnorm_rows(src, 2 * D, Lt, D, w.g_ck, m->desc.eps, dst, c->stream);
+        if (e == cudaSuccess)
+          e = cudaMemcpy2DAsync(dst + per, D * 2, src + D, 2 * D * 2, D * 2, Lt, cudaMemcpyDeviceToDevice, c->stream);
+        if (e != cudaSuccess) rc = fail(c, GS_ECUDA, "text cache: %s", cudaGetErrorString(e));
+      }
+    }
+  } while (0);
+  cleanup();
+  if (rc != GS_OK && buf.p) {
+    cudaFree(buf.p);
+    buf.p = nullptr;
+    buf.cap = 0;
+  }
+  return rc;
+}
+
+void free_text_cache(Request* q) {
+  for (auto& kv : q->ctx_kv)
+    if (kv.second.p) cudaFree(kv.second.p);
+  q->ctx_kv.clear();
 }
 
 }  // namespace
@@ -688,15 +884,17 @@ void gs_destroy(gs_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (auto& kv : c->reqs)
+  for (auto& kv : c->reqs) {
     for (auto& s : kv.second->shards)
       if (s.z) cudaFree(s.z);
+    free_text_cache(kv.second.get());
+  }
   for (auto& m : c->models)
     for (void* p : m->allocs) cudaFree(p);
   for (auto& A : c->local) {
     DevBuf* bufs[] = {&A.x, &A.a, &A.qkv, &A.qs, &A.ks, &A.vs, &A.qr, &A.kr, &A.vr, &A.o, &A.orecv,
                       &A.ostage, &A.h, &A.zpack, &A.zb, &A.e0, &A.e, &A.temb, &A.row_req, &A.row_tok,
-                      &A.req_grid};
+                      &A.req_grid, &A.qc, &A.vbuf};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
   }
@@ -728,13 +926,45 @@ int gs_model_create(gs_ctx* c, const gs_model_desc* d, int* model_id) {
     return fail(c, GS_EINVAL, "unsupported model shape (dim %d heads %d ffn %d lat %d)", d->dim, d->heads, d->ffn, d->lat);
   const int hd = d->dim / d->heads;
   if (hd != 64 && hd != 128) return fail(c, GS_EUNSUPPORTED, "head dim %d not in {64, 128}", hd);
+  if (d->cross_attn && (d->text_len < 1 || d->text_len > 4096 || d->text_dim < 64 || d->text_dim % 64))
+    return fail(c, GS_EINVAL, "bad text shape (len %d dim %d)", d->text_len, d->text_dim);
   auto m = std::make_unique<Model>();
   m->desc = *d;
   m->hd = hd;
   m->blocks.resize(d->layers);
   for (int l = 0; l < d->layers; ++l)
-    for (const WSpec& s : block_specs(*d)) RET(gen(c, *m, block_slot(m->blocks[l], s.name), s, d->weight_seed + l));
-  for (const WSpec& s : global_specs(*d)) RET(gen(c, *m, global_slot(*m, s.name), s, d->weight_seed + 1000000ull));
+    for (const WSpec& s : all_block_specs(*d)) RET(gen(c, *m, block_slot(m->blocks[l], s.name), s, d->weight_seed + l));
+  for (const WSpec& s : all_global_specs(*d)) RET(gen(c, *m, global_slot(*m, s.name), s, d->weight_seed + 1000000ull));
+  if (d->cross_attn) {
+    // norm3 affine as ln_modulate tables: LN(x) * (1 + (w - 1)) + b, w - 1 exact in fp32
+    const int D = d->dim;
+    std::vector<float> zeros(D, 0.f), sm1(D), sh(D);
+    std::vector<bf16> wv(D), bv(D);
+    void* pz = nullptr;
+    CK(cudaMalloc(&pz, D * 4));
+    m->allocs.push_back(pz);
+    CK(cudaMemcpy(pz, zeros.data(), D * 4, cudaMemcpyHostToDevice));
+    m->zeros = static_cast<float*>(pz);
+    CK(cudaStreamSynchronize(c->stream));
+    for (int l = 0; l < d->layers; ++l) {
+      BlockW& b = m->blocks[l];
+      CK(cudaMemcpy(wv.data(), b.ln3_w, D * 2, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(bv.data(), b.ln3_b, D * 2, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < D; ++i) {
+        sm1[i] = __bfloat162float(wv[i]) - 1.0f;
+        sh[i] = __bfloat162float(bv[i]);
+      }
+      void *ps = nullptr, *pb = nullptr;
+      CK(cudaMalloc(&ps, D * 4));
+      m->allocs.push_back(ps);
+      CK(cudaMalloc(&pb, D * 4));
+      m->allocs.push_back(pb);
+      CK(cudaMemcpy(ps, sm1.data(), D * 4, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(pb, sh.data(), D * 4, cudaMemcpyHostToDevice));
+      b.ln3_scale_m1 = static_cast<float*>(ps);
+      b.ln3_shift = static_cast<float*>(pb);
+    }
+  }
   // RoPE table (reading 1 / SURVEY.md §8(c) step 4): slots [d/2 - 2 floor(d/6), floor(d/6), floor(d/6)]
   const int half = hd / 2, s3 = hd / 6;
   const int slots[3] = {half - 2 * s3, s3, s3};
@@ -771,7 +1001,7 @@ int gs_get_weight(gs_ctx* c, int model, int layer, const char* name, void* host,
   if (!c || !name || !host) return GS_EINVAL;
   if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
   Model& m = *c->models[model];
-  const auto specs = layer < 0 ? global_specs(m.desc) : block_specs(m.desc);
+  const auto specs = layer < 0 ? all_global_specs(m.desc) : all_block_specs(m.desc);
   if (layer >= m.desc.layers) return fail(c, GS_EINVAL, "bad layer");
   for (const WSpec& s : specs) {
     if (strcmp(s.name, name)) continue;
@@ -786,8 +1016,9 @@ int gs_get_weight(gs_ctx* c, int model, int layer, const char* name, void* host,
   return fail(c, GS_EINVAL, "unknown tensor %s", name);
 }
 
-int gs_submit(gs_ctx* c, int model, int width, int height, int frames, int steps, uint64_t noise_seed,
-              const float* init_latent, const int* ranks, int nranks, gs_req* out) {
+static int submit_impl(gs_ctx* c, int model, int width, int height, int frames, int steps, uint64_t noise_seed,
+                       const float* init_latent, const int* ranks, int nranks, bool text, uint64_t prompt_seed,
+                       float cfg_scale, const void* prompt_embeds, gs_req* out) {
   if (!c || !out) return GS_EINVAL;
   std::lock_guard<std::mutex> g(c->run_mu);
   CK(cudaSetDevice(c->device));
@@ -796,6 +1027,9 @@ int gs_submit(gs_ctx* c, int model, int width, int height, int frames, int steps
     return fail(c, GS_EINVAL, "bad request shape %dx%d frames %d steps %d", width, height, frames, steps);
   RET(check_ranks(c, ranks, nranks));
   Model& m = *c->models[model];
+  if (text != (m.desc.cross_attn != 0))
+    return fail(c, GS_EINVAL, text ? "gs_submit_text needs a cross-attention model"
+                                   : "cross-attention model: submit with gs_submit_text");
   auto q = std::make_unique<Request>();
   q->model = model;
   q->grid[0] = 1 + (frames - 1) / 4;
@@ -805,6 +1039,15 @@ int gs_submit(gs_ctx* c, int model, int width, int height, int frames, int steps
     return fail(c, GS_EINVAL, "token grid exceeds RoPE table (%d)", m.p_max);
   q->n = q->grid[0] * q->grid[1] * q->grid[2];
   q->steps = steps;
+  if (text) {
+    q->nb = cfg_scale > 0.f ? 2 : 1;
+    q->cfg = cfg_scale > 0.f ? cfg_scale : 0.f;
+    q->prompt_seed = prompt_seed;
+    if (prompt_embeds) {
+      const size_t n = static_cast<size_t>(q->nb) * m.desc.text_len * m.desc.text_dim;
+      q->prompt_host.assign(static_cast<const uint16_t*>(prompt_embeds), static_cast<const uint16_t*>(prompt_embeds) + n);
+    }
+  }
   q->ranks.assign(ranks, ranks + nranks);
   q->shards.resize(nranks);
   for (int i = 0; i < nranks; ++i) {
@@ -825,6 +1068,19 @@ int gs_submit(gs_ctx* c, int model, int width, int height, int frames, int steps
   *out = q->id;
   c->reqs[q->id] = std::move(q);
   return GS_OK;
+}
+
+int gs_submit(gs_ctx* c, int model, int width, int height, int frames, int steps, uint64_t noise_seed,
+              const float* init_latent, const int* ranks, int nranks, gs_req* out) {
+  return submit_impl(c, model, width, height, frames, steps, noise_seed, init_latent, ranks, nranks, false, 0, 0.f,
+                     nullptr, out);
+}
+
+int gs_submit_text(gs_ctx* c, int model, int width, int height, int frames, int steps, uint64_t noise_seed,
+                   uint64_t prompt_seed, float cfg_scale, const float* init_latent, const void* prompt_embeds,
+                   const int* ranks, int nranks, gs_req* out) {
+  return submit_impl(c, model, width, height, frames, steps, noise_seed, init_latent, ranks, nranks, true,
+                     prompt_seed, cfg_scale, prompt_embeds, out);
 }
 
 int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int nranks, int k, int* steps_run) {
@@ -853,6 +1109,7 @@ int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int n
   const std::vector<int> mine = local_positions(c, P);
   for (int i : mine) {
     RankArena& A = c->local[local_index(c, P.ranks[i])];
+    for (Request* q : reqs) RET(ensure_text_cache(c, m, q, local_index(c, P.ranks[i])));
     RET(prepare_rank(c, P, i, A));
     RET(move_latent(c, P, i, A, 0));
   }
@@ -963,6 +1220,7 @@ int gs_resume(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
   CK(cudaStreamSynchronize(c->stream));
   for (Shard& o : q->shards)
     if (o.z) cudaFree(o.z);
+  free_text_cache(q);  // rebuilt on the new ranks at their first step
   q->shards = ns;
   q->ranks.assign(ranks, ranks + nranks);
   q->state = q->step_idx >= q->steps ? GS_REQ_DONE : GS_REQ_PLACED;
@@ -1012,6 +1270,7 @@ int gs_release(gs_ctx* c, gs_req id) {
   cudaStreamSynchronize(c->stream);
   for (auto& s : it->second->shards)
     if (s.z) cudaFree(s.z);
+  free_text_cache(it->second.get());
   c->reqs.erase(it);
   return GS_OK;
 }
@@ -1117,7 +1376,7 @@ int gs_debug_time_embed(gs_ctx* c, int model, int nreq, const float* t, float* e
 }
 
 int gs_debug_block(gs_ctx* c, int model, int layer, float* x, int nreq, const int* grids, const int* tok_lo,
-                   const int* n_rows, const float* t) {
+                   const int* n_rows, const float* t, const void* prompts) {
   if (!c || !x || !grids || !tok_lo || !n_rows || !t) return GS_EINVAL;
   std::lock_guard<std::mutex> g(c->run_mu);
   CK(cudaSetDevice(c->device));
@@ -1127,13 +1386,20 @@ int gs_debug_block(gs_ctx* c, int model, int layer, float* x, int nreq, const in
   if (nreq < 1 || nreq > MAX_BATCH) return fail(c, GS_EINVAL, "nreq");
   // A p = 1 plan over segments [tok_lo, tok_lo + n_rows) of each request; attention runs over
   // the segment only (pass full requests, tok_lo = 0, for the block of the method).
+  if (m->desc.cross_attn && !prompts) return fail(c, GS_EINVAL, "cross-attention model: prompts required");
   std::vector<std::unique_ptr<Request>> own(nreq);
   std::vector<Request*> reqs(nreq);
+  const size_t psz = static_cast<size_t>(m->desc.text_len) * m->desc.text_dim;
   for (int r = 0; r < nreq; ++r) {
     own[r] = std::make_unique<Request>();
     for (int a = 0; a < 3; ++a) own[r]->grid[a] = grids[3 * r + a];
     own[r]->n = n_rows[r];
     own[r]->steps = 1;
+    if (m->desc.cross_attn) {
+      const uint16_t* pp = static_cast<const uint16_t*>(prompts) + r * psz;
+      own[r]->prompt_host.assign(pp, pp + psz);
+      RET(ensure_text_cache(c, m, own[r].get(), 0));
+    }
     reqs[r] = own[r].get();
   }
   int rank0 = c->local[0].rank;
@@ -1159,6 +1425,7 @@ int gs_debug_block(gs_ctx* c, int model, int layer, float* x, int nreq, const in
   RET(block_post(c, P, 0, A, layer));
   CK(cudaMemcpyAsync(x, A.x.p, xbytes, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  for (auto& q : own) free_text_cache(q.get());
   prof_flush(c);
   return GS_OK;
 }

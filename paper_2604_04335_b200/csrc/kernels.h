@@ -16,6 +16,7 @@ enum EpiKind : int {
   EPI_F32 = 2,         // out fp32 = acc + bias
   EPI_RESID_F32 = 3,   // out fp32 += (gate_a[n] + gate_b[req(m)*gate_b_stride + n]) * (acc + bias)
   EPI_EULER_F32 = 4,   // out fp32 += dsig[req(m)] * (acc + bias)
+  EPI_ADD_F32 = 5,     // out fp32 += acc + bias (ungated residual: text cross-attention output)
 };
 
 struct EpiParams {
@@ -40,6 +41,11 @@ cudaError_t gemm_bf16_tc(int epi, int M, int N, int K, const void* A, int lda, c
 cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                          int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
                          int nreq, int num_sms, cudaStream_t stream);
+// General form: segment r's q_len[r] query rows (from q_off[r]) attend to its kv_len[r] key/value
+// rows (from kv_off[r]) -- text cross-attention uses a separate context K/V buffer.
+cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, void* O, int heads, int d,
+                                  int q_rs, int kv_rs, int o_rs, const int* q_off, const int* q_len,
+                                  const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream);
 
 // ----------------------------------------------------------------- element-wise (elementwise.cu)
 // out[m, :] = LN(x[m, :]) * (1 + sc) + sh, sh = sh_a + sh_b[req(m)*b_stride], same for sc.
@@ -78,11 +84,23 @@ cudaError_t time_embed(const TimeEmbedW& w, int B, const float* t_host /*B*/, fl
 
 cudaError_t f32_to_bf16(const float* in, __nv_bfloat16* out, long long n, cudaStream_t stream);
 
+// out[m, :] = in[m, :D] * rsqrt(mean(in[m, :D]^2) + eps) * g  (bf16 in with row stride ld_in,
+// bf16 out dense [M, D]); fixed-order reduction as in the other row kernels.
+cudaError_t rmsnorm_rows(const __nv_bfloat16* in, int ld_in, int M, int D, const __nv_bfloat16* g, float eps,
+                         __nv_bfloat16* out, cudaStream_t stream);
+// Classifier-free guidance + Euler on n floats: z += dsig * (vu + g (vc - vu)); vu == null: z += dsig vc.
+// z2 (optional) receives the same updated values (the uncond branch's rows of the shared latent).
+cudaError_t cfg_euler(float* z, float* z2, const float* vc, const float* vu, long long n, float dsig, float g,
+                      cudaStream_t stream);
+
 // ----------------------------------------------------------------- RNG (rng.cu)
 // Counter RNG of DESIGN.md "Input recipe" (independent re-implementation of synth/rng.py).
 enum RngKind : int { RNG_BF16_SCALED = 0, RNG_BF16_GAIN = 1, RNG_F32_SCALED = 2 };
 cudaError_t rng_fill(void* out, long long n, uint64_t seed, uint32_t tensor_id, int kind,
                      float scale, cudaStream_t stream);
+// Standard-normal (Irwin-Hall(4)) values rounded to bf16: synthetic prompt embeddings.
+cudaError_t rng_normal_bf16(__nv_bfloat16* out, long long n, uint64_t seed, uint32_t tensor_id,
+                            cudaStream_t stream);
 // z[i, c] for tokens [tok_lo, tok_lo + ntok) of a request's [n, 64] noise latent.
 cudaError_t rng_noise(float* out, long long tok_lo, long long ntok, int channels, uint64_t seed,
                       cudaStream_t stream);

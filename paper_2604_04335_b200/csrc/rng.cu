@@ -49,7 +49,27 @@ __global__ void rng_noise_kernel(float* out, long long first, long long n, uint6
     out[i] = __double2float_rn(__dmul_rn(s, c));
   }
 }
+__global__ void rng_normal_bf16_kernel(__nv_bfloat16* out, long long n, uint64_t key) {
+  const double c = 0.8660254037844386;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t g = static_cast<uint64_t>(i) * 4;
+    const double s = ((double)unif(key, g) + (double)unif(key, g + 1)) +
+                     ((double)unif(key, g + 2) + (double)unif(key, g + 3));
+    out[i] = __float2bfloat16_rn(__double2float_rn(__dmul_rn(s, c)));
+  }
+}
 }  // namespace
+
+cudaError_t rng_normal_bf16(__nv_bfloat16* out, long long n, uint64_t seed, uint32_t tensor_id,
+                            cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const uint64_t key = seed ^ (static_cast<uint64_t>(tensor_id) << 40);
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  rng_normal_bf16_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(out, n, key);
+  return cudaGetLastError();
+}
 
 cudaError_t rng_fill(void* out, long long n, uint64_t seed, uint32_t tensor_id, int kind,
                      float scale, cudaStream_t stream) {

@@ -28,6 +28,10 @@ struct DevBuf {
 struct BlockW {
   bf16 *w_qkv, *b_qkv, *g_q, *g_k, *w_o, *b_o, *w_1, *b_1, *w_2, *b_2;
   float* mod;  // [6, D]
+  // text cross-attention (NEXT-1; null without cross_attn)
+  bf16 *ln3_w = nullptr, *ln3_b = nullptr, *w_cq = nullptr, *b_cq = nullptr, *w_ckv = nullptr,
+       *b_ckv = nullptr, *g_cq = nullptr, *g_ck = nullptr, *w_co = nullptr, *b_co = nullptr;
+  float *ln3_scale_m1 = nullptr, *ln3_shift = nullptr;  // fp32 (ln3_w - 1), ln3_b for ln_modulate
 };
 
 struct Model {
@@ -35,6 +39,8 @@ struct Model {
   int hd = 0;  // head dim
   std::vector<BlockW> blocks;
   bf16 *w_pe, *b_pe, *w_t1, *b_t1, *w_t2, *b_t2, *w_tp, *b_tp, *w_head, *b_head;
+  bf16 *w_te1 = nullptr, *b_te1 = nullptr, *w_te2 = nullptr, *b_te2 = nullptr;  // text embedding
+  float* zeros = nullptr;  // [D] fp32
   float* mod_head;     // [2, D]
   float2* cs_tab;      // [p_max, hd/2]
   int* slot_axis;      // [hd/2]
@@ -59,13 +65,20 @@ struct Request {
   std::vector<int> ranks;
   std::vector<Shard> shards;  // one per SP position
   std::atomic<int> preempt{0};
+  // text conditioning (cross-attention models): nb = 1 (cond) or 2 (cond + uncond, CFG scale cfg)
+  int nb = 1;
+  float cfg = 0.f;
+  uint64_t prompt_seed = 0;
+  std::vector<uint16_t> prompt_host;  // [nb][text_len][text_dim] bf16 bits if given by the caller
+  // per local rank index: context K / V of every layer [nb][layers][2][text_len][D] bf16
+  std::map<int, DevBuf> ctx_kv;
 };
 
 // Per-local-rank arena (grow-only device buffers).
 struct RankArena {
   int rank = 0;
   DevBuf x, a, qkv, qs, ks, vs, qr, kr, vr, o, orecv, ostage, h, zpack, zb, e0, e, temb, row_req,
-      row_tok, req_grid;
+      row_tok, req_grid, qc, vbuf;
 };
 
 struct Prof {
