@@ -47,11 +47,17 @@ WORKLOADS = {
     "t2v720": (sm.WAN_14B, [(1280, 720, 81)], True),
     "t2v480": (sm.WAN_1_3B, [(832, 480, 81)], True),
     "t2i1024": (sm.WAN_1_3B, [(1024, 1024, 1)] * 4, False),
+    # NEXT-1: the full Wan block (text cross-attention over 512 prompt tokens) with classifier-free
+    # guidance g = 5 (cond + uncond forward per step)
+    "t2v720_text_cfg": (sm.WAN_14B.with_text(512, 4096), [(1280, 720, 81)], True),
 }
+CFG_SCALE = {"t2v720_text_cfg": 5.0}
 CONFIG_NAME = {
     "t2v720": "config4: 720x1280 81f T2V (75600 tok), Wan-14B-shaped DiT step",
     "t2v480": "config3: 480x832 81f T2V (32760 tok), Wan-1.3B-shaped DiT step",
     "t2i1024": "config2: 4 x 1024px T2I (4 x 4096 tok) batch, Wan-1.3B-shaped DiT step",
+    "t2v720_text_cfg": "config4 + NEXT-1: 720x1280 81f T2V, Wan-14B-shaped step with text "
+                       "cross-attention (512 tok) and CFG g=5 (2 forwards)",
 }
 
 
@@ -140,16 +146,24 @@ def oracle_sample(workload, reps=1, budget_tokens=None):
     g = np.random.default_rng(5)
     x = g.standard_normal((n, shape.dim))
     e_req = g.uniform(-0.5, 0.5, (1, 6, shape.dim))
+    ctxs = [g.standard_normal((shape.text_len, shape.dim))] if shape.cross_attn else None
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        dit.dit_block(x, blk, e_req, [(0, n, grid)], shape.heads)
+        dit.dit_block(x, blk, e_req, [(0, n, grid)], shape.heads, ctxs)
         times.append(time.perf_counter() - t0)
     t = float(np.median(times))
-    f_sample = costmodel.flops_per_block([n], shape.dim, shape.ffn)
+
+    def block_flops(ns):
+        f = costmodel.flops_per_block(ns, shape.dim, shape.ffn)
+        if shape.cross_attn:  # cross q/o projections + attention over the text tokens
+            f += sum(4 * m * shape.dim ** 2 + 4 * m * shape.text_len * shape.dim for m in ns)
+        return f
+    f_sample = block_flops([n])
     full_seqs = [sm.token_grid(*r) for r in reqs]
     full_n = [a * b * c for a, b, c in full_seqs]
-    f_step = shape.layers * costmodel.flops_per_block(full_n, shape.dim, shape.ffn)
+    nb = 2 if CFG_SCALE.get(workload, 0.0) > 0 else 1
+    f_step = nb * shape.layers * block_flops(full_n)
     ms_step = t * 1e3 * f_step / f_sample
     info = {"sample": (f"oracle dit_block (fp64 numpy) layer 0 of {shape.name} on a {grid} "
                        f"token grid ({n} tokens, {f_sample / 1e9:.1f} GFLOP) in {t:.2f} s; "
@@ -230,14 +244,21 @@ def run_gpu(args, rank, world, local_rank):
     if not sp_over_ranks and world > 1:
         # replicas: every rank owns its own single-rank placement (images use <= 1 GPU)
         pass
-    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed)
+    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed,
+                           cross_attn=shape.cross_attn, text_len=shape.text_len, text_dim=shape.text_dim)
     total_steps = max(50, args.warmup + args.steps + 1)
+    cfg = CFG_SCALE.get(args.workload, 0.0)
+    nb = 2 if cfg > 0 else 1
 
     def submit_all(init=None):
         out = []
         for r, (w, h, f) in enumerate(reqs_spec):
             lat = None if init is None else init[r]
-            out.append(ctx.submit(mid, w, h, f, total_steps, 1000 + r, ranks, init_latent=lat))
+            if shape.cross_attn:
+                out.append(ctx.submit_text(mid, w, h, f, total_steps, 1000 + r, ranks, prompt_seed=2000 + r,
+                                           cfg_scale=cfg, init_latent=lat))
+            else:
+                out.append(ctx.submit(mid, w, h, f, total_steps, 1000 + r, ranks, init_latent=lat))
         return out
 
     stream = torch.cuda.ExternalStream(ctx.stream_ptr(rank))
@@ -312,15 +333,18 @@ def run_gpu(args, rank, world, local_rank):
     H_loc = head_split(shape.heads, p, 0)  # rank 0 carries the most heads
     attn = st.get("attention", {"ms": 0.0, "n": 0})
     attn_avg_ms = attn["ms"] / max(attn["n"], 1)
-    af = attn_flops_per_launch(shape, seqlens, H_loc)
+    af = attn_flops_per_launch(shape, seqlens * nb, H_loc)  # CFG: cond + uncond sequences
     achieved = af / (attn_avg_ms * 1e-3) / 1e12 if attn_avg_ms > 0 else 0.0
     peak = pk["bf16_sustained"]
     traffic = load_traffic(args.workload, p)
     gemm_ms = sum(v["ms"] for k, v in st.items() if isinstance(v, dict) and k.startswith("gemm"))
-    gemm_flops = shape.layers * costmodel.gemm_flops_per_block(sum(seqlens) / p, shape.dim, shape.ffn)
+    rows = nb * sum(seqlens) / p
+    cross_gemm = 4 * rows * shape.dim ** 2 if shape.cross_attn else 0  # cross q and o projections
+    gemm_flops = shape.layers * (costmodel.gemm_flops_per_block(rows, shape.dim, shape.ffn) + cross_gemm)
     gemm_tflops = gemm_flops * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
-    step_flops = shape.layers * (costmodel.gemm_flops_per_block(sum(seqlens) / p, shape.dim, shape.ffn)
-                                 + af)
+    cross_attn_flops = 4 * rows * shape.text_len * shape.dim if shape.cross_attn else 0
+    step_flops = shape.layers * (costmodel.gemm_flops_per_block(rows, shape.dim, shape.ffn) + cross_gemm + af
+                                 + cross_attn_flops)
     breakdown = {k: round(v["ms"] / args.steps, 3) for k, v in st.items() if isinstance(v, dict)}
 
     cpu = None

@@ -87,7 +87,7 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[128], float
       const int col = c * 32 + 2 * i;
       const float2 x =
           __ffma2_rn(make_float2(__uint_as_float(v[col]), __uint_as_float(v[col + 1])), sc2, nm2);
-      // exp2: MUFU for most pairs, FMA-pipe polynomial for POLY8 of every 8 pairs (reading 18)
+      // exp2: MUFU for most pairs, FMA-pipe polynomial for POLY8 of every 8 pairs (reading 22)
       float2 p;
       if (poly_pair<POLY8>(i & 7)) {
         p = exp2_poly2(x);

@@ -97,7 +97,7 @@ print("ok")
 
 @pytest.mark.parametrize("poly8", [2, 3, 4])
 def test_attention_poly_exp2_variants(poly8):
-    """The FMA-pipe exp2 polynomial (reading 18) at each offload fraction."""
+    """The FMA-pipe exp2 polynomial (reading 22) at each offload fraction."""
     env = dict(os.environ, GS_ATTN_POLY8=str(poly8))
     r = subprocess.run([sys.executable, "-c", POLY_SCRIPT.format(root=ROOT)], env=env,
                        capture_output=True, text=True, timeout=300)
