@@ -44,20 +44,27 @@ struct SeqTable {
   int nreq;
   int q_off[MAX_REQ], q_len[MAX_REQ];    // query rows of segment r
   int kv_off[MAX_REQ], kv_len[MAX_REQ];  // key / value rows it attends to (= q for self-attention)
-  int tile_start[MAX_REQ + 1];           // prefix sum of ceil(q_len / 256)
+  int tile_start[MAX_REQ + 1];           // prefix sum of ceil(q_len / rows per CTA (pair))
 };
 
-template <int HD>
+// PAIR (d = 128): CTA pairs with cta_group::2 MMAs (M = 256 = both CTAs' Q tile w): each CTA stages
+// half of every K tile (64 keys, the B operand's N half) and half of every V tile (64 of the d
+// columns), halving per-SM shared-memory B reads and L2 -> SM traffic (tools/micro: the UMMA smem
+// read path is 128 B/clk).
+template <int HD, bool PAIR>
 struct Cfg {
   static constexpr int BOXES = HD / 64;                  // 64-element (128 B) column boxes
-  static constexpr int TILE_BYTES = 128 * HD * 2;        // one 128-row tile
+  static constexpr int TILE_BYTES = 128 * HD * 2;        // one 128-row Q tile
+  static constexpr int KT_BYTES = (PAIR ? 64 : 128) * HD * 2;       // this CTA's part of a K tile
+  static constexpr int KBOX_BYTES = (PAIR ? 64 : 128) * 128;       // one [rows][64] K box
+  static constexpr int VT_BYTES = 128 * (PAIR ? HD / 2 : HD) * 2;  // this CTA's part of a V tile
   // K ring deeper than V: a K slot frees after both S MMAs, a V slot only after both PV MMAs
-  static constexpr int KST = HD == 128 ? 3 : 4;          // K stages
-  static constexpr int VST = HD == 128 ? 2 : 4;          // V stages
+  static constexpr int KST = PAIR ? 4 : (HD == 128 ? 3 : 4);
+  static constexpr int VST = PAIR ? 4 : (HD == 128 ? 2 : 4);
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = 2 * TILE_BYTES;
-  static constexpr int V_OFF = K_OFF + KST * TILE_BYTES;
-  static constexpr int BAR_OFF = V_OFF + VST * TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + KST * KT_BYTES;
+  static constexpr int BAR_OFF = V_OFF + VST * VT_BYTES;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
 };
 
@@ -110,12 +117,12 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[128], float
   return __fadd2_rn(acc0, acc1);
 }
 
-template <int HD, int POLY8, bool TRACE = false>
+template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128)>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
                    const __grid_constant__ SeqTable tab, float scale_log2) {
-  using C = Cfg<HD>;
+  using C = Cfg<HD, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -131,29 +138,33 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;  // 0 = leader (issues the MMAs)
+  constexpr int ROWS = PAIR ? 512 : 256;               // query rows per CTA pair / CTA
 
-  // locate (request, pair-of-tiles) of this CTA
+  // locate (request, block of ROWS query rows) of this CTA (pair)
+  const int blk = PAIR ? (blockIdx.x >> 1) : blockIdx.x;
   int r = 0;
-  while (r + 1 < tab.nreq && static_cast<int>(blockIdx.x) >= tab.tile_start[r + 1]) ++r;
-  const int pair = blockIdx.x - tab.tile_start[r];
+  while (r + 1 < tab.nreq && blk >= tab.tile_start[r + 1]) ++r;
+  const int pair = blk - tab.tile_start[r];
   const int kv_off = tab.kv_off[r], kv_len = tab.kv_len[r];
-  const int q_row0 = tab.q_off[r] + pair * 256;
-  const int q_rows = min(256, tab.q_len[r] - pair * 256);
+  const int q_row0 = tab.q_off[r] + pair * ROWS + rank * 256;
+  const int q_rows = min(256, tab.q_len[r] - pair * ROWS - static_cast<int>(rank) * 256);  // may be <= 0
   const int nkv = (kv_len + 127) / 128;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    constexpr int NC = PAIR ? 2 : 1;  // leader-side full barriers count one arrival per CTA
+    mbar_init(q_full, NC);
     for (int s = 0; s < C::KST; ++s) {
-      mbar_init(&kfull[s], 1);
+      mbar_init(&kfull[s], NC);
       mbar_init(&kempty[s], 1);
     }
     for (int s = 0; s < C::VST; ++s) {
-      mbar_init(&vfull[s], 1);
+      mbar_init(&vfull[s], NC);
       mbar_init(&vempty[s], 1);
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&sfull[w], 1);
-      mbar_init(&pfull[w], 4);
+      mbar_init(&pfull[w], 4 * NC);
       mbar_init(&ofull[w], 1);
     }
     fence_barrier_init();
@@ -163,9 +174,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
   }
-  if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
+  if (warp == kMmaWarp) {
+    if (PAIR)
+      tmem_alloc_2sm(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync();  // both CTAs' barriers initialised before any remote arrive / 2-SM TMA
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -176,34 +195,55 @@ __global__ void __launch_bounds__(THREADS, 1)
   asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
   if (warp == kProducerWarp) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * C::TILE_BYTES);
+      // bytes land in this CTA's smem; the (leader's) full barrier counts them
+      auto arrive_tx = [&](uint64_t* bar, uint32_t bytes) {
+        if (PAIR)
+          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(bar), 0), bytes);
+        else
+          mbar_arrive_expect_tx(bar, bytes);
+      };
+      auto load = [&](const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+        if (PAIR)
+          tma_load_3d_2sm(map, bar, dst, c0, c1, c2);
+        else
+          tma_load_3d(map, bar, dst, c0, c1, c2);
+      };
+      arrive_tx(q_full, 2 * C::TILE_BYTES);
       for (int w = 0; w < 2; ++w)
         for (int b = 0; b < C::BOXES; ++b)
-          tma_load_3d(&tmQ, q_full, smem + C::Q_OFF + w * C::TILE_BYTES + b * 16384, b * 64, head,
-                      q_row0 + w * 128);
+          load(&tmQ, q_full, smem + C::Q_OFF + w * C::TILE_BYTES + b * 16384, b * 64, head, q_row0 + w * 128);
       for (int j = 0; j < nkv; ++j) {
         const int ks = j % C::KST, vs = j % C::VST;
         mbar_wait(&kempty[ks], ((j / C::KST) & 1) ^ 1);
-        uint8_t* sk = smem + C::K_OFF + ks * C::TILE_BYTES;
+        uint8_t* sk = smem + C::K_OFF + ks * C::KT_BYTES;
         TRACE_EV(8, 0, j);
-        mbar_arrive_expect_tx(&kfull[ks], C::TILE_BYTES);
-        for (int b = 0; b < C::BOXES; ++b)
-          tma_load_3d(&tmK, &kfull[ks], sk + b * 16384, b * 64, head, kv_off + j * 128);
+        arrive_tx(&kfull[ks], C::KT_BYTES);
+        for (int b = 0; b < C::BOXES; ++b)  // PAIR: keys [64 rank, 64 rank + 64) of the tile
+          load(&tmK, &kfull[ks], sk + b * C::KBOX_BYTES, b * 64, head, kv_off + j * 128 + (PAIR ? 64 * rank : 0));
         mbar_wait(&vempty[vs], ((j / C::VST) & 1) ^ 1);
-        uint8_t* sv = smem + C::V_OFF + vs * C::TILE_BYTES;
+        uint8_t* sv = smem + C::V_OFF + vs * C::VT_BYTES;
         TRACE_EV(9, 0, j);
-        mbar_arrive_expect_tx(&vfull[vs], C::TILE_BYTES);
-        for (int b = 0; b < C::BOXES; ++b)
-          tma_load_3d(&tmV, &vfull[vs], sv + b * 16384, b * 64, head, kv_off + j * 128);
+        arrive_tx(&vfull[vs], C::VT_BYTES);
+        if (PAIR)  // d columns [64 rank, 64 rank + 64) of all 128 keys
+          load(&tmV, &vfull[vs], sv, 64 * rank, head, kv_off + j * 128);
+        else
+          for (int b = 0; b < C::BOXES; ++b)
+            load(&tmV, &vfull[vs], sv + b * 16384, b * 64, head, kv_off + j * 128);
       }
     }
-  } else if (warp == kMmaWarp) {
-    // Single MMA issuer.  Its fixed order PV0_j, S0_j+1, PV1_j, S1_j+1 keeps the two softmax
+  } else if (warp == kMmaWarp && rank == 0) {
+    // Single MMA issuer (the leader CTA of a pair).  Its fixed order PV0_j, S0_j+1, PV1_j, S1_j+1 keeps the two softmax
     // warpgroups half a period apart (ping-pong: one group's exp work overlaps the other's MMAs);
     // independent per-group issuers were measured to fall into lock-step (profiles/r01_notes.md).
     if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16(128, HD, 0, 1);
+      constexpr uint32_t idesc_s = idesc_bf16(PAIR ? 256 : 128, 128, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(PAIR ? 256 : 128, HD, 0, 1);
+      auto commit = [&](uint64_t* bar) {
+        if (PAIR)
+          mma_commit_2sm_mc(bar, 0x3);
+        else
+          mma_commit(bar);
+      };
       const uint32_t sq = smem_u32(smem + C::Q_OFF);
       const uint32_t sk0 = smem_u32(smem + C::K_OFF);
       const uint32_t sv0 = smem_u32(smem + C::V_OFF);
@@ -212,23 +252,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T -> TMEM cols [128 w, 128 w + 128)
         TRACE_EV(0, w, j);
         const uint32_t qa = sq + w * C::TILE_BYTES;
-        const uint32_t kb = sk0 + (j % C::KST) * C::TILE_BYTES;
+        const uint32_t kb = sk0 + (j % C::KST) * C::KT_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          mma_ss(tmem + w * 128, sdesc_sw128(qa + off, 16, 1024), sdesc_sw128(kb + off, 16, 1024),
-                 idesc_s, kk > 0);
+          const uint32_t qoff = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * C::KBOX_BYTES + (kk & 3) * 32;
+          if (PAIR)
+            mma_ss_2sm(tmem + w * 128, sdesc_sw128(qa + qoff, 16, 1024), sdesc_sw128(kb + koff, 16, 1024),
+                       idesc_s, kk > 0);
+          else
+            mma_ss(tmem + w * 128, sdesc_sw128(qa + qoff, 16, 1024), sdesc_sw128(kb + koff, 16, 1024),
+                   idesc_s, kk > 0);
         }
-        mma_commit(&sfull[w]);
+        commit(&sfull[w]);
         TRACE_EV(13, w, j);
       };
       auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j, P_w read from TMEM (bf16 over S_w)
         TRACE_EV(1, w, j);
-        const uint32_t vb = sv0 + (j % C::VST) * C::TILE_BYTES;
+        const uint32_t vb = sv0 + (j % C::VST) * C::VT_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          mma_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
-                 idesc_o, (j > 0) || (kk > 0));
+          if (PAIR)
+            mma_ts_2sm(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
+                       idesc_o, (j > 0) || (kk > 0));
+          else
+            mma_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
+                   idesc_o, (j > 0) || (kk > 0));
         }
         TRACE_EV(14, w, j);
       };
@@ -242,7 +291,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       issue_s(0, 0);
       issue_s(1, 0);
-      mma_commit(&kempty[0]);
+      commit(&kempty[0]);
       for (int j = 0; j < nkv; ++j) {
         const bool more = j + 1 < nkv;
         // V_j and K_{j+1} landed long ago in steady state: check them before waiting on P
@@ -255,14 +304,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (more) issue_s(0, j + 1);
         wait_p(1, j);
         issue_pv(1, j);
-        mma_commit(&vempty[j % C::VST]);
+        commit(&vempty[j % C::VST]);
         if (more) {
           issue_s(1, j + 1);
-          mma_commit(&kempty[(j + 1) % C::KST]);
+          commit(&kempty[(j + 1) % C::KST]);
         }
       }
-      mma_commit(&ofull[0]);
-      mma_commit(&ofull[1]);
+      commit(&ofull[0]);
+      commit(&ofull[1]);
     }
   }
   } else {
@@ -333,7 +382,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       const long long t_done = TRACE ? clock64() : 0;
-      if (lane == 0) mbar_arrive(&pfull[w]);
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&pfull[w]), 0));
+        else
+          mbar_arrive(&pfull[w]);
+      }
       if (TRACE && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && j < 32)
         g_attn_trace[((4 + quarter) * 32 + j) * 2 + w] = t_done;
     }
@@ -361,20 +415,25 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_before();
   }
   __syncthreads();
+  if (PAIR) cluster_sync();  // the peer may still arrive on our barriers / read our TMEM until here
   if (warp == kMmaWarp) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if (PAIR)
+      tmem_dealloc_2sm(tmem, 512);
+    else
+      tmem_dealloc(tmem, 512);
   }
 }
 
 template <int HD, int POLY8>
 cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
                    int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
-  using C = Cfg<HD>;
+  constexpr bool PAIR = HD == 128;
+  using C = Cfg<HD, PAIR>;
   CUtensorMap tq, tk, tv;
   if (!make_tma_3d_bf16(&tq, Q, HD, heads, q_rows, HD * 2ull, q_rs * 2ull, 64, 1, 128) ||
-      !make_tma_3d_bf16(&tk, K, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128) ||
+      !make_tma_3d_bf16(&tk, K, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, PAIR ? 64 : 128) ||
       !make_tma_3d_bf16(&tv, V, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
   static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
@@ -382,11 +441,21 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
-  dim3 grid(tab.tile_start[tab.nreq], heads);
+  dim3 grid(tab.tile_start[tab.nreq] * (PAIR ? 2 : 1), heads);
   if (grid.x == 0) return cudaSuccess;  // no query rows (an empty shard)
-  kern<<<grid, THREADS, C::SMEM, stream>>>(tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs,
-                                                          tab, scale_log2);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = PAIR ? 2 : 1;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2);
 }
 
 // Fraction of exp2 pairs (in eighths) computed by the FMA-pipe polynomial.  Default from the
@@ -420,13 +489,14 @@ cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, v
   tab.nreq = nreq;
   int q_rows = 1, kv_rows = 1;
   tab.tile_start[0] = 0;
+  const int rows_per_block = d == 128 ? 512 : 256;  // a CTA pair (d = 128) or a CTA (d = 64)
   for (int r = 0; r < nreq; ++r) {
     if (q_len[r] < 0 || kv_len[r] < 1) return cudaErrorInvalidValue;
     tab.q_off[r] = q_off[r];
     tab.q_len[r] = q_len[r];
     tab.kv_off[r] = kv_off[r];
     tab.kv_len[r] = kv_len[r];
-    tab.tile_start[r + 1] = tab.tile_start[r] + (q_len[r] + 255) / 256;
+    tab.tile_start[r + 1] = tab.tile_start[r] + (q_len[r] + rows_per_block - 1) / rows_per_block;
     q_rows = std::max(q_rows, q_off[r] + q_len[r]);
     kv_rows = std::max(kv_rows, kv_off[r] + kv_len[r]);
   }
