@@ -151,15 +151,19 @@ int gs_stream(gs_ctx* ctx, int rank, void** stream_out);
  * for one participant.  Pure host computation (no GPU, no context): the NCCL executor, the
  * emulated executor and the CPU multi-process tests all run these plans.  Messages between a
  * pair of participants are matched in list order (NCCL point-to-point semantics).
- * Offsets / sizes are in elements of the named buffers (bf16 for a2a, fp32 for the latent):
- *   a2a kind 0 (Q,K,V; apply to each): SEND buffer [dest j][rows_me][H_j][d] (pack-kernel layout),
- *     RECV buffer [rows of the whole batch][H_me][d];
- *   a2a kind 1 (O): O buffer [rows of the batch][H_me][d] (attention output), STAGE buffer
+ * Offsets / sizes are in elements of the named buffers (bf16 for a2a, fp32 for the latent).
+ * Head partition (reading 9): every position holds Hf = floor(H/p) full heads; the
+ * R = H mod p remaining heads are cut into c = p / gcd(R, p) query chunks each ([ci n/c, (ci+1) n/c)
+ * of every request), dealt out in order R / gcd(R, p) per position, so all positions do H/p heads
+ * of attention work.  Token shard i of p is [floor(i n/p), floor((i+1) n/p)) (reading 10).
+ *   SEND buffer of a position (pack-kernel layout): chunks j < p = [rows_me][Hf][d] (full heads of
+ *     position j), then chunk p+u = [rows_me][d] (partial head Hf p + u);
+ *   RECV buffer: full heads [rows of the whole batch][Hf][d], then per local unit t a K / V block
+ *     [rows of the batch][d] (kind 0) or a Q block [chunk rows of every request][d] (kind 2);
+ *   a2a kind 1 (O): O buffer in the kind-2 (Q) layout (attention output), STAGE buffer
  *     (*stage_elems elements), ORECV buffer [rows_me][heads * d]; COPY entries (2-D blocks) run
  *     after all sends/recvs completed;
- *   reshard: OLD shard [old rows][lat], NEW shard [new rows][lat]; peers are global ranks.
- * Token shard i of p is [floor(i n/p), floor((i+1) n/p)) (reading 10); heads split
- * contiguously with positions < H mod p holding ceil(H/p) (reading 9). */
+ *   reshard: OLD shard [old rows][lat], NEW shard [new rows][lat]; peers are global ranks. */
 enum { GS_XFER_SEND = 0, GS_XFER_RECV = 1, GS_XFER_COPY = 2 };
 enum { GS_BUF_SEND = 0, GS_BUF_RECV = 1, GS_BUF_O = 2, GS_BUF_STAGE = 3, GS_BUF_ORECV = 4,
        GS_BUF_OLD = 5, GS_BUF_NEW = 6 };
@@ -171,8 +175,8 @@ typedef struct {
   long long rows, width;   /* a rows x width block                                         */
   long long src_pitch, dst_pitch;
 } gs_xfer;
-/* kind 0 = seq->head (Q,K,V), 1 = head->seq (O) for SP position `me` of p over a batch of nreq
- * requests with n_tokens[r] tokens.  out may be NULL to query *n_out; GS_EINVAL if max_out is
+/* kind 0 = seq->head of K and V, 2 = seq->head of Q, 1 = head->seq of O, for SP position `me` of p
+ * over a batch of nreq requests with n_tokens[r] tokens.  out may be NULL to query *n_out; GS_EINVAL if max_out is
  * too small or an argument is out of range. */
 int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
                 gs_xfer* out, int max_out, int* n_out, long long* stage_elems);

@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(ROW_THREADS)
       int h0 = pk.head_off[0], h1 = pk.head_off[1];
       long long doff = pk.dest_off[0];
 #pragma unroll
-      for (int t = 1; t < 8; ++t) {
+      for (int t = 1; t < 16; ++t) {
         if (t < pk.ndest && h >= pk.head_off[t]) {
           h0 = pk.head_off[t];
           h1 = pk.head_off[t + 1];
@@ -312,7 +312,7 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream) {
   if (M == 0) return cudaSuccess;
   const int d = D / heads;
-  if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > 8)
+  if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > 16)
     return cudaErrorInvalidValue;
   qk_norm_rope_pack_kernel<<<M, ROW_THREADS, 0, stream>>>(qkv, D, d, g_q, g_k, eps, rp, pk, q_out,
                                                            k_out, v_out);

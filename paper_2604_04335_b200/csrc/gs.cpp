@@ -321,18 +321,20 @@ void make_plan(Plan& P, Model* m, const std::vector<Request*>& ureqs, const int*
 int prepare_rank(gs_ctx* c, const Plan& P, int i, RankArena& A) {
   const size_t rows = std::max(P.rows[i], 1), rf = std::max(P.rows_full, 1);
   const size_t D = P.D, F = P.F, lat = P.m->desc.lat;
-  const size_t hl = static_cast<size_t>(P.H_loc(i)) * P.hd;
+
   RET(ensure(c, A.x, rows * D * 4));
   RET(ensure(c, A.a, rows * D * 2));
   RET(ensure(c, A.qkv, rows * 3 * D * 2));
   RET(ensure(c, A.qs, rows * D * 2));
   RET(ensure(c, A.ks, rows * D * 2));
   RET(ensure(c, A.vs, rows * D * 2));
+  (void)rf;
   if (P.p > 1) {
-    RET(ensure(c, A.qr, rf * hl * 2));
-    RET(ensure(c, A.kr, rf * hl * 2));
-    RET(ensure(c, A.vr, rf * hl * 2));
-    RET(ensure(c, A.o, rf * hl * 2));
+    // receive layouts of A2aGeometry: full heads, then the position's partial-head units
+    RET(ensure(c, A.qr, std::max<size_t>(P.recv_q_elems(i), 1) * 2));
+    RET(ensure(c, A.kr, std::max<size_t>(P.recv_kv_elems(i), 1) * 2));
+    RET(ensure(c, A.vr, std::max<size_t>(P.recv_kv_elems(i), 1) * 2));
+    RET(ensure(c, A.o, std::max<size_t>(P.recv_q_elems(i), 1) * 2));
     RET(ensure(c, A.orecv, rows * D * 2));
     RET(ensure(c, A.ostage, rows * D * 2));
   } else {
@@ -435,37 +437,42 @@ int run_emulated(gs_ctx* c, const std::vector<std::vector<gs_xfer>>& plans, BufF
 // seq -> head: Q/K/V chunk j of position i (rows of i, heads of j) -> recv buffers of j.
 int exchange_qkv(gs_ctx* c, const Plan& P) {
   Scope sc(c, "a2a_qkv", 0);
+  // t = 0: Q (plan_q), t = 1, 2: K, V (plan_kv); they differ only for partial-head units
   if (c->emulated) {
-    std::vector<std::vector<gs_xfer>> plans(P.p);
-    for (int i = 0; i < P.p; ++i) plan_qkv(P, i, plans[i]);
+    std::vector<std::vector<gs_xfer>> qplans(P.p), kvplans(P.p);
+    for (int i = 0; i < P.p; ++i) {
+      plan_q(P, i, qplans[i]);
+      plan_kv(P, i, kvplans[i]);
+    }
     for (int t = 0; t < 3; ++t) {
       auto bufs = [&](int pos, int id) -> void* {
         RankArena& A = c->local[P.ranks[pos]];
         if (id == GS_BUF_SEND) return t == 0 ? A.qs.p : t == 1 ? A.ks.p : A.vs.p;
         return t == 0 ? A.qr.p : t == 1 ? A.kr.p : A.vr.p;
       };
-      RET(run_emulated(c, plans, bufs, 2));
+      RET(run_emulated(c, t == 0 ? qplans : kvplans, bufs, 2));
     }
     return GS_OK;
   }
   const int me = my_position(c, P);
-  std::vector<gs_xfer> plan;
-  plan_qkv(P, me, plan);
+  std::vector<gs_xfer> plans[2];
+  plan_q(P, me, plans[0]);
+  plan_kv(P, me, plans[1]);
   RankArena& A = c->local[0];
   bf16* snd[3] = {A.qs.as<bf16>(), A.ks.as<bf16>(), A.vs.as<bf16>()};
   bf16* rcv[3] = {A.qr.as<bf16>(), A.kr.as<bf16>(), A.vr.as<bf16>()};
   NK(ncclGroupStart());
-  for (const gs_xfer& x : plan)
-    for (int t = 0; t < 3; ++t) {
+  for (int t = 0; t < 3; ++t)
+    for (const gs_xfer& x : plans[t ? 1 : 0]) {
       if (x.op == GS_XFER_SEND)
         NK(ncclSend(snd[t] + x.src_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, c->stream));
       else if (x.op == GS_XFER_RECV)
         NK(ncclRecv(rcv[t] + x.dst_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, c->stream));
     }
   NK(ncclGroupEnd());
-  for (const gs_xfer& x : plan)
-    if (x.op == GS_XFER_COPY)
-      for (int t = 0; t < 3; ++t) RET(copy_block(c, rcv[t] + x.dst_off, snd[t] + x.src_off, x, 2));
+  for (int t = 0; t < 3; ++t)
+    for (const gs_xfer& x : plans[t ? 1 : 0])
+      if (x.op == GS_XFER_COPY) RET(copy_block(c, rcv[t] + x.dst_off, snd[t] + x.src_off, x, 2));
   return GS_OK;
 }
 
@@ -535,10 +542,10 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
     RopeParams rp{A.row_req.as<int>(), A.row_tok.as<int>(), A.req_grid.as<int>(), P.m->cs_tab, P.m->slot_axis,
                   P.m->p_max};
     PackParams pk{};
-    pk.ndest = P.p;
+    pk.ndest = P.nchunks();
     pk.rows = M;
-    for (int j = 0; j <= P.p; ++j) pk.head_off[j] = P.hoff[j];
-    for (int j = 0; j < P.p; ++j) pk.dest_off[j] = static_cast<long long>(M) * P.hoff[j] * P.hd;
+    for (int j = 0; j <= P.nchunks(); ++j) pk.head_off[j] = P.hoff[j];
+    for (int j = 0; j < P.nchunks(); ++j) pk.dest_off[j] = static_cast<long long>(M) * P.hoff[j] * P.hd;
     if (M) CK(qk_norm_rope_pack(A.qkv.as<bf16>(), M, D, P.H, w.g_q, w.g_k, eps, rp, pk, A.qs.as<bf16>(),
                                 A.ks.as<bf16>(), A.vs.as<bf16>(), c->stream));
   }
@@ -547,20 +554,38 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
 
 int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
   Scope sc(c, "attention", 1);
-  const int Hj = P.H_loc(j);
-  if (Hj == 0) return GS_OK;
   std::vector<int> so(P.B), sl(P.B);
   for (int r = 0; r < P.B; ++r) {
     so[r] = P.off_full[r];
     sl[r] = P.reqs[r]->n;
   }
-  const int rs = Hj * P.hd;
-  if (P.p == 1)
-    CK(attention_tc(A.qs.p, A.ks.p, A.vs.p, A.o.p, Hj, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
+  if (P.p == 1) {
+    const int rs = P.H * P.hd;
+    CK(attention_tc(A.qs.p, A.ks.p, A.vs.p, A.o.p, P.H, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
                     c->stream));
-  else
-    CK(attention_tc(A.qr.p, A.kr.p, A.vr.p, A.o.p, Hj, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
+    return GS_OK;
+  }
+  // full heads of this position
+  if (P.Hf) {
+    const int rs = P.Hf * P.hd;
+    CK(attention_tc(A.qr.p, A.kr.p, A.vr.p, A.o.p, P.Hf, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
                     c->stream));
+  }
+  // partial-head units: the unit's query chunk of every request against the head's full K / V
+  for (size_t t = 0; t < P.units_of[j].size(); ++t) {
+    const Unit& u = P.units[P.units_of[j][t]];
+    std::vector<int> qo(P.B), ql(P.B);
+    for (int r = 0; r < P.B; ++r) {
+      qo[r] = P.qpre(r, u.ci);
+      ql[r] = P.chunk_hi(r, u.ci) - P.chunk_lo(r, u.ci);
+    }
+    const bf16* q = A.qr.as<bf16>() + P.unit_q_off(j, static_cast<int>(t));
+    const bf16* k = A.kr.as<bf16>() + P.unit_kv_off(j, static_cast<int>(t));
+    const bf16* v = A.vr.as<bf16>() + P.unit_kv_off(j, static_cast<int>(t));
+    bf16* o = A.o.as<bf16>() + P.unit_q_off(j, static_cast<int>(t));
+    CK(attention_tc_segments(q, k, v, o, 1, P.hd, P.hd, P.hd, P.hd, qo.data(), ql.data(), so.data(), sl.data(), P.B,
+                             c->stream));
+  }
   return GS_OK;
 }
 

@@ -64,10 +64,10 @@ struct RopeParams {
   int p_max;
 };
 struct PackParams {
-  int ndest;
-  int head_off[9];       // head_off[j]..head_off[j+1]: heads of destination j
-  long long dest_off[8]; // element offset of destination chunk j in each send buffer
-  int rows;              // M (local rows; chunk j is [rows][H_j][d])
+  int ndest;              // pack chunks: p full-head chunks + one per partial head (<= 16)
+  int head_off[17];       // head_off[j]..head_off[j+1]: heads of chunk j
+  long long dest_off[16]; // element offset of chunk j in each send buffer
+  int rows;               // M (local rows; chunk j is [rows][H_j][d])
 };
 cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,

@@ -4,10 +4,12 @@
 // NCCL executor, the emulated executor and the CPU gloo tests (tests/test_plan_gloo.py).
 //
 // Partitioning readings: token shard i of p is [floor(i n / p), floor((i+1) n / p))
-// (reading 10); heads split contiguously, positions < H mod p get ceil(H / p) (reading 9).
+// (reading 10); heads: floor(H / p) full heads per position plus query-chunk units of the
+// H mod p remaining heads, balanced so every position does H / p heads of work (reading 9).
 #include "plan.h"
 
 #include <algorithm>
+#include <numeric>
 
 namespace gs {
 
@@ -16,7 +18,6 @@ void shard_bounds(int n, int p, int i, int* lo, int* hi) {
   *hi = static_cast<int>((static_cast<long long>(i + 1) * n) / p);
 }
 
-int head_offset(int H, int p, int j) { return j * (H / p) + std::min(j, H % p); }
 
 void A2aGeometry::init(int p_, const int* n_tokens, int nreq, int heads_, int hd_) {
   p = p_;
@@ -24,8 +25,22 @@ void A2aGeometry::init(int p_, const int* n_tokens, int nreq, int heads_, int hd
   H = heads_;
   hd = hd_;
   n.assign(n_tokens, n_tokens + nreq);
-  hoff.resize(p + 1);
-  for (int j = 0; j <= p; ++j) hoff[j] = head_offset(H, p, j);
+  Hf = H / p;
+  R = H % p;
+  const int gg = R ? std::gcd(R, p) : p;
+  c = R ? p / gg : 1;
+  hoff.resize(p + R + 1);
+  for (int j = 0; j <= p; ++j) hoff[j] = j * Hf;
+  for (int u = 1; u <= R; ++u) hoff[p + u] = p * Hf + u;
+  units.clear();
+  units_of.assign(p, {});
+  if (R) {
+    const int per = R / gg;  // units per position
+    for (int k = 0; k < R * c; ++k) {
+      units.push_back({k / per, p * Hf + k / c, k % c});
+      units_of[k / per].push_back(k);
+    }
+  }
   off_full.resize(B);
   rows_full = 0;
   for (int r = 0; r < B; ++r) {
@@ -64,94 +79,190 @@ gs_xfer flat(int op, int peer, int sb, long long so, int db, long long dof, long
 }
 }  // namespace
 
-// seq -> head (Q, K, V; the plan applies to each of the three buffers).
-// send buffer of position i: [dest j][rows_i][H_j][d]; recv buffer of j: [rows_full][H_j][d].
-void plan_qkv(const A2aGeometry& g, int me, std::vector<gs_xfer>& out) {
-  out.clear();
-  const long long d = g.hd;
-  const long long Hm = g.H_loc(me);
-  for (int j = 0; j < g.p; ++j) {  // my rows, heads of j -> j
-    const long long Hj = g.H_loc(j);
+// seq -> head, full heads (identical for Q, K and V): chunk j of my rows -> position j.
+void plan_full(const A2aGeometry& g, int me, std::vector<gs_xfer>& out) {
+  const long long d = g.hd, Hf = g.Hf;
+  if (!Hf) return;
+  for (int j = 0; j < g.p; ++j) {
     const long long chunk = static_cast<long long>(g.rows[me]) * g.hoff[j] * d;
     for (int r = 0; r < g.B; ++r) {
-      const long long cnt = static_cast<long long>(g.hi[me][r] - g.lo[me][r]) * Hj * d;
+      const long long cnt = static_cast<long long>(g.hi[me][r] - g.lo[me][r]) * Hf * d;
       if (!cnt) continue;
-      const long long so = chunk + static_cast<long long>(g.loff[me][r]) * Hj * d;
+      const long long so = chunk + static_cast<long long>(g.loff[me][r]) * Hf * d;
+      const long long dof = static_cast<long long>(g.off_full[r] + g.lo[me][r]) * Hf * d;
       if (j == me)
-        out.push_back(flat(GS_XFER_COPY, -1, GS_BUF_SEND, so, GS_BUF_RECV,
-                           static_cast<long long>(g.off_full[r] + g.lo[me][r]) * Hm * d, cnt));
+        out.push_back(flat(GS_XFER_COPY, -1, GS_BUF_SEND, so, GS_BUF_RECV, dof, cnt));
       else
         out.push_back(flat(GS_XFER_SEND, j, GS_BUF_SEND, so, -1, -1, cnt));
     }
   }
-  for (int i = 0; i < g.p; ++i) {  // rows of i, my heads <- i
+  for (int i = 0; i < g.p; ++i) {
     if (i == me) continue;
     for (int r = 0; r < g.B; ++r) {
-      const long long cnt = static_cast<long long>(g.hi[i][r] - g.lo[i][r]) * Hm * d;
+      const long long cnt = static_cast<long long>(g.hi[i][r] - g.lo[i][r]) * Hf * d;
       if (!cnt) continue;
       out.push_back(flat(GS_XFER_RECV, i, -1, -1, GS_BUF_RECV,
-                         static_cast<long long>(g.off_full[r] + g.lo[i][r]) * Hm * d, cnt));
+                         static_cast<long long>(g.off_full[r] + g.lo[i][r]) * Hf * d, cnt));
     }
   }
 }
 
-// head -> seq (O).  O buffer of position j: [rows_full][H_j][d] (attention output); the rows of
-// position i arrive in a staging buffer [src j][req r][rows][H_j d] and are unpacked by 2-D copies
-// into orecv [rows_i][D] at column H offset hoff[j] * d.
+// Position of unit k inside its position's unit list.
+static int local_unit(const A2aGeometry& g, int k) {
+  const auto& v = g.units_of[g.units[k].pos];
+  return static_cast<int>(std::find(v.begin(), v.end(), k) - v.begin());
+}
+
+// K / V: full heads as above; a partial head's K / V of all my rows go to every unit of that head.
+// send buffer of position i: pack chunks (chunk j = [rows_i][H_j][d]); recv buffer of j: see
+// A2aGeometry (full heads, then per local unit [rows_full][d]).
+void plan_kv(const A2aGeometry& g, int me, std::vector<gs_xfer>& out) {
+  out.clear();
+  plan_full(g, me, out);
+  const long long d = g.hd;
+  for (size_t k = 0; k < g.units.size(); ++k) {  // my K / V rows of the unit's head -> unit's position
+    const Unit& u = g.units[k];
+    const long long src0 = static_cast<long long>(g.rows[me]) * g.hoff[g.p + (u.head - g.p * g.Hf)] * d;
+    for (int r = 0; r < g.B; ++r) {
+      const long long cnt = static_cast<long long>(g.hi[me][r] - g.lo[me][r]) * d;
+      if (!cnt) continue;
+      const long long so = src0 + static_cast<long long>(g.loff[me][r]) * d;
+      const long long dof = g.unit_kv_off(u.pos, local_unit(g, static_cast<int>(k))) +
+                            static_cast<long long>(g.off_full[r] + g.lo[me][r]) * d;
+      if (u.pos == me)
+        out.push_back(flat(GS_XFER_COPY, -1, GS_BUF_SEND, so, GS_BUF_RECV, dof, cnt));
+      else
+        out.push_back(flat(GS_XFER_SEND, u.pos, GS_BUF_SEND, so, -1, -1, cnt));
+    }
+  }
+  for (int i = 0; i < g.p; ++i) {  // everyone's rows of my units' heads
+    if (i == me) continue;
+    for (size_t t = 0; t < g.units_of[me].size(); ++t)
+      for (int r = 0; r < g.B; ++r) {
+        const long long cnt = static_cast<long long>(g.hi[i][r] - g.lo[i][r]) * d;
+        if (!cnt) continue;
+        out.push_back(flat(GS_XFER_RECV, i, -1, -1, GS_BUF_RECV,
+                           g.unit_kv_off(me, static_cast<int>(t)) + static_cast<long long>(g.off_full[r] + g.lo[i][r]) * d,
+                           cnt));
+      }
+  }
+}
+
+// Q: full heads as above; for a partial unit only my rows inside its query chunk.
+void plan_q(const A2aGeometry& g, int me, std::vector<gs_xfer>& out) {
+  out.clear();
+  plan_full(g, me, out);
+  const long long d = g.hd;
+  for (size_t k = 0; k < g.units.size(); ++k) {
+    const Unit& u = g.units[k];
+    const long long src0 = static_cast<long long>(g.rows[me]) * g.hoff[g.p + (u.head - g.p * g.Hf)] * d;
+    const long long dst0 = g.unit_q_off(u.pos, local_unit(g, static_cast<int>(k)));
+    for (int r = 0; r < g.B; ++r) {
+      const int clo = g.chunk_lo(r, u.ci), chi = g.chunk_hi(r, u.ci);
+      const int a = std::max(g.lo[me][r], clo), b = std::min(g.hi[me][r], chi);
+      if (a >= b) continue;
+      const long long cnt = static_cast<long long>(b - a) * d;
+      const long long so = src0 + static_cast<long long>(g.loff[me][r] + a - g.lo[me][r]) * d;
+      const long long dof = dst0 + static_cast<long long>(g.qpre(r, u.ci) + a - clo) * d;
+      if (u.pos == me)
+        out.push_back(flat(GS_XFER_COPY, -1, GS_BUF_SEND, so, GS_BUF_RECV, dof, cnt));
+      else
+        out.push_back(flat(GS_XFER_SEND, u.pos, GS_BUF_SEND, so, -1, -1, cnt));
+    }
+  }
+  for (int i = 0; i < g.p; ++i) {
+    if (i == me) continue;
+    for (size_t t = 0; t < g.units_of[me].size(); ++t) {
+      const Unit& u = g.units[g.units_of[me][t]];
+      const long long dst0 = g.unit_q_off(me, static_cast<int>(t));
+      for (int r = 0; r < g.B; ++r) {
+        const int clo = g.chunk_lo(r, u.ci), chi = g.chunk_hi(r, u.ci);
+        const int a = std::max(g.lo[i][r], clo), b = std::min(g.hi[i][r], chi);
+        if (a >= b) continue;
+        out.push_back(flat(GS_XFER_RECV, i, -1, -1, GS_BUF_RECV, dst0 + static_cast<long long>(g.qpre(r, u.ci) + a - clo) * d,
+                           static_cast<long long>(b - a) * d));
+      }
+    }
+  }
+}
+
+// head -> seq (O).  O buffer of position j: the Q receive layout (full heads [rows_full][Hf][d],
+// then per local unit [qrows][d]).  Rows of position i arrive in a staging buffer (one contiguous
+// slot per message) and are unpacked by 2-D copies into orecv [rows_i][D] at the head's columns.
 void plan_o(const A2aGeometry& g, int me, std::vector<gs_xfer>& out, long long* stage_elems) {
   out.clear();
   const long long d = g.hd, D = static_cast<long long>(g.H) * d;
-  const long long wm = g.H_loc(me) * d;
-  for (int i = 0; i < g.p; ++i) {
-    if (i == me) continue;
-    for (int r = 0; r < g.B; ++r) {
-      const long long cnt = static_cast<long long>(g.hi[i][r] - g.lo[i][r]) * wm;
-      if (!cnt) continue;
-      out.push_back(flat(GS_XFER_SEND, i, GS_BUF_O, static_cast<long long>(g.off_full[r] + g.lo[i][r]) * wm, -1, -1,
-                         cnt));
-    }
+  const long long wf = static_cast<long long>(g.Hf) * d;  // full-head row width
+  std::vector<gs_xfer> copies;
+  auto unpack = [&](int src_buf, long long src_off, long long src_pitch, int r, int a, long long rows, long long col,
+                    long long width) {
+    gs_xfer x{};
+    x.op = GS_XFER_COPY;
+    x.peer = -1;
+    x.src_buf = src_buf;
+    x.src_off = src_off;
+    x.dst_buf = GS_BUF_ORECV;
+    x.dst_off = static_cast<long long>(g.loff[me][r] + a - g.lo[me][r]) * D + col;
+    x.rows = rows;
+    x.width = width;
+    x.src_pitch = src_pitch;
+    x.dst_pitch = D;
+    copies.push_back(x);
+  };
+  long long stage = 0;
+  // my full heads -> the rows' owners
+  if (wf)
+    for (int i = 0; i < g.p; ++i)
+      for (int r = 0; r < g.B; ++r) {
+        const long long rows = g.hi[i][r] - g.lo[i][r];
+        if (!rows) continue;
+        const long long so = static_cast<long long>(g.off_full[r] + g.lo[i][r]) * wf;
+        if (i == me)
+          unpack(GS_BUF_O, so, wf, r, g.lo[me][r], rows, static_cast<long long>(g.hoff[me]) * d, wf);
+        else
+          out.push_back(flat(GS_XFER_SEND, i, GS_BUF_O, so, -1, -1, rows * wf));
+      }
+  // my partial units: each owner gets its rows inside the unit's query chunk
+  for (size_t t = 0; t < g.units_of[me].size(); ++t) {
+    const Unit& u = g.units[g.units_of[me][t]];
+    const long long base = g.unit_q_off(me, static_cast<int>(t));
+    for (int i = 0; i < g.p; ++i)
+      for (int r = 0; r < g.B; ++r) {
+        const int clo = g.chunk_lo(r, u.ci), chi = g.chunk_hi(r, u.ci);
+        const int a = std::max(g.lo[i][r], clo), b = std::min(g.hi[i][r], chi);
+        if (a >= b) continue;
+        const long long so = base + static_cast<long long>(g.qpre(r, u.ci) + a - clo) * d;
+        if (i == me)
+          unpack(GS_BUF_O, so, d, r, a, b - a, static_cast<long long>(u.head) * d, d);
+        else
+          out.push_back(flat(GS_XFER_SEND, i, GS_BUF_O, so, -1, -1, static_cast<long long>(b - a) * d));
+      }
   }
-  long long acc = 0;
-  std::vector<long long> stage_off(static_cast<size_t>(g.p) * g.B, 0);
-  for (int j = 0; j < g.p; ++j)
-    for (int r = 0; r < g.B; ++r) {
-      stage_off[static_cast<size_t>(j) * g.B + r] = acc;
-      if (j != me) acc += static_cast<long long>(g.hi[me][r] - g.lo[me][r]) * g.H_loc(j) * d;
-    }
-  if (stage_elems) *stage_elems = acc;
+  // receive my rows from the other positions: their full heads, then their units
   for (int j = 0; j < g.p; ++j) {
     if (j == me) continue;
-    const long long wj = g.H_loc(j) * d;
-    for (int r = 0; r < g.B; ++r) {
-      const long long cnt = static_cast<long long>(g.hi[me][r] - g.lo[me][r]) * wj;
-      if (!cnt) continue;
-      out.push_back(flat(GS_XFER_RECV, j, -1, -1, GS_BUF_STAGE, stage_off[static_cast<size_t>(j) * g.B + r], cnt));
-    }
-  }
-  for (int j = 0; j < g.p; ++j) {  // unpack (after the exchange completes)
-    const long long wj = g.H_loc(j) * d;
-    for (int r = 0; r < g.B; ++r) {
-      const long long rows = g.hi[me][r] - g.lo[me][r];
-      if (!rows || !wj) continue;
-      gs_xfer x{};
-      x.op = GS_XFER_COPY;
-      x.peer = -1;
-      if (j == me) {
-        x.src_buf = GS_BUF_O;
-        x.src_off = static_cast<long long>(g.off_full[r] + g.lo[me][r]) * wm;
-      } else {
-        x.src_buf = GS_BUF_STAGE;
-        x.src_off = stage_off[static_cast<size_t>(j) * g.B + r];
+    if (wf)
+      for (int r = 0; r < g.B; ++r) {
+        const long long rows = g.hi[me][r] - g.lo[me][r];
+        if (!rows) continue;
+        out.push_back(flat(GS_XFER_RECV, j, -1, -1, GS_BUF_STAGE, stage, rows * wf));
+        unpack(GS_BUF_STAGE, stage, wf, r, g.lo[me][r], rows, static_cast<long long>(g.hoff[j]) * d, wf);
+        stage += rows * wf;
       }
-      x.dst_buf = GS_BUF_ORECV;
-      x.dst_off = static_cast<long long>(g.loff[me][r]) * D + static_cast<long long>(g.hoff[j]) * d;
-      x.rows = rows;
-      x.width = wj;
-      x.src_pitch = wj;
-      x.dst_pitch = D;
-      out.push_back(x);
+    for (int k : g.units_of[j]) {
+      const Unit& u = g.units[k];
+      for (int r = 0; r < g.B; ++r) {
+        const int clo = g.chunk_lo(r, u.ci), chi = g.chunk_hi(r, u.ci);
+        const int a = std::max(g.lo[me][r], clo), b = std::min(g.hi[me][r], chi);
+        if (a >= b) continue;
+        out.push_back(flat(GS_XFER_RECV, j, -1, -1, GS_BUF_STAGE, stage, static_cast<long long>(b - a) * d));
+        unpack(GS_BUF_STAGE, stage, d, r, a, b - a, static_cast<long long>(u.head) * d, d);
+        stage += static_cast<long long>(b - a) * d;
+      }
     }
   }
+  if (stage_elems) *stage_elems = stage;
+  out.insert(out.end(), copies.begin(), copies.end());  // unpack after the exchange
 }
 
 // Re-shard of one request's latent [n, lat] from (old_ranks, old_p) to (new_ranks, new_p):
@@ -202,8 +313,11 @@ extern "C" int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_token
   gs::A2aGeometry g;
   g.init(p, n_tokens, nreq, heads, head_dim);
   std::vector<gs_xfer> v;
-  if (kind == 0) {
-    gs::plan_qkv(g, me, v);
+  if (kind == 0 || kind == 2) {
+    if (kind == 0)
+      gs::plan_kv(g, me, v);
+    else
+      gs::plan_q(g, me, v);
     if (stage_elems) *stage_elems = 0;
   } else if (kind == 1) {
     gs::plan_o(g, me, v, stage_elems);

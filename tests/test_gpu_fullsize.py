@@ -215,3 +215,21 @@ def test_config5_mixed_coserving_trace_bit_exact(gs):
         ctx.release(r)
         assert np.array_equal(got[f"I{i}"].view(np.uint32), ref.view(np.uint32)), f"I{i}"
     ctx.close()
+
+
+def test_config3_sp_degrees_balanced_heads_bit_exact_fullsize(gs):
+    """Config 3: 480x832, 81 frames (32,760 tokens), Wan-1.3B-shaped (12 heads, 1 layer) at SP 1/2/4/8.
+    At p = 8 the 12 heads split into 1 full head + half a head (a query chunk) per position
+    (reading 9); every degree must give identical bytes."""
+    shape = sm.WAN_1_3B
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, 1, shape.weight_seed)
+    zs = {}
+    for p in (1, 2, 4, 8):
+        req = ctx.submit(mid, 832, 480, 81, 50, 1000, list(range(p)))
+        assert ctx.run_steps([req], list(range(p)), 2) == 2
+        zs[p] = ctx.read_latent(req)
+        ctx.release(req)
+    ctx.close()
+    for p in (2, 4, 8):
+        assert np.array_equal(zs[p].view(np.uint32), zs[1].view(np.uint32)), p

@@ -3,8 +3,10 @@ Ulysses all-to-alls and the resume re-shard (row
 (1) for all positions in one process with NCCL's matching rule and (2) by two real processes over
 torch.distributed `gloo` (world_size 2), and the resulting buffers are checked against the
 layouts include/gs.h defines, re-derived here from the partition readings (readings 9,
-10): token shard i of p = [i n // p, (i+1) n // p), contiguous head split with positions < H mod p
-holding ceil(H/p) heads."""
+10): token shard i of p = [i n // p, (i+1) n // p); every position holds H // p full heads and the
+H % p remaining heads are cut into c = p / gcd(H % p, p) query chunks dealt out in order,
+(H % p) / gcd per position (balanced work units)."""
+import math
 import os
 import socket
 
@@ -18,17 +20,47 @@ def shards(n, p):
     return [(i * n // p, (i + 1) * n // p) for i in range(p)]
 
 
-def head_offsets(H, p):
-    return [j * (H // p) + min(j, H % p) for j in range(p + 1)]
+class Units:
+    """Balanced head partition (reading 9), re-derived independently of plan.cpp."""
+
+    def __init__(self, H, p):
+        self.Hf, self.R = H // p, H % p
+        g = math.gcd(self.R, p) if self.R else p
+        self.c = p // g if self.R else 1
+        per = self.R // g if self.R else 0
+        self.units = [(k // per, p * self.Hf + k // self.c, k % self.c) for k in range(self.R * self.c)]
+        self.of = [[u for u in self.units if u[0] == j] for j in range(p)]
+        # pack chunks: p full-head chunks, then one chunk per partial head
+        self.chunks = [list(range(j * self.Hf, (j + 1) * self.Hf)) for j in range(p)] + \
+                      [[p * self.Hf + u] for u in range(self.R)]
+
+    def chunk_rows(self, n, ci):
+        return ci * n // self.c, (ci + 1) * n // self.c
 
 
 # ----------------------------------------------------------------------------- reference layouts
 def send_buffer(q, ns, p, i, H, d):
-    """Pack layout of position i: [dest j][rows_i][H_j][d] (rows_i = its shards of each request)."""
-    hoff = head_offsets(H, p)
+    """Pack layout of position i: chunk j = [rows_i][heads of chunk j][d], chunks in order."""
+    U = Units(H, p)
     offs = np.cumsum([0] + ns[:-1])
     rows = np.concatenate([q[o + lo:o + hi] for o, n in zip(offs, ns) for lo, hi in [shards(n, p)[i]]])
-    return np.concatenate([rows[:, hoff[j]:hoff[j + 1], :].ravel() for j in range(p)])
+    return np.concatenate([rows[:, hs, :].ravel() for hs in U.chunks if hs] + [np.zeros(0, q.dtype)])
+
+
+def recv_layout(x, ns, p, j, H, kind):
+    """Receive layout at position j: full heads [rows][Hf][d], then per local unit a [rows][d]
+    block: all rows (kind 'kv') or the unit's query-chunk rows of every request (kind 'q', also the
+    attention-output layout)."""
+    U = Units(H, p)
+    offs = np.cumsum([0] + ns[:-1])
+    parts = [x[:, j * U.Hf:(j + 1) * U.Hf, :].ravel()]
+    for _pos, h, ci in U.of[j]:
+        if kind == "kv":
+            parts.append(x[:, h, :].ravel())
+        else:
+            parts.append(np.concatenate([x[o + a:o + b, h, :] for o, n in zip(offs, ns)
+                                         for a, b in [U.chunk_rows(n, ci)]]).ravel())
+    return np.concatenate(parts)
 
 
 def execute(plans, bufs):
@@ -63,7 +95,21 @@ def copy_block(bufs, x):
 CASES = [
     (1, [256], 6, 4), (2, [4096 // 64], 12, 8), (2, [33, 17, 64], 12, 8), (4, [1001], 40, 4),
     (8, [75600 // 100], 40, 4), (8, [32760 // 40], 12, 8), (8, [7, 300, 13], 12, 4), (4, [3], 6, 2),
+    (8, [101, 29], 6, 4), (4, [55, 2, 77], 6, 4), (8, [300], 13, 2), (2, [9, 1], 5, 2),
 ]
+
+
+def test_balanced_units_cover_every_head_row_once_and_balance_work():
+    for H in range(1, 41):
+        for p in (1, 2, 4, 8):
+            U = Units(H, p)
+            work = [U.Hf * 1.0] * p
+            cover = {}
+            for pos, h, ci in U.units:
+                work[pos] += 1.0 / U.c
+                cover[(h, ci)] = cover.get((h, ci), 0) + 1
+            assert all(abs(w - H / p) < 1e-12 for w in work), (H, p, work)
+            assert len(cover) == U.R * U.c and set(cover.values()) <= {1}
 
 
 @pytest.mark.parametrize("p,ns,H,d", CASES)
@@ -72,22 +118,21 @@ def test_a2a_plans_realise_ulysses_layouts(p, ns, H, d):
     N = sum(ns)
     q = g.integers(-1000, 1000, (N, H, d)).astype(np.int64)
     o = g.integers(-1000, 1000, (N, H, d)).astype(np.int64)
-    hoff = head_offsets(H, p)
     offs = np.cumsum([0] + ns[:-1])
-    # seq -> head
-    plans = [gs.plan_a2a(0, p, i, ns, H, d)[0] for i in range(p)]
-    bufs = [{gs.BUF_SEND: send_buffer(q, ns, p, i, H, d),
-             gs.BUF_RECV: np.full(N * (hoff[i + 1] - hoff[i]) * d, -7, np.int64)} for i in range(p)]
-    execute(plans, bufs)
-    for j in range(p):
-        want = q[:, hoff[j]:hoff[j + 1], :].ravel()
-        np.testing.assert_array_equal(bufs[j][gs.BUF_RECV], want)
+    # seq -> head: K / V (kind 0) and Q (kind 2)
+    for kind, name in ((0, "kv"), (2, "q")):
+        plans = [gs.plan_a2a(kind, p, i, ns, H, d)[0] for i in range(p)]
+        bufs = [{gs.BUF_SEND: send_buffer(q, ns, p, i, H, d),
+                 gs.BUF_RECV: np.full(recv_layout(q, ns, p, i, H, name).size, -7, np.int64)} for i in range(p)]
+        execute(plans, bufs)
+        for j in range(p):
+            np.testing.assert_array_equal(bufs[j][gs.BUF_RECV], recv_layout(q, ns, p, j, H, name), err_msg=name)
     # head -> seq
     plans, stages = zip(*[gs.plan_a2a(1, p, i, ns, H, d) for i in range(p)])
     bufs = []
     for i in range(p):
         rows_i = sum(hi - lo for n in ns for lo, hi in [shards(n, p)[i]])
-        bufs.append({gs.BUF_O: o[:, hoff[i]:hoff[i + 1], :].ravel().copy(),
+        bufs.append({gs.BUF_O: recv_layout(o, ns, p, i, H, "q").copy(),
                      gs.BUF_STAGE: np.full(max(stages[i], 1), -9, np.int64),
                      gs.BUF_ORECV: np.full(rows_i * H * d, -5, np.int64)})
     execute(plans, bufs)
@@ -173,22 +218,22 @@ def _worker(rank, world, port, errq):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        p, ns, H, d = 2, [37, 64, 5], 12, 4
+        p, ns, H, d = 2, [37, 64, 5], 13, 4  # 13 heads: 6 full each + one head in query halves
         N = sum(ns)
         g = np.random.default_rng(7)      # same seed: every rank knows the global tensors
         q = g.integers(-99, 99, (N, H, d)).astype(np.int64)
         o = g.integers(-99, 99, (N, H, d)).astype(np.int64)
-        hoff = head_offsets(H, p)
         offs = np.cumsum([0] + ns[:-1])
         me = rank
-        plan, _ = gs.plan_a2a(0, p, me, ns, H, d)
-        bufs = {gs.BUF_SEND: send_buffer(q, ns, p, me, H, d),
-                gs.BUF_RECV: np.full(N * (hoff[me + 1] - hoff[me]) * d, -7, np.int64)}
-        _run_plan_dist(dist, torch, plan, bufs)
-        np.testing.assert_array_equal(bufs[gs.BUF_RECV], q[:, hoff[me]:hoff[me + 1], :].ravel())
+        for kind, name in ((0, "kv"), (2, "q")):
+            plan, _ = gs.plan_a2a(kind, p, me, ns, H, d)
+            bufs = {gs.BUF_SEND: send_buffer(q, ns, p, me, H, d),
+                    gs.BUF_RECV: np.full(recv_layout(q, ns, p, me, H, name).size, -7, np.int64)}
+            _run_plan_dist(dist, torch, plan, bufs)
+            np.testing.assert_array_equal(bufs[gs.BUF_RECV], recv_layout(q, ns, p, me, H, name))
         plan, stage = gs.plan_a2a(1, p, me, ns, H, d)
         rows_me = sum(hi - lo for n in ns for lo, hi in [shards(n, p)[me]])
-        bufs = {gs.BUF_O: o[:, hoff[me]:hoff[me + 1], :].ravel().copy(),
+        bufs = {gs.BUF_O: recv_layout(o, ns, p, me, H, "q").copy(),
                 gs.BUF_STAGE: np.zeros(max(stage, 1), np.int64),
                 gs.BUF_ORECV: np.zeros(rows_me * H * d, np.int64)}
         _run_plan_dist(dist, torch, plan, bufs)
