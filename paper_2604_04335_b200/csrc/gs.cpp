@@ -73,6 +73,34 @@ int ensure(gs_ctx* c, DevBuf& b, size_t bytes) {
   return GS_OK;
 }
 
+// ------------------------------------------------------------------ caching allocator
+constexpr size_t kPoolGrain = size_t(2) << 20;  // 2 MiB blocks
+
+size_t pool_round(size_t bytes) { return (std::max<size_t>(bytes, 1) + kPoolGrain - 1) / kPoolGrain * kPoolGrain; }
+
+void* pool_alloc(gs_ctx* c, size_t bytes) {
+  const size_t sz = pool_round(bytes);
+  auto it = c->pool.find(sz);
+  if (it != c->pool.end()) {
+    void* p = it->second;
+    c->pool.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, sz) == cudaSuccess) return p;
+  cudaGetLastError();
+  cudaStreamSynchronize(c->stream);  // out of memory: return the cached blocks and retry
+  for (auto& kv : c->pool) cudaFree(kv.second);
+  c->pool.clear();
+  if (cudaMalloc(&p, sz) == cudaSuccess) return p;
+  cudaGetLastError();
+  return nullptr;
+}
+
+void pool_free(gs_ctx* c, void* p, size_t bytes) {
+  if (p) c->pool.emplace(pool_round(bytes), p);
+}
+
 // ------------------------------------------------------------------ profiling scopes
 cudaEvent_t get_event(gs_ctx* c) {
   if (!c->event_pool.empty()) {
@@ -767,12 +795,9 @@ Request* find_req(gs_ctx* c, gs_req id) {
 }
 
 int alloc_shard(gs_ctx* c, Shard& s, int lat) {
-  const size_t bytes = static_cast<size_t>(std::max(s.hi - s.lo, 1)) * lat * 4;
-  if (cudaMalloc(&s.z, bytes) != cudaSuccess) {
-    cudaGetLastError();
-    s.z = nullptr;
-    return fail(c, GS_ENOMEM, "latent shard alloc failed");
-  }
+  s.bytes = static_cast<size_t>(std::max(s.hi - s.lo, 1)) * lat * 4;
+  s.z = static_cast<float*>(pool_alloc(c, s.bytes));
+  if (!s.z) return fail(c, GS_ENOMEM, "latent shard alloc failed");
   return GS_OK;
 }
 
@@ -785,7 +810,9 @@ int ensure_text_cache(gs_ctx* c, Model* m, Request* q, int li) {
   if (buf.p) return GS_OK;
   const int Lt = m->desc.text_len, T = m->desc.text_dim, D = m->desc.dim, NL = m->desc.layers, nb = q->nb;
   const size_t per = static_cast<size_t>(Lt) * D;
-  RET(ensure(c, buf, static_cast<size_t>(nb) * NL * 2 * per * 2));
+  buf.cap = static_cast<size_t>(nb) * NL * 2 * per * 2;
+  buf.p = pool_alloc(c, buf.cap);
+  if (!buf.p) return fail(c, GS_ENOMEM, "text cache alloc failed");
   DevBuf emb, h1, cx, kv;
   auto cleanup = [&] {
     cudaStreamSynchronize(c->stream);
@@ -827,17 +854,23 @@ int ensure_text_cache(gs_ctx* c, Model* m, Request* q, int li) {
   } while (0);
   cleanup();
   if (rc != GS_OK && buf.p) {
-    cudaFree(buf.p);
+    pool_free(c, buf.p, buf.cap);
     buf.p = nullptr;
     buf.cap = 0;
   }
   return rc;
 }
 
-void free_text_cache(Request* q) {
-  for (auto& kv : q->ctx_kv)
-    if (kv.second.p) cudaFree(kv.second.p);
+void free_text_cache(gs_ctx* c, Request* q) {
+  for (auto& kv : q->ctx_kv) pool_free(c, kv.second.p, kv.second.cap);
   q->ctx_kv.clear();
+}
+
+void free_shards(gs_ctx* c, std::vector<Shard>& v) {
+  for (Shard& s : v) {
+    pool_free(c, s.z, s.bytes);
+    s.z = nullptr;
+  }
 }
 
 }  // namespace
@@ -910,10 +943,11 @@ void gs_destroy(gs_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& kv : c->reqs) {
-    for (auto& s : kv.second->shards)
-      if (s.z) cudaFree(s.z);
-    free_text_cache(kv.second.get());
+    free_shards(c, kv.second->shards);
+    free_text_cache(c, kv.second.get());
   }
+  for (auto& kv : c->pool) cudaFree(kv.second);
+  c->pool.clear();
   for (auto& m : c->models)
     for (void* p : m->allocs) cudaFree(p);
   for (auto& A : c->local) {
@@ -1243,9 +1277,8 @@ int gs_resume(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
       if (x.op == GS_XFER_COPY) RET(copy_block(c, zn + x.dst_off, zo + x.src_off, x, 4));
   }
   CK(cudaStreamSynchronize(c->stream));
-  for (Shard& o : q->shards)
-    if (o.z) cudaFree(o.z);
-  free_text_cache(q);  // rebuilt on the new ranks at their first step
+  free_shards(c, q->shards);
+  free_text_cache(c, q);  // rebuilt on the new ranks at their first step
   q->shards = ns;
   q->ranks.assign(ranks, ranks + nranks);
   q->state = q->step_idx >= q->steps ? GS_REQ_DONE : GS_REQ_PLACED;
@@ -1293,9 +1326,8 @@ int gs_release(gs_ctx* c, gs_req id) {
   if (it->second->state == GS_REQ_RUNNING) return fail(c, GS_ESTATE, "request is running");
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
-  for (auto& s : it->second->shards)
-    if (s.z) cudaFree(s.z);
-  free_text_cache(it->second.get());
+  free_shards(c, it->second->shards);
+  free_text_cache(c, it->second.get());
   c->reqs.erase(it);
   return GS_OK;
 }
@@ -1450,7 +1482,7 @@ int gs_debug_block(gs_ctx* c, int model, int layer, float* x, int nreq, const in
   RET(block_post(c, P, 0, A, layer));
   CK(cudaMemcpyAsync(x, A.x.p, xbytes, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  for (auto& q : own) free_text_cache(q.get());
+  for (auto& q : own) free_text_cache(c, q.get());
   prof_flush(c);
   return GS_OK;
 }

@@ -2,7 +2,7 @@
 # Profiling pass run under gpurun (one GPU): launch list of one bench step + ncu --set full of
 # the top kernels.  Outputs land in gpurun_out/ (scratch); summaries are copied to profiles/.
 set -x
-TAG=${TAG:-r01b}
+TAG=${TAG:-r01c}
 python paper_2604_04335_b200/build.py >/dev/null
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
