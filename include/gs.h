@@ -208,8 +208,9 @@ int gs_debug_attention(gs_ctx* ctx, const void* q, const void* k, const void* v,
  * segment); NULL otherwise. */
 int gs_debug_block(gs_ctx* ctx, int model, int layer, float* x, int nreq, const int* grids,
                    const int* tok_lo, const int* n_rows, const float* t, const void* prompts);
-/* Development aid: clock64 stamps written by the first attention CTA when the environment has
- * GS_ATTN_TRACE=1 (16 events x 32 KV tiles x 2 softmax groups); n <= 1024 entries to host. */
+/* Development aid: clock64 stamps written by attention CTAs 0 and 1 (for d = 128 a CTA pair) of
+ * head 0 when the environment has GS_ATTN_TRACE=1: [2 CTAs][16 events][32 KV tiles][2 softmax
+ * groups]; n <= 2048 entries to host, -1 if larger. */
 int gs_debug_attention_trace(unsigned long long* host, size_t n);
 /* Time embedding of nreq timesteps: e0 [nreq, D], e [nreq, 6D] fp32 (host outputs). */
 int gs_debug_time_embed(gs_ctx* ctx, int model, int nreq, const float* t, float* e0, float* e);

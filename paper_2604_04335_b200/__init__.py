@@ -316,11 +316,12 @@ class Context:
                                           _ints(flat), _ints(tok_lo), _ints(n_rows), _fl(t), pp))
         return x
 
-    def debug_attention_trace(self):
-        """clock64 stamps of the first attention CTA (needs GS_ATTN_TRACE=1 at process start)."""
-        buf = np.zeros(16 * 64, dtype=np.uint64)
+    def debug_attention_trace(self, cta=0):
+        """clock64 stamps of attention CTA `cta` (0, or 1 = CTA 0's pair peer for d = 128) of the
+        last launch (needs GS_ATTN_TRACE=1 at process start)."""
+        buf = np.zeros(2 * 16 * 64, dtype=np.uint64)
         self._ck(self._lib.gs_debug_attention_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.size))
-        return buf.reshape(16, 32, 2)
+        return buf.reshape(2, 16, 32, 2)[cta]
 
     def debug_time_embed(self, model, t, dim):
         e0 = np.zeros((len(t), dim), np.float32)

@@ -28,10 +28,11 @@
 
 namespace gs {
 // Development trace (GS_ATTN_TRACE=1): clock64 stamps of CTA (0,0) for the first 32 KV tiles.
-__device__ unsigned long long g_attn_trace[16 * 64];
+__device__ unsigned long long g_attn_trace[2 * 16 * 64];  // [CTA 0 / its pair peer][event][tile][group]
 namespace {
 #define TRACE_EV(ev, w, j) \
-  if (TRACE && blockIdx.x == 0 && blockIdx.y == 0 && (j) < 32) g_attn_trace[((ev) * 32 + (j)) * 2 + (w)] = clock64()
+  if (TRACE && blockIdx.x < 2 && blockIdx.y == 0 && (j) < 32) \
+    g_attn_trace[blockIdx.x * 1024 + ((ev) * 32 + (j)) * 2 + (w)] = clock64()
 
 constexpr int MAX_REQ = 64;
 constexpr int THREADS = 384;
@@ -249,35 +250,37 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t sv0 = smem_u32(smem + C::V_OFF);
       mbar_wait(q_full, 0);
       // issue without waiting: callers wait for K_j (kfull) / V_j (vfull) + P (pfull) first
+      // descriptors: start-address field (addr >> 4, 14 bits) advanced by plain adds; smem < 256 KB so no carry
+      const uint64_t qdesc0 = sdesc_sw128(sq, 16, 1024);
+      const uint64_t kdesc0 = sdesc_sw128(sk0, 16, 1024);
+      const uint64_t vdesc0 = sdesc_sw128(sv0, 16384, 1024);
       auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T -> TMEM cols [128 w, 128 w + 128)
         TRACE_EV(0, w, j);
-        const uint32_t qa = sq + w * C::TILE_BYTES;
-        const uint32_t kb = sk0 + (j % C::KST) * C::KT_BYTES;
+        const uint64_t qa = qdesc0 + ((w * C::TILE_BYTES) >> 4);
+        const uint64_t kb = kdesc0 + (((j % C::KST) * C::KT_BYTES) >> 4);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t qoff = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t koff = (kk >> 2) * C::KBOX_BYTES + (kk & 3) * 32;
+          const uint32_t qoff = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          const uint32_t koff = ((kk >> 2) * C::KBOX_BYTES + (kk & 3) * 32) >> 4;
           if (PAIR)
-            mma_ss_2sm(tmem + w * 128, sdesc_sw128(qa + qoff, 16, 1024), sdesc_sw128(kb + koff, 16, 1024),
-                       idesc_s, kk > 0);
+            mma_ss_2sm(tmem + w * 128, qa + qoff, kb + koff, idesc_s, kk > 0);
           else
-            mma_ss(tmem + w * 128, sdesc_sw128(qa + qoff, 16, 1024), sdesc_sw128(kb + koff, 16, 1024),
-                   idesc_s, kk > 0);
+            mma_ss(tmem + w * 128, qa + qoff, kb + koff, idesc_s, kk > 0);
         }
         commit(&sfull[w]);
         TRACE_EV(13, w, j);
       };
       auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j, P_w read from TMEM (bf16 over S_w)
         TRACE_EV(1, w, j);
-        const uint32_t vb = sv0 + (j % C::VST) * C::VT_BYTES;
+        const uint64_t vb = vdesc0 + (((j % C::VST) * C::VT_BYTES) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           if (PAIR)
-            mma_ts_2sm(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
-                       idesc_o, (j > 0) || (kk > 0));
+            mma_ts_2sm(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, vb + ((kk * 2048) >> 4), idesc_o,
+                       (j > 0) || (kk > 0));
           else
-            mma_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, sdesc_sw128(vb + kk * 2048, 16384, 1024),
-                   idesc_o, (j > 0) || (kk > 0));
+            mma_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, vb + ((kk * 2048) >> 4), idesc_o,
+                   (j > 0) || (kk > 0));
         }
         TRACE_EV(14, w, j);
       };
@@ -294,7 +297,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       commit(&kempty[0]);
       for (int j = 0; j < nkv; ++j) {
         const bool more = j + 1 < nkv;
-        // V_j and K_{j+1} landed long ago in steady state: check them before waiting on P
+        // V_j and K_{j+1} landed long ago in steady state: check them before waiting on P (folding
+        // these checks into P0's barrier via a helper warp was measured: no gain, see r01_notes.md)
         TRACE_EV(15, 0, j);
         mbar_wait_spin(&vfull[j % C::VST], (j / C::VST) & 1);
         if (more) mbar_wait_spin(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
@@ -388,8 +392,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         else
           mbar_arrive(&pfull[w]);
       }
-      if (TRACE && lane == 0 && blockIdx.x == 0 && blockIdx.y == 0 && j < 32)
-        g_attn_trace[((4 + quarter) * 32 + j) * 2 + w] = t_done;
+      if (TRACE && lane == 0 && blockIdx.x < 2 && blockIdx.y == 0 && j < 32)
+        g_attn_trace[blockIdx.x * 1024 + ((4 + quarter) * 32 + j) * 2 + w] = t_done;
     }
     // epilogue: O / l -> bf16 -> global
     mbar_wait(&ofull[w], 0);

@@ -14,6 +14,7 @@ ctx = gs.Context(device=0)
 N, H, d = 75600, 5, 128
 q, k, v = (torch.randn(N, H, d, device="cuda").to(torch.bfloat16) for _ in range(3))
 o = torch.empty_like(q)
+QKV = (q, k, v)
 for _ in range(2):
     ctx.debug_attention(q, k, v, o, H, d, [0], [N])
 t = ctx.debug_attention_trace().astype(np.int64)
@@ -51,3 +52,32 @@ for j in range(20, 26):
     print(f"tile {j}: K issued {t[8, j, 0] - t0}  V issued {t[9, j, 0] - t0}  MMA pfull0-ok {t[10, j, 0] - t0} "
           f"PV0 issued {t[1, j, 0] - t0}  pfull1-ok {t[10, j, 1] - t0} PV1 issued {t[1, j, 1] - t0}")
 ctx.close()
+
+# pair peer (CTA 1): its clock64 is another SM's counter, so compare durations, not stamps
+if d == 128:
+    ctx2 = gs.Context(device=0)
+    for _ in range(2):
+        ctx2.debug_attention(*QKV, o, H, d, [0], [N])
+    t0s = ctx2.debug_attention_trace(0).astype(np.int64)
+    t1s = ctx2.debug_attention_trace(1).astype(np.int64)
+    for name, tt in (("leader", t0s), ("peer", t1s)):
+        print(f"{name}: period {np.median(np.diff(tt[2, 4:30, 0]))} T_s {np.median(tt[4:8, 4:30, 0].max(0) - tt[2, 4:30, 0])}"
+              f" T_s WG1 {np.median(tt[4:8, 4:30, 1].max(0) - tt[2, 4:30, 1])}")
+    # offset estimate: wake events of both CTAs are triggered by the same multicast commit
+    off = np.median(t1s[2, 4:30, 0] - t0s[2, 4:30, 0])
+    print("peer clock offset (from wake of WG0, assumes simultaneous wake)", off)
+    for j in range(20, 24):
+        for w in range(2):
+            print(f" j={j} WG{w}: leader wake {t0s[2, j, w] - t0s[1, j, 0]:+d} Pdone {t0s[4:8, j, w].max() - t0s[1, j, 0]:+d}"
+                  f" | peer wake {t1s[2, j, w] - off - t0s[1, j, 0]:+.0f} Pdone {t1s[4:8, j, w].max() - off - t0s[1, j, 0]:+.0f}"
+                  f" | leader pfull_ok {t0s[10, j, w] - t0s[1, j, 0]:+d}")
+    ctx2.close()
+
+print("MMA-thread timeline rel. to PV0(j) issue: head, kv-ok | wait_p0, p0-ok, PV0 issue..end, S0(j+1) issue..end |"
+      " wait_p1, p1-ok, PV1 issue..end, S1(j+1) issue..end")
+for j in range(20, 24):
+    b = t[1, j, 0]
+    r = lambda e, w, jj=j: t[e, jj, w] - b  # noqa: E731
+    print(f" j={j}: {r(15, 0):+d} {r(11, 0):+d} | {r(12, 0):+d} {r(10, 0):+d} {r(1, 0):+d}..{r(14, 0):+d} "
+          f"{r(0, 0, j + 1):+d}..{r(13, 0, j + 1):+d} | {r(12, 1):+d} {r(10, 1):+d} {r(1, 1):+d}..{r(14, 1):+d} "
+          f"{r(0, 1, j + 1):+d}..{r(13, 1, j + 1):+d} | Pdone WG0 {t[4:8, j, 0].max() - b:+d} WG1 {t[4:8, j, 1].max() - b:+d}")
