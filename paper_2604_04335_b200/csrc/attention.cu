@@ -83,12 +83,13 @@ __device__ __forceinline__ constexpr bool poly_pair(int k) {
 // P = exp2(S * scale - m) for the 128 columns of this thread's row, packed to bf16 pairs and
 // stored over the S columns [0, 64) in TMEM (P aliases S).  Returns the fp32 partial row sums.
 // FULL = false is the last (partial) KV tile of a request: masked columns get p = 0 exactly.
-template <int POLY8, bool FULL>
-__device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[128], float2 sc2, float2 nm2,
-                                                 int kv_valid, uint32_t tS) {
+// NCOL = 64: the v6 column half [col0, col0 + 64) of the row (v holds those 64 values).
+template <int POLY8, bool FULL, int NCOL = 128>
+__device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], float2 sc2, float2 nm2,
+                                                 int kv_valid, uint32_t tS, int col0 = 0) {
   float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  for (int c = 0; c < NCOL / 32; ++c) {
     uint32_t pk[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -104,8 +105,8 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[128], float
         p.y = ex2_approx(x.y);
       }
       if (!FULL) {
-        p.x = col < kv_valid ? p.x : 0.f;
-        p.y = col + 1 < kv_valid ? p.y : 0.f;
+        p.x = col0 + col < kv_valid ? p.x : 0.f;
+        p.y = col0 + col + 1 < kv_valid ? p.y : 0.f;
       }
       if (i & 1)
         acc1 = __fadd2_rn(acc1, p);
@@ -430,10 +431,374 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// v6 (d = 128): one 128-row Q tile per CTA (256 per CTA pair, M = 256 cta_group::2 MMAs), with S
+// and P double-buffered in TMEM:
+//   cols [0,128) O  |  [128,256) S0  |  [256,384) S1  |  [384,448) P0  |  [448,512) P1.
+// S_{j+2} is issued into S_j's buffer as soon as the softmax has loaded S_j (sfree), ahead of
+// PV_j, so the softmax of tile j+1 starts as soon as tile j's ends: the per-tile period is
+// max(softmax, PV + S on the tensor core) instead of the v3-v5 chain softmax + hand-off + PV + S
+// (profiles/r01_notes.md).  P_j goes to buffer j & 1, free once PV_{j-2} completed: S_j's
+// completion is committed after PV_{j-2} is issued, so waiting for S_j implies it.  The lazy O rescale waits for PV_{j-1} (rare: only when the running max grows
+// by more than 2^8).
+// Softmax: two warps per TMEM lane quarter (warps q and q + 4), each owning one 64-column half of
+// the 32 rows' S / P / O; the halves exchange their partial row maxima through shared memory
+// (named barrier per warp pair).  Two warps per SMSP hide the MUFU / F2FP latencies a single
+// warp exposes (tools/micro/xu_mix_bench.cu: 2 ex2 + F2FP + FADD2 per pair = 19.9 cycles with
+// one warp, 16.2 = the MUFU floor with two).
+//   warps 0-7: softmax, warp 8: TMA producer, warp 9: TMEM owner + MMA issuer (leader CTA).
+constexpr int THREADS1 = 320;
+constexpr int kProducerWarp1 = 8, kMmaWarp1 = 9;
+struct Cfg1 {
+  static constexpr int HD = 128;
+  static constexpr int TILE_BYTES = 128 * HD * 2;   // this CTA's Q tile
+  static constexpr int KT_BYTES = 64 * HD * 2;      // 64 of the tile's 128 keys
+  static constexpr int KBOX_BYTES = 64 * 128;       // one [64 keys][64 d] box
+  static constexpr int VT_BYTES = 128 * 64 * 2;     // 64 of the d columns of all 128 keys
+  static constexpr int KST = 5, VST = 5;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = TILE_BYTES;
+  static constexpr int V_OFF = K_OFF + KST * KT_BYTES;
+  static constexpr int BAR_OFF = V_OFF + VST * VT_BYTES;
+  static constexpr int RED_OFF = BAR_OFF + 256;
+  static constexpr int SMEM = RED_OFF + 2 * 2 * 128 * 4 + 1024;
+  static constexpr uint32_t T_O = 0, T_S = 128, T_P = 384;
+};
+
+template <int POLY8, bool TRACE>
+__global__ void __launch_bounds__(THREADS1, 1)
+    attn_db_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
+                   const __grid_constant__ SeqTable tab, float scale_log2, int flags) {
+  using C = Cfg1;
+  // flags (development A/B, GS_ATTN_FLAGS): bit 0 = softmax waits suspend (try_wait) instead of
+  // polling test_wait, bit 1 = same for the MMA issuer.  Polling loops are MIO-queue traffic that
+  // competes with MUFU (ncu: MUFU stalls on mio_throttle).
+  auto wait_sm = [&](uint64_t* bar, uint32_t par) {
+    if (flags & 1) mbar_wait(bar, par); else mbar_wait_spin(bar, par);
+  };
+  auto wait_mma = [&](uint64_t* bar, uint32_t par) {
+    if (flags & 2) mbar_wait(bar, par); else mbar_wait_spin(bar, par);
+  };
+  constexpr int HD = C::HD;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* kfull = bars + 1;           // [KST]
+  uint64_t* kempty = kfull + C::KST;    // [KST]
+  uint64_t* vfull = kempty + C::KST;    // [VST]
+  uint64_t* vempty = vfull + C::VST;    // [VST]
+  uint64_t* sfull = vempty + C::VST;    // [2] S_j in buffer j & 1
+  uint64_t* pfull = sfull + 2;          // [2] P_j in buffer j & 1 (leader: 8 warp arrivals)
+  uint64_t* pvdone = pfull + 2;         // [2] PV_j (reads P buffer j & 1) completed
+  uint64_t* sfree = pvdone + 2;         // [2] softmax loaded S_j (leader: 16 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
+  float* red = reinterpret_cast<float*>(smem + C::RED_OFF);  // [tile parity][half][128 rows]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int head = blockIdx.y;
+  const uint32_t rank = cluster_ctarank();  // 0 = leader (issues the MMAs)
+
+  const int blk = blockIdx.x >> 1;
+  int r = 0;
+  while (r + 1 < tab.nreq && blk >= tab.tile_start[r + 1]) ++r;
+  const int pair = blk - tab.tile_start[r];
+  const int kv_off = tab.kv_off[r], kv_len = tab.kv_len[r];
+  const int q_row0 = tab.q_off[r] + pair * 256 + rank * 128;
+  const int q_rows = min(128, tab.q_len[r] - pair * 256 - static_cast<int>(rank) * 128);  // may be <= 0
+  const int nkv = (kv_len + 127) / 128;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 2);
+    for (int s = 0; s < C::KST; ++s) {
+      mbar_init(&kfull[s], 2);
+      mbar_init(&kempty[s], 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
+      mbar_init(&vfull[s], 2);
+      mbar_init(&vempty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sfull[b], 1);
+      mbar_init(&pfull[b], 16);
+      mbar_init(&pvdone[b], 1);
+      mbar_init(&sfree[b], 16);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kProducerWarp1 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+  }
+  if (warp == kMmaWarp1) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers initialised before any remote arrive / 2-SM TMA
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kProducerWarp1) {
+    if (lane == 0) {
+      auto arrive_tx = [&](uint64_t* bar, uint32_t bytes) {
+        mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(bar), 0), bytes);
+      };
+      arrive_tx(q_full, C::TILE_BYTES);
+      for (int b = 0; b < 2; ++b)
+        tma_load_3d_2sm(&tmQ, q_full, smem + C::Q_OFF + b * 16384, b * 64, head, q_row0);
+      for (int j = 0; j < nkv; ++j) {
+        const int ks = j % C::KST, vs = j % C::VST;
+        mbar_wait(&kempty[ks], ((j / C::KST) & 1) ^ 1);
+        uint8_t* sk = smem + C::K_OFF + ks * C::KT_BYTES;
+        arrive_tx(&kfull[ks], C::KT_BYTES);
+        for (int b = 0; b < 2; ++b)  // keys [64 rank, 64 rank + 64) of the tile
+          tma_load_3d_2sm(&tmK, &kfull[ks], sk + b * C::KBOX_BYTES, b * 64, head, kv_off + j * 128 + 64 * rank);
+        mbar_wait(&vempty[vs], ((j / C::VST) & 1) ^ 1);
+        arrive_tx(&vfull[vs], C::VT_BYTES);  // d columns [64 rank, 64 rank + 64) of all 128 keys
+        tma_load_3d_2sm(&tmV, &vfull[vs], smem + C::V_OFF + vs * C::VT_BYTES, 64 * rank, head, kv_off + j * 128);
+      }
+    }
+  } else if (warp == kMmaWarp1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16(256, 128, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16(256, HD, 0, 1);
+      const uint64_t qdesc0 = sdesc_sw128(smem_u32(smem + C::Q_OFF), 16, 1024);
+      const uint64_t kdesc0 = sdesc_sw128(smem_u32(smem + C::K_OFF), 16, 1024);
+      const uint64_t vdesc0 = sdesc_sw128(smem_u32(smem + C::V_OFF), 16384, 1024);
+      auto issue_s = [&](int j) {  // S_j = Q K_j^T -> S buffer j & 1
+        TRACE_EV(0, 0, j);
+        const uint64_t kb = kdesc0 + (((j % C::KST) * C::KT_BYTES) >> 4);
+        const uint32_t d = tmem + C::T_S + (j & 1) * 128;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t qoff = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+          const uint32_t koff = ((kk >> 2) * C::KBOX_BYTES + (kk & 3) * 32) >> 4;
+          mma_ss_2sm(d, qdesc0 + qoff, kb + koff, idesc_s, kk > 0);
+        }
+        mma_commit_2sm_mc(&kempty[j % C::KST], 0x3);
+      };
+      auto issue_pv = [&](int j) {  // O += P_j V_j, P_j read from TMEM buffer j & 1
+        TRACE_EV(1, 0, j);
+        const uint64_t vb = vdesc0 + (((j % C::VST) * C::VT_BYTES) >> 4);
+        const uint32_t pa = tmem + C::T_P + (j & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts_2sm(tmem + C::T_O, pa + kk * 8, vb + ((kk * 2048) >> 4), idesc_o, (j > 0) || (kk > 0));
+        mma_commit_2sm_mc(&pvdone[j & 1], 0x3);
+        mma_commit_2sm_mc(&vempty[j % C::VST], 0x3);
+      };
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < 2 && j < nkv; ++j) {
+        wait_mma(&kfull[j % C::KST], (j / C::KST) & 1);
+        tc_fence_after();
+        issue_s(j);
+        mma_commit_2sm_mc(&sfull[j], 0x3);
+      }
+      const bool early_s = flags & 4;  // A/B: S_{j+2} issued before PV_j (after sfree) vs after it
+      if (nkv > 0) wait_mma(&vfull[0], 0);
+      for (int j = 0; j < nkv; ++j) {
+        const bool more = j + 2 < nkv;
+        if (more && early_s) {  // S_{j+2} into S_j's buffer as soon as the softmax has loaded S_j
+          wait_mma(&sfree[j & 1], (j >> 1) & 1);
+          wait_mma(&kfull[(j + 2) % C::KST], ((j + 2) / C::KST) & 1);
+          tc_fence_after();
+          issue_s(j + 2);
+        }
+        // V_j was checked at the end of the previous iteration: P_j is the only wait on the path
+        // from the softmax's hand-off to PV_j
+        if (flags & 8)
+          mbar_wait(&pfull[j & 1], (j >> 1) & 1);
+        else
+          mbar_wait_spin(&pfull[j & 1], (j >> 1) & 1);
+        TRACE_EV(10, 0, j);
+        tc_fence_after();
+        issue_pv(j);
+        if (more && !early_s) {  // S_j's buffer is free: P_j's arrival follows the softmax's load of S_j
+          wait_mma(&kfull[(j + 2) % C::KST], ((j + 2) / C::KST) & 1);
+          tc_fence_after();
+          issue_s(j + 2);
+        }
+        // S_{j+2}'s completion is signalled only after PV_j is issued: the commit tracks both, so
+        // the softmax's wait for S_{j+2} also guarantees P buffer j & 1 is free again.
+        if (more) mma_commit_2sm_mc(&sfull[j & 1], 0x3);
+        if (j + 1 < nkv) wait_mma(&vfull[(j + 1) % C::VST], ((j + 1) / C::VST) & 1);
+      }
+    }
+  } else if (warp < 8) {
+    const int quarter = warp & 3, half = warp >> 2;  // lane quarter, column half
+    const int row_in = quarter * 32 + lane;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
+    const uint32_t tO = tmem + lane_base + C::T_O + half * (HD / 2);
+    const float2 sc2 = make_float2(scale_log2, scale_log2);
+    const uint32_t pfull_leader = mapa_shared(smem_u32(&pfull[0]), 0);
+    const uint32_t sfree_leader = mapa_shared(smem_u32(&sfree[0]), 0);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      const int b = j & 1;
+      const uint32_t tS = tmem + lane_base + C::T_S + b * 128 + half * 64;
+      const uint32_t tP = tmem + lane_base + C::T_P + b * 64 + half * 32;
+      wait_sm(&sfull[b], (j >> 1) & 1);
+      tc_fence_after();
+      if (warp == 0 && lane == 0) TRACE_EV(2, 0, j);
+      const int kv_valid = min(128, kv_len - j * 128);
+      uint32_t v[64];
+      GS_TMEM_LD32(tS + 0, (*reinterpret_cast<uint32_t(*)[32]>(v + 0)));
+      GS_TMEM_LD32(tS + 32, (*reinterpret_cast<uint32_t(*)[32]>(v + 32)));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(sfree_leader + b * 8);  // S buffer b may be overwritten
+      if (warp == 0 && lane == 0) TRACE_EV(3, 0, j);
+      const bool full = kv_valid == 128;
+      if (!full) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (half * 64 + i >= kv_valid) v[i] = __float_as_uint(-INFINITY);
+      }
+      // partial row max over this half: 4 independent FMNMX3 chains
+      float mx[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mx[c] = fmax3(__uint_as_float(v[16 * c]), __uint_as_float(v[16 * c + 1]),
+                                                __uint_as_float(v[16 * c + 2]));
+#pragma unroll
+      for (int i = 3; i < 15; i += 2)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          mx[c] = fmax3(mx[c], __uint_as_float(v[16 * c + i]), __uint_as_float(v[16 * c + i + 1]));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) mx[c] = fmaxf(mx[c], __uint_as_float(v[16 * c + 15]));
+      const float m_half = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      if (warp == 0 && lane == 0) TRACE_EV(11, 0, j);
+      // exchange with the other half's warp (double-buffered by tile parity: the partner cannot
+      // reach tile j + 2's write before passing tile j + 1's barrier, i.e. after reading tile j)
+      red[(b * 2 + half) * 128 + row_in] = m_half;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+      const float m_tile = fmaxf(m_half, red[(b * 2 + (half ^ 1)) * 128 + row_in]) * scale_log2;
+      if (warp == 0 && lane == 0) TRACE_EV(12, 0, j);
+      const bool need = m_tile > m_run + 8.0f;
+      const float alpha = need ? ex2_approx(m_run - m_tile) : 1.0f;
+      if (need) m_run = m_tile;
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        mbar_wait(&pvdone[(j - 1) & 1], ((j - 1) >> 1) & 1);  // O holds PV_0..PV_{j-1}
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < HD / 64; ++c) {
+          uint32_t o[32];
+          GS_TMEM_LD32(tO + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          GS_TMEM_ST32(tO + c * 32, o);
+        }
+      }
+      l_run *= alpha;
+      // P buffer b was last read by PV_{j-2}, which is complete: S_j's completion is committed
+      // after PV_{j-2} is issued and a commit tracks all of the issuing thread's earlier MMAs (an
+      // explicit wait on pv_done here measured ~290 cycles per tile under MUFU / MIO load).
+      if (warp == 0 && lane == 0) TRACE_EV(13, 0, j);
+      float2 acc;
+      if (full)
+        acc = exp_pack_store<POLY8, true, 64>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tP, half * 64);
+      else
+        acc = exp_pack_store<POLY8, false, 64>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tP, half * 64);
+      l_run += acc.x + acc.y;
+      if (warp == 0 && lane == 0) TRACE_EV(14, 0, j);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (TRACE && lane == 0 && half == 0 && blockIdx.x < 2 && blockIdx.y == 0 && j < 32)
+        g_attn_trace[blockIdx.x * 1024 + ((4 + quarter) * 32 + j) * 2] = clock64();
+      if (lane == 0) mbar_arrive_cluster(pfull_leader + b * 8);
+    }
+    // row sum = both halves' partial sums (exchange slot of parity nkv & 1 is free: see above)
+    const int bf = nkv & 1;
+    red[(bf * 2 + half) * 128 + row_in] = l_run;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    l_run += red[(bf * 2 + (half ^ 1)) * 128 + row_in];
+    // epilogue: O / l -> bf16 -> global, after the last PV (commits track all earlier MMAs)
+    if (nkv > 0) mbar_wait(&pvdone[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv = 1.0f / l_run;
+    __nv_bfloat16* orow = O + static_cast<long long>(q_row0 + row_in) * o_rs + head * HD + half * (HD / 2);
+#pragma unroll
+    for (int c = 0; c < HD / 64; ++c) {
+      uint32_t v[32];
+      GS_TMEM_LD32(tO + c * 32, v);
+      tmem_ld_wait();
+      if (row_in < q_rows) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
+        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  cluster_sync();  // the peer may still arrive on our barriers / read our TMEM until here
+  if (warp == kMmaWarp1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem, 512);
+  }
+}
+
+// Kernel version for d = 128: 5 (default, attn_tc_kernel) or 6 (attn_db_kernel, GS_ATTN_V=6).
+// v6 measured slower (1050-1130 vs 1360-1380 TFLOP/s at the c4 sp8 shape, profiles/r01_notes.md):
+// its two softmax warps per lane quarter run in lock-step, so the MUFU pipe idles through the
+// max / exchange / barrier phases that v5's two Q-tile groups overlap.
+int attn_version() {
+  static int v = [] {
+    const char* e = getenv("GS_ATTN_V");
+    return e ? atoi(e) : 5;
+  }();
+  return v;
+}
+
+template <int POLY8>
+cudaError_t launch_db(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs, int kv_rs, int o_rs,
+                      const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
+  using C = Cfg1;
+  CUtensorMap tq, tk, tv;
+  if (!make_tma_3d_bf16(&tq, Q, 128, heads, q_rows, 256ull, q_rs * 2ull, 64, 1, 128) ||
+      !make_tma_3d_bf16(&tk, K, 128, heads, kv_rows, 256ull, kv_rs * 2ull, 64, 1, 64) ||
+      !make_tma_3d_bf16(&tv, V, 128, heads, kv_rows, 256ull, kv_rs * 2ull, 64, 1, 128))
+    return cudaErrorInvalidValue;
+  static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
+  auto kern = trace ? attn_db_kernel<POLY8, true> : attn_db_kernel<POLY8, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  if (e != cudaSuccess) return e;
+  const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(128.0));
+  dim3 grid(tab.tile_start[tab.nreq] * 2, heads);
+  if (grid.x == 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(THREADS1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  static const int flags = [] {
+    const char* e = getenv("GS_ATTN_FLAGS");
+    return e ? atoi(e) : 0;
+  }();
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2, flags);
+}
+
 template <int HD, int POLY8>
 cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
                    int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
   constexpr bool PAIR = HD == 128;
+  if (HD == 128 && attn_version() >= 6)
+    return launch_db<POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
   using C = Cfg<HD, PAIR>;
   CUtensorMap tq, tk, tv;
   if (!make_tma_3d_bf16(&tq, Q, HD, heads, q_rows, HD * 2ull, q_rs * 2ull, 64, 1, 128) ||
@@ -493,7 +858,8 @@ cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, v
   tab.nreq = nreq;
   int q_rows = 1, kv_rows = 1;
   tab.tile_start[0] = 0;
-  const int rows_per_block = d == 128 ? 512 : 256;  // a CTA pair (d = 128) or a CTA (d = 64)
+  // a CTA pair (d = 128: 256 rows in v6, 512 in v3-v5) or a CTA (d = 64)
+  const int rows_per_block = d == 128 ? (attn_version() >= 6 ? 256 : 512) : 256;
   for (int r = 0; r < nreq; ++r) {
     if (q_len[r] < 0 || kv_len[r] < 1) return cudaErrorInvalidValue;
     tab.q_off[r] = q_off[r];
