@@ -85,6 +85,13 @@ int gs_init(int device, int world_size, int rank, const void* nccl_uid, gs_ctx**
 int gs_init_emulated(int device, int world_size, gs_ctx** out);
 void gs_destroy(gs_ctx* ctx);
 const char* gs_last_error(gs_ctx* ctx);
+/* Runtime options.  "a2a": 1 (default) = fused all-to-alls by peer stores wherever the SP degree
+ * divides the heads (the QKV pack kernel and the attention epilogue store straight into the
+ * consuming GPU's buffers over NVLink -- CUDA IPC mappings exchanged over NCCL at gs_run_steps
+ * -- ordered by a flag barrier), 0 = transfer plans (grouped ncclSend/Recv, or
+ * device copies in emulated mode).  Both give bit-identical results.  Every process of an SP
+ * group must use the same setting.  GS_EINVAL for an unknown key or value. */
+int gs_set_option(gs_ctx* ctx, const char* key, long long value);
 /* Number of SMs of the context's device, world size, ranks owned by this process. */
 int gs_info(gs_ctx* ctx, int* num_sms, int* world_size, int* nlocal);
 
@@ -139,7 +146,8 @@ int gs_release(gs_ctx* ctx, gs_req req);
 /* ------------------------------------------------------------------ measurement */
 /* Enable per-kernel-class CUDA-event timing inside gs_run_steps (events on the launching
  * stream); gs_stats writes a JSON object {"class": {"ms": total, "n": launches}, ...,
- * "launches": total kernel launches} accumulated since the last reset. */
+ * "a2a_peer": exchanges run as peer stores, "a2a_plan": exchanges run as transfer plans,
+ * "launches": total kernel launches} accumulated since the last reset (a2a counts: since init). */
 int gs_profile(gs_ctx* ctx, int enable, int reset);
 int gs_stats(gs_ctx* ctx, char* json, size_t len);
 /* The CUDA stream (cudaStream_t) the context launches rank `rank`'s work on, as a pointer. */
@@ -180,6 +188,15 @@ typedef struct {
  * too small or an argument is out of range. */
 int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
                 gs_xfer* out, int max_out, int* n_out, long long* stage_elems);
+/* Peer-store addressing of the fused all-to-alls (p divides heads; DESIGN.md §8 "fused exchange"):
+ * the QKV pack kernel of SP position `me` stores local row m of request r as full-batch row
+ * m + row_delta[r] of the RECV buffer of the position owning each head, and its attention kernel
+ * stores the output row of token t of request r into the owner i = max{i : own_lo[r*p+i] <= t} at
+ * element o_base[r*p+i] + t*heads*head_dim + (h - me*heads/p)*head_dim of that owner's ORECV
+ * buffer [rows_i][heads*head_dim].  Outputs: row_delta [nreq], own_lo [nreq*p], o_base [nreq*p].
+ * GS_EUNSUPPORTED when p does not divide heads (those batches use the gs_plan_a2a transfers). */
+int gs_plan_peer(int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
+                 long long* row_delta, int* own_lo, long long* o_base);
 /* Re-shard of a request's latent [n_tokens, lat] from old_ranks (old_p) to new_ranks (new_p), as
  * seen by global rank `me` (which may be in either set, both or none). */
 int gs_plan_reshard(int n_tokens, int lat, const int* old_ranks, int old_p, const int* new_ranks,

@@ -77,6 +77,9 @@ _SIG = {
     "gs_plan_a2a": [_I, _I, _I, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP,
                     ctypes.POINTER(ctypes.c_longlong)],
     "gs_plan_reshard": [_I, _I, _IP, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP],
+    "gs_plan_peer": [_I, _I, _I, _IP, _I, _I, ctypes.POINTER(ctypes.c_longlong), _IP,
+                     ctypes.POINTER(ctypes.c_longlong)],
+    "gs_set_option": [_P, ctypes.c_char_p, ctypes.c_longlong],
 }
 _lib = None
 
@@ -153,6 +156,22 @@ def plan_reshard(n_tokens, lat, old_ranks, new_ranks, me):
                                                          len(new_ranks), me, out, mx, n))
 
 
+def plan_peer(p, me, n_tokens, heads, head_dim):
+    """Peer-store addressing of the fused all-to-alls for SP position `me` (include/gs.h
+    gs_plan_peer): (row_delta [nreq], own_lo [nreq, p], o_base [nreq, p]); raises GsError
+    (GS_EUNSUPPORTED) when p does not divide heads."""
+    lib = load()
+    B = len(n_tokens)
+    rd = (ctypes.c_longlong * B)()
+    ol = (ctypes.c_int * (B * p))()
+    ob = (ctypes.c_longlong * (B * p))()
+    rc = lib.gs_plan_peer(p, me, B, _ints(n_tokens), heads, head_dim, rd, ol, ob)
+    if rc != GS_OK:
+        raise GsError(rc, "gs_plan_peer rejected its arguments")
+    return (np.array(rd[:], dtype=np.int64), np.array(ol[:], dtype=np.int64).reshape(B, p),
+            np.array(ob[:], dtype=np.int64).reshape(B, p))
+
+
 class Context:
     """One process-side context: a CUDA device and its ranks (see include/gs.h)."""
 
@@ -187,6 +206,10 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def set_option(self, key, value):
+        """Runtime option (include/gs.h gs_set_option), e.g. ("a2a", 0 | 1)."""
+        self._ck(self._lib.gs_set_option(self._h, key.encode(), int(value)))
 
     def info(self):
         a, b, c = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()

@@ -123,7 +123,8 @@ template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128)>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
-                   const __grid_constant__ SeqTable tab, float scale_log2) {
+                   const __grid_constant__ SeqTable tab, float scale_log2,
+                   const __grid_constant__ OScatter osc) {
   using C = Cfg<HD, PAIR>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -401,7 +402,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     const int row_in = w * 128 + quarter * 32 + lane;
     const float inv = 1.0f / l_run;
-    __nv_bfloat16* orow = O + static_cast<long long>(q_row0 + row_in) * o_rs + head * HD;
+    __nv_bfloat16* orow;
+    if (osc.nown > 0) {  // fused head->seq exchange: straight into the token owner's O-proj input
+      const int t = q_row0 + row_in - tab.q_off[r];
+      int i = 0;
+#pragma unroll
+      for (int k = 1; k < 8; ++k)
+        if (k < osc.nown && t >= osc.lo[r][k]) i = k;
+      orow = osc.base[r][i] + static_cast<long long>(t) * o_rs + head * HD;
+    } else {
+      orow = O + static_cast<long long>(q_row0 + row_in) * o_rs + head * HD;
+    }
 #pragma unroll
     for (int c = 0; c < HD / 32; ++c) {
       uint32_t v[32];
@@ -795,9 +806,10 @@ cudaError_t launch_db(const void* Q, const void* K, const void* V, void* O, int 
 
 template <int HD, int POLY8>
 cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
-                   int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
+                   int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream,
+                   const OScatter& osc) {
   constexpr bool PAIR = HD == 128;
-  if (HD == 128 && attn_version() >= 6)
+  if (HD == 128 && attn_version() >= 6 && osc.nown == 0)
     return launch_db<POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
   using C = Cfg<HD, PAIR>;
   CUtensorMap tq, tk, tv;
@@ -824,7 +836,7 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
   attr.val.clusterDim.z = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2);
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2, osc);
 }
 
 // Fraction of exp2 pairs (in eighths) computed by the FMA-pipe polynomial.  Default from the
@@ -840,20 +852,27 @@ int poly8_setting() {
 
 template <int HD>
 cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
-                   int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
+                   int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream,
+                   const OScatter& osc) {
   switch (poly8_setting()) {
-    case 2: return launch_t<HD, 2>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
-    case 4: return launch_t<HD, 4>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
-    case 3: return launch_t<HD, 3>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
-    default: return launch_t<HD, 0>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
+    case 2: return launch_t<HD, 2>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
+    case 4: return launch_t<HD, 4>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
+    case 3: return launch_t<HD, 3>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
+    default: return launch_t<HD, 0>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
   }
 }
 }  // namespace
 
 cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                                   int q_rs, int kv_rs, int o_rs, const int* q_off, const int* q_len,
-                                  const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream) {
+                                  const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream,
+                                  const OScatter* scatter) {
   if (nreq < 1 || nreq > MAX_REQ || (d != 64 && d != 128) || heads < 1) return cudaErrorInvalidValue;
+  OScatter osc{};
+  if (scatter && scatter->nown > 0) {
+    if (nreq > OSC_MAX_REQ || scatter->nown > 8) return cudaErrorInvalidValue;
+    osc = *scatter;
+  }
   SeqTable tab{};
   tab.nreq = nreq;
   int q_rows = 1, kv_rows = 1;
@@ -870,18 +889,18 @@ cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, v
     q_rows = std::max(q_rows, q_off[r] + q_len[r]);
     kv_rows = std::max(kv_rows, kv_off[r] + kv_len[r]);
   }
-  return d == 128 ? launch<128>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream)
-                  : launch<64>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
+  return d == 128 ? launch<128>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc)
+                  : launch<64>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
 }
 
 cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                          int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
-                         int nreq, int num_sms, cudaStream_t stream) {
+                         int nreq, int num_sms, cudaStream_t stream, const OScatter* scatter) {
   (void)num_sms;
   for (int r = 0; r < nreq; ++r)
     if (seq_len[r] < 1) return cudaErrorInvalidValue;
   return attention_tc_segments(Q, K, V, O, heads, d, q_rs, kv_rs, o_rs, seq_off, seq_len, seq_off, seq_len, nreq,
-                               stream);
+                               stream, scatter);
 }
 
 }  // namespace gs

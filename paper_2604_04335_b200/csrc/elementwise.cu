@@ -139,17 +139,29 @@ __global__ void __launch_bounds__(ROW_THREADS)
     if (c < nv) {
       const int e0 = c * 8;
       const int h = e0 / d, i0 = e0 - h * d;
-      int h0 = pk.head_off[0], h1 = pk.head_off[1];
-      long long doff = pk.dest_off[0];
+      int h0 = pk.head_off[0], h1 = pk.head_off[1], jc = 0;
 #pragma unroll
       for (int t = 1; t < 16; ++t) {
         if (t < pk.ndest && h >= pk.head_off[t]) {
           h0 = pk.head_off[t];
           h1 = pk.head_off[t + 1];
-          doff = pk.dest_off[t];
+          jc = t;
         }
       }
-      const long long o = doff + (row * (h1 - h0) + (h - h0)) * (long long)d + i0;
+      __nv_bfloat16 *dq = q_out, *dk = k_out, *dv = v_out;
+      long long o;
+      if (pk.peer) {  // straight into the destination's RECV buffer (full-batch row)
+        int sq = 0;
+#pragma unroll
+        for (int t = 1; t < 16; ++t)
+          if (t < pk.nseq && row >= pk.seq_lo[t]) sq = t;
+        dq = pk.dst_q[jc];
+        dk = pk.dst_k[jc];
+        dv = pk.dst_v[jc];
+        o = ((row + pk.row_delta[sq]) * (h1 - h0) + (h - h0)) * (long long)d + i0;
+      } else {
+        o = pk.dest_off[jc] + (row * (h1 - h0) + (h - h0)) * (long long)d + i0;
+      }
       float fq[8], fk[8], wq[8], wk[8];
       unpack8(qv[i], fq);
       unpack8(kv[i], fk);
@@ -167,9 +179,9 @@ __global__ void __launch_bounds__(ROW_THREADS)
         oq[p] = pack_bf16x2(q0 * cs.x - q1 * cs.y, q0 * cs.y + q1 * cs.x);
         ok[p] = pack_bf16x2(k0 * cs.x - k1 * cs.y, k0 * cs.y + k1 * cs.x);
       }
-      *reinterpret_cast<uint4*>(q_out + o) = make_uint4(oq[0], oq[1], oq[2], oq[3]);
-      *reinterpret_cast<uint4*>(k_out + o) = make_uint4(ok[0], ok[1], ok[2], ok[3]);
-      *reinterpret_cast<uint4*>(v_out + o) = src[2 * nv + c];
+      *reinterpret_cast<uint4*>(dq + o) = make_uint4(oq[0], oq[1], oq[2], oq[3]);
+      *reinterpret_cast<uint4*>(dk + o) = make_uint4(ok[0], ok[1], ok[2], ok[3]);
+      *reinterpret_cast<uint4*>(dv + o) = src[2 * nv + c];
     }
   }
 }
@@ -316,6 +328,47 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
     return cudaErrorInvalidValue;
   qk_norm_rope_pack_kernel<<<M, ROW_THREADS, 0, stream>>>(qkv, D, d, g_q, g_k, eps, rp, pk, q_out,
                                                            k_out, v_out);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ peer barrier
+__global__ void peer_signal_kernel(const PeerFlags f) {
+  const int t = threadIdx.x;
+  if (t < f.n) {
+    // order every store this device made before (the producing kernels, earlier on the stream)
+    // ahead of the flag at system scope, then publish the flag with release semantics
+    asm volatile("fence.sc.sys;" ::: "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f.slot[t]), "l"(f.val[t]) : "memory");
+  }
+}
+
+__global__ void peer_wait_kernel(const PeerFlags f) {
+  const int t = threadIdx.x;
+  if (t < f.n) {
+    unsigned long long v = 0;
+    const long long t0 = clock64();
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f.slot[t]) : "memory");
+      if (v >= f.val[t]) break;
+      if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s at 2 GHz: a peer died / mismatched plan
+      __nanosleep(64);
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+cudaError_t peer_signal(const PeerFlags& f, cudaStream_t stream) {
+  if (f.n < 0 || f.n > 8) return cudaErrorInvalidValue;
+  if (f.n == 0) return cudaSuccess;
+  peer_signal_kernel<<<1, 32, 0, stream>>>(f);
+  return cudaGetLastError();
+}
+
+cudaError_t peer_wait(const PeerFlags& f, cudaStream_t stream) {
+  if (f.n < 0 || f.n > 8) return cudaErrorInvalidValue;
+  if (f.n == 0) return cudaSuccess;
+  peer_wait_kernel<<<1, 32, 0, stream>>>(f);
   return cudaGetLastError();
 }
 

@@ -322,6 +322,11 @@ struct Plan : A2aGeometry {
   std::vector<Request*> ureqs;   // the batch's requests
   std::vector<int> ranks;
   bool text = false;
+  // fused exchange (peer stores): per position its RECV / ORECV buffers and barrier flag words,
+  // addressed from this process (local arenas, or CUDA IPC mappings of the peers' buffers)
+  bool peer = false;
+  std::vector<bf16*> qr_of, kr_of, vr_of, orecv_of;
+  std::vector<unsigned long long*> flags_of;
 };
 
 void make_plan(Plan& P, Model* m, const std::vector<Request*>& ureqs, const int* ranks, int p) {
@@ -465,6 +470,7 @@ int run_emulated(gs_ctx* c, const std::vector<std::vector<gs_xfer>>& plans, BufF
 // seq -> head: Q/K/V chunk j of position i (rows of i, heads of j) -> recv buffers of j.
 int exchange_qkv(gs_ctx* c, const Plan& P) {
   Scope sc(c, "a2a_qkv", 0);
+  ++c->a2a_plan;
   // t = 0: Q (plan_q), t = 1, 2: K, V (plan_kv); they differ only for partial-head units
   if (c->emulated) {
     std::vector<std::vector<gs_xfer>> qplans(P.p), kvplans(P.p);
@@ -507,6 +513,7 @@ int exchange_qkv(gs_ctx* c, const Plan& P) {
 // head -> seq: attention output of position j (all rows, heads of j) -> rows' owners.
 int exchange_o(gs_ctx* c, const Plan& P) {
   Scope sc(c, "a2a_o", 0);
+  ++c->a2a_plan;
   auto arena_buf = [&](RankArena& A, int id) -> void* {
     return id == GS_BUF_O ? A.o.p : id == GS_BUF_STAGE ? A.ostage.p : A.orecv.p;
   };
@@ -534,6 +541,137 @@ int exchange_o(gs_ctx* c, const Plan& P) {
     if (x.op == GS_XFER_COPY)
       RET(copy_block(c, static_cast<bf16*>(arena_buf(A, x.dst_buf)) + x.dst_off,
                      static_cast<bf16*>(arena_buf(A, x.src_buf)) + x.src_off, x, 2));
+  return GS_OK;
+}
+
+// ------------------------------------------------------------------ fused exchange (peer stores)
+// The QKV pack kernel stores each head chunk straight into the RECV buffer of the position that
+// attends over it, and the attention kernel stores each output row straight into the O-proj input
+// (ORECV) of the token's owner: no send / stage buffers, no unpack copies, no NCCL kernels, and the
+// NVLink traffic overlaps the producing kernels.  Between producer and consumer a flag barrier
+// (peer_signal / peer_wait kernels, system-scope release / acquire) orders the stores; two per
+// block (after the pack, after attention) also make every buffer reuse safe: a position writes a
+// peer's RECV (ORECV) of layer l + 1 only after that peer passed the barrier that follows its own
+// reads of layer l.  Requires p | H (full heads only); other batches use the transfer plans.
+struct IpcExport {
+  cudaIpcMemHandle_t h[5];
+  int ok;
+};
+
+int peer_setup(gs_ctx* c, Plan& P) {
+  P.peer = false;
+  if (c->a2a_mode != 1 || P.p == 1 || P.R != 0 || P.B > OSC_MAX_REQ || c->world > 8) return GS_OK;
+  P.qr_of.assign(P.p, nullptr);
+  P.kr_of.assign(P.p, nullptr);
+  P.vr_of.assign(P.p, nullptr);
+  P.orecv_of.assign(P.p, nullptr);
+  P.flags_of.assign(P.p, nullptr);
+  if (!c->flags) {
+    const size_t words = static_cast<size_t>(c->emulated ? c->world : 1) * 8;
+    CK(cudaMalloc(&c->flags, words * 8));
+    CK(cudaMemset(c->flags, 0, words * 8));
+  }
+  if (c->emulated) {
+    for (int j = 0; j < P.p; ++j) {
+      RankArena& A = c->local[P.ranks[j]];
+      P.qr_of[j] = A.qr.as<bf16>();
+      P.kr_of[j] = A.kr.as<bf16>();
+      P.vr_of[j] = A.vr.as<bf16>();
+      P.orecv_of[j] = A.orecv.as<bf16>();
+      P.flags_of[j] = c->flags + static_cast<size_t>(P.ranks[j]) * 8;
+    }
+    P.peer = true;
+    return GS_OK;
+  }
+  // NCCL mode: exchange CUDA IPC handles of the four buffers and the flag words with the plan's
+  // peers (re-opened only when a peer re-allocated), then agree that every position mapped all
+  // of them before any kernel stores into peer memory.
+  const int me = my_position(c, P);
+  RankArena& A = c->local[0];
+  IpcExport mine{};
+  void* bases[5] = {A.qr.p, A.kr.p, A.vr.p, A.orecv.p, c->flags};
+  for (int b = 0; b < 5; ++b) CK(cudaIpcGetMemHandle(&mine.h[b], bases[b]));
+  mine.ok = 1;
+  if (!c->ipc_dev) CK(cudaMalloc(&c->ipc_dev, 9 * sizeof(IpcExport)));
+  IpcExport* dev = static_cast<IpcExport*>(c->ipc_dev);
+  auto exchange = [&](IpcExport* host_all) -> int {
+    CK(cudaMemcpyAsync(dev + me, host_all + me, sizeof(IpcExport), cudaMemcpyHostToDevice, c->stream));
+    NK(ncclGroupStart());
+    for (int j = 0; j < P.p; ++j) {
+      if (j == me) continue;
+      NK(ncclSend(dev + me, sizeof(IpcExport), ncclUint8, P.ranks[j], c->comm, c->stream));
+      NK(ncclRecv(dev + j, sizeof(IpcExport), ncclUint8, P.ranks[j], c->comm, c->stream));
+    }
+    NK(ncclGroupEnd());
+    CK(cudaMemcpyAsync(host_all, dev, P.p * sizeof(IpcExport), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return GS_OK;
+  };
+  std::vector<IpcExport> all(P.p);
+  all[me] = mine;
+  RET(exchange(all.data()));
+  int ok = 1;
+  for (int j = 0; j < P.p && ok; ++j) {
+    if (j == me) continue;
+    gs_ctx::PeerMap& pm = c->peers[P.ranks[j]];
+    for (int b = 0; b < 5 && ok; ++b) {
+      if (pm.p[b] && memcmp(&pm.h[b], &all[j].h[b], sizeof(cudaIpcMemHandle_t)) == 0) continue;
+      if (pm.p[b]) cudaIpcCloseMemHandle(pm.p[b]);
+      pm.p[b] = nullptr;
+      if (cudaIpcOpenMemHandle(&pm.p[b], all[j].h[b], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        pm.p[b] = nullptr;
+        ok = 0;
+      } else {
+        pm.h[b] = all[j].h[b];
+      }
+    }
+  }
+  // second round: peer stores only if every position mapped every peer (else all use the plans)
+  std::vector<IpcExport> agree(P.p);
+  agree[me].ok = ok;
+  RET(exchange(agree.data()));
+  for (int j = 0; j < P.p; ++j) ok &= agree[j].ok;
+  if (!ok) return GS_OK;
+  for (int j = 0; j < P.p; ++j) {
+    void* const* p = j == me ? bases : c->peers[P.ranks[j]].p;
+    P.qr_of[j] = static_cast<bf16*>(p[0]);
+    P.kr_of[j] = static_cast<bf16*>(p[1]);
+    P.vr_of[j] = static_cast<bf16*>(p[2]);
+    P.orecv_of[j] = static_cast<bf16*>(p[3]);
+    P.flags_of[j] = static_cast<unsigned long long*>(p[4]);
+  }
+  P.peer = true;
+  return GS_OK;
+}
+
+// Flag barrier over the plan's positions (the ones this process owns signal / wait; emulated mode
+// signals for every position before any waits, so one stream can carry all of them).  Position
+// i tells j "my stores into you are done" by raising word [rank i] of j's flags to the number of
+// barriers the pair (i, j) has passed.
+int peer_barrier(gs_ctx* c, const Plan& P, const std::vector<int>& mine) {
+  Scope sc(c, "a2a_peer_barrier", 2 * static_cast<int>(mine.size()));
+  for (int i : mine) {
+    PeerFlags f{};
+    for (int j = 0; j < P.p; ++j) {
+      if (j == i) continue;
+      f.slot[f.n] = P.flags_of[j] + P.ranks[i];
+      f.val[f.n] = ++c->sig_sent[P.ranks[i]][P.ranks[j]];
+      ++f.n;
+    }
+    CK(peer_signal(f, c->stream));
+  }
+  for (int j : mine) {
+    PeerFlags f{};
+    for (int i = 0; i < P.p; ++i) {
+      if (i == j) continue;
+      f.slot[f.n] = P.flags_of[j] + P.ranks[i];
+      f.val[f.n] = ++c->sig_seen[P.ranks[i]][P.ranks[j]];
+      ++f.n;
+    }
+    CK(peer_wait(f, c->stream));
+  }
+  ++c->a2a_peer;
   return GS_OK;
 }
 
@@ -574,6 +712,22 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
     pk.rows = M;
     for (int j = 0; j <= P.nchunks(); ++j) pk.head_off[j] = P.hoff[j];
     for (int j = 0; j < P.nchunks(); ++j) pk.dest_off[j] = static_cast<long long>(M) * P.hoff[j] * P.hd;
+    if (P.peer) {  // fused seq->head exchange: chunk j straight into position j's RECV buffers
+      std::vector<long long> rd, ob;
+      std::vector<int> ol;
+      if (!peer_tables(P, i, rd, ol, ob)) return fail(c, GS_ESTATE, "peer tables for a batch with p !| H");
+      pk.peer = 1;
+      for (int j = 0; j < P.p; ++j) {
+        pk.dst_q[j] = P.qr_of[j];
+        pk.dst_k[j] = P.kr_of[j];
+        pk.dst_v[j] = P.vr_of[j];
+      }
+      pk.nseq = P.B;
+      for (int r = 0; r < P.B; ++r) {
+        pk.row_delta[r] = rd[r];
+        pk.seq_lo[r] = P.loff[i][r];
+      }
+    }
     if (M) CK(qk_norm_rope_pack(A.qkv.as<bf16>(), M, D, P.H, w.g_q, w.g_k, eps, rp, pk, A.qs.as<bf16>(),
                                 A.ks.as<bf16>(), A.vs.as<bf16>(), c->stream));
   }
@@ -591,6 +745,22 @@ int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
     const int rs = P.H * P.hd;
     CK(attention_tc(A.qs.p, A.ks.p, A.vs.p, A.o.p, P.H, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
                     c->stream));
+    return GS_OK;
+  }
+  if (P.peer) {  // fused head->seq exchange: output rows straight into their owners' ORECV
+    std::vector<long long> rd, ob;
+    std::vector<int> ol;
+    if (!peer_tables(P, j, rd, ol, ob)) return fail(c, GS_ESTATE, "peer tables for a batch with p !| H");
+    OScatter osc{};
+    osc.nown = P.p;
+    for (int r = 0; r < P.B; ++r)
+      for (int i = 0; i < P.p; ++i) {
+        osc.lo[r][i] = ol[static_cast<size_t>(r) * P.p + i];
+        osc.base[r][i] = P.orecv_of[i] + ob[static_cast<size_t>(r) * P.p + i];
+      }
+    const int rs = P.Hf * P.hd;
+    CK(attention_tc(A.qr.p, A.kr.p, A.vr.p, nullptr, P.Hf, P.hd, rs, rs, P.D, so.data(), sl.data(), P.B,
+                    c->num_sms, c->stream, &osc));
     return GS_OK;
   }
   // full heads of this position
@@ -752,9 +922,9 @@ int run_one_step(gs_ctx* c, const Plan& P, const std::vector<int>& mine) {
   for (int i : mine) RET(step_prologue(c, P, i, c->local[local_index(c, P.ranks[i])], t));
   for (int l = 0; l < P.m->desc.layers; ++l) {
     for (int i : mine) RET(block_pre(c, P, i, c->local[local_index(c, P.ranks[i])], l));
-    if (P.p > 1) RET(exchange_qkv(c, P));
+    if (P.p > 1) RET(P.peer ? peer_barrier(c, P, mine) : exchange_qkv(c, P));
     for (int i : mine) RET(block_attn(c, P, i, c->local[local_index(c, P.ranks[i])]));
-    if (P.p > 1) RET(exchange_o(c, P));
+    if (P.p > 1) RET(P.peer ? peer_barrier(c, P, mine) : exchange_o(c, P));
     for (int i : mine) RET(block_post(c, P, i, c->local[local_index(c, P.ranks[i])], l));
   }
   for (int i : mine) RET(step_epilogue(c, P, i, c->local[local_index(c, P.ranks[i])], dsig));
@@ -957,6 +1127,11 @@ void gs_destroy(gs_ctx* c) {
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
   }
+  for (auto& pm : c->peers)
+    for (void* p : pm.p)
+      if (p) cudaIpcCloseMemHandle(p);
+  if (c->flags) cudaFree(c->flags);
+  if (c->ipc_dev) cudaFree(c->ipc_dev);
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->ev_order) cudaEventDestroy(c->ev_order);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -967,6 +1142,16 @@ void gs_destroy(gs_ctx* c) {
 }
 
 const char* gs_last_error(gs_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int gs_set_option(gs_ctx* c, const char* key, long long value) {
+  if (!c || !key) return GS_EINVAL;
+  if (strcmp(key, "a2a") == 0) {
+    if (value != 0 && value != 1) return fail(c, GS_EINVAL, "a2a option %lld (0 = transfer plans, 1 = peer stores)", value);
+    c->a2a_mode = static_cast<int>(value);
+    return GS_OK;
+  }
+  return fail(c, GS_EINVAL, "unknown option '%s'", key);
+}
 
 int gs_info(gs_ctx* c, int* num_sms, int* world_size, int* nlocal) {
   if (!c) return GS_EINVAL;
@@ -1172,6 +1357,7 @@ int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int n
     RET(prepare_rank(c, P, i, A));
     RET(move_latent(c, P, i, A, 0));
   }
+  RET(peer_setup(c, P));
   for (Request* q : reqs) q->state = GS_REQ_RUNNING;
   int done = 0, rc = GS_OK;
   for (int s = 0; s < k; ++s) {
@@ -1350,8 +1536,9 @@ int gs_stats(gs_ctx* c, char* json, size_t len) {
     snprintf(buf, sizeof buf, "\"%s\": {\"ms\": %.6f, \"n\": %lld}, ", kv.first.c_str(), kv.second.ms, kv.second.n);
     s += buf;
   }
-  char buf[64];
-  snprintf(buf, sizeof buf, "\"launches\": %lld}", c->launches);
+  char buf[160];
+  snprintf(buf, sizeof buf, "\"a2a_peer\": %lld, \"a2a_plan\": %lld, \"launches\": %lld}", c->a2a_peer,
+           c->a2a_plan, c->launches);
   s += buf;
   if (s.size() + 1 > len) return fail(c, GS_EINVAL, "stats buffer too small (%zu)", s.size() + 1);
   memcpy(json, s.c_str(), s.size() + 1);

@@ -38,14 +38,25 @@ cudaError_t gemm_bf16_tc(int epi, int M, int N, int K, const void* A, int lda, c
 // O[r, h, :] = softmax(Q_h K_h^T / sqrt(d)) V_h over each request's own rows (block-diagonal).
 // Q/K/V/O: bf16 [rows, heads, d] with row strides (elements) *_rs; seq_off/seq_len per request
 // (host arrays, nreq <= 64).
+// Output scatter (fused head->seq exchange): with nown > 0 the output row of token
+// t of segment r (t = row - seq_off[r]) is stored at base[r][i] + t * o_rs + head * d for the
+// owner i = max{i < nown : lo[r][i] <= t} (peer memory over NVLink, or a local buffer); O is
+// then unused.
+constexpr int OSC_MAX_REQ = 16;
+struct OScatter {
+  int nown;
+  int lo[OSC_MAX_REQ][8];
+  __nv_bfloat16* base[OSC_MAX_REQ][8];
+};
 cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                          int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
-                         int nreq, int num_sms, cudaStream_t stream);
+                         int nreq, int num_sms, cudaStream_t stream, const OScatter* scatter = nullptr);
 // General form: segment r's q_len[r] query rows (from q_off[r]) attend to its kv_len[r] key/value
 // rows (from kv_off[r]) -- text cross-attention uses a separate context K/V buffer.
 cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                                   int q_rs, int kv_rs, int o_rs, const int* q_off, const int* q_len,
-                                  const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream);
+                                  const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream,
+                                  const OScatter* scatter = nullptr);
 
 // ----------------------------------------------------------------- element-wise (elementwise.cu)
 // out[m, :] = LN(x[m, :]) * (1 + sc) + sh, sh = sh_a + sh_b[req(m)*b_stride], same for sc.
@@ -68,6 +79,18 @@ struct PackParams {
   int head_off[17];       // head_off[j]..head_off[j+1]: heads of chunk j
   long long dest_off[16]; // element offset of chunk j in each send buffer
   int rows;               // M (local rows; chunk j is [rows][H_j][d])
+  // peer-store mode (fused seq->head exchange): chunk j goes straight into the
+  // RECV buffers of the position holding it (peer memory over NVLink, or a local buffer), local
+  // row m of sequence s (the s with seq_lo[s] <= m: sequences are contiguous row segments; with
+  // CFG a request has two) as row m + row_delta[s] of [rows_full][H_j][d]; q_out / k_out / v_out
+  // and dest_off are then unused.
+  int peer;
+  int nseq;
+  int seq_lo[16];
+  __nv_bfloat16* dst_q[16];
+  __nv_bfloat16* dst_k[16];
+  __nv_bfloat16* dst_v[16];
+  long long row_delta[16];
 };
 cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,
@@ -92,6 +115,18 @@ cudaError_t rmsnorm_rows(const __nv_bfloat16* in, int ld_in, int M, int D, const
 // z2 (optional) receives the same updated values (the uncond branch's rows of the shared latent).
 cudaError_t cfg_euler(float* z, float* z2, const float* vc, const float* vu, long long n, float dsig, float g,
                       cudaStream_t stream);
+
+// ----------------------------------------------------------------- peer barrier (elementwise.cu)
+// Cross-GPU step barrier of the fused exchanges: thread t stores val[t] into slot[t] (a flag word
+// in a peer's memory) with system-scope release after a system fence (signal), or spins with
+// system-scope acquire until *slot[t] >= val[t] (wait; traps after ~20 s instead of hanging).
+struct PeerFlags {
+  int n;
+  unsigned long long* slot[8];
+  unsigned long long val[8];
+};
+cudaError_t peer_signal(const PeerFlags& f, cudaStream_t stream);
+cudaError_t peer_wait(const PeerFlags& f, cudaStream_t stream);
 
 // ----------------------------------------------------------------- RNG (rng.cu)
 // Counter RNG of DESIGN.md "Input recipe" (independent re-implementation of synth/rng.py).

@@ -291,6 +291,31 @@ void plan_reshard(int n, int lat, const int* old_ranks, int old_p, const int* ne
   }
 }
 
+// Peer-store exchange (fused a2a, R == 0): no send / recv buffers or transfer lists, the
+// producing kernels store straight into the consumer's buffer.
+//   pack (seq -> head): local row m of request r at position `me` is full-batch row
+//     m + row_delta[r] of every destination's RECV buffer ([rows_full][Hf][d], heads of chunk j);
+//   attention output (head -> seq): full-batch row of token t of request r goes to the owner
+//     i = max{i : own_lo[r][i] <= t}, element offset o_base[r][i] + t D + (h - hoff[me]) d of
+//     the owner's ORECV buffer [rows_i][D] (o_base includes this position's column offset).
+bool peer_tables(const A2aGeometry& g, int me, std::vector<long long>& row_delta, std::vector<int>& own_lo,
+                 std::vector<long long>& o_base) {
+  if (g.R != 0 || me < 0 || me >= g.p) return false;
+  const long long D = static_cast<long long>(g.H) * g.hd;
+  row_delta.assign(g.B, 0);
+  own_lo.assign(static_cast<size_t>(g.B) * g.p, 0);
+  o_base.assign(static_cast<size_t>(g.B) * g.p, 0);
+  for (int r = 0; r < g.B; ++r) {
+    row_delta[r] = static_cast<long long>(g.off_full[r]) + g.lo[me][r] - g.loff[me][r];
+    for (int i = 0; i < g.p; ++i) {
+      own_lo[static_cast<size_t>(r) * g.p + i] = g.lo[i][r];
+      o_base[static_cast<size_t>(r) * g.p + i] =
+          static_cast<long long>(g.loff[i][r] - g.lo[i][r]) * D + static_cast<long long>(g.hoff[me]) * g.hd;
+    }
+  }
+  return true;
+}
+
 }  // namespace gs
 
 // ------------------------------------------------------------------ C-ABI (host only)
@@ -334,4 +359,22 @@ extern "C" int gs_plan_reshard(int n_tokens, int lat, const int* old_ranks, int 
   std::vector<gs_xfer> v;
   gs::plan_reshard(n_tokens, lat, old_ranks, old_p, new_ranks, new_p, me, v);
   return copy_out(v, out, max_out, n_out);
+}
+
+extern "C" int gs_plan_peer(int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
+                            long long* row_delta, int* own_lo, long long* o_base) {
+  if (p < 1 || p > 8 || me < 0 || me >= p || nreq < 1 || !n_tokens || heads < 1 || head_dim < 1 ||
+      !row_delta || !own_lo || !o_base)
+    return GS_EINVAL;
+  for (int r = 0; r < nreq; ++r)
+    if (n_tokens[r] < 0) return GS_EINVAL;
+  gs::A2aGeometry g;
+  g.init(p, n_tokens, nreq, heads, head_dim);
+  std::vector<long long> rd, ob;
+  std::vector<int> ol;
+  if (!gs::peer_tables(g, me, rd, ol, ob)) return GS_EUNSUPPORTED;
+  std::copy(rd.begin(), rd.end(), row_delta);
+  std::copy(ol.begin(), ol.end(), own_lo);
+  std::copy(ob.begin(), ob.end(), o_base);
+  return GS_OK;
 }

@@ -57,6 +57,8 @@ struct A2aGeometry {
 void plan_kv(const A2aGeometry& g, int me, std::vector<gs_xfer>& out);
 void plan_q(const A2aGeometry& g, int me, std::vector<gs_xfer>& out);
 void plan_o(const A2aGeometry& g, int me, std::vector<gs_xfer>& out, long long* stage_elems);
+bool peer_tables(const A2aGeometry& g, int me, std::vector<long long>& row_delta, std::vector<int>& own_lo,
+                 std::vector<long long>& o_base);
 void plan_reshard(int n, int lat, const int* old_ranks, int old_p, const int* new_ranks, int new_p, int me,
                   std::vector<gs_xfer>& out);
 

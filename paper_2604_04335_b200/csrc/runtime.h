@@ -118,4 +118,16 @@ struct gs_ctx {
   // pinned scratch for preemption agreement
   int* h_flag = nullptr;
   int* d_flag = nullptr;
+  // fused (peer-store) all-to-alls: mode 1 = peer stores wherever p divides the
+  // heads (default), 0 = transfer plans (NCCL send / recv, emulated device copies)
+  int a2a_mode = 1;
+  unsigned long long* flags = nullptr;                    // [world (emulated) or 1][8] barrier words
+  unsigned long long sig_sent[8][8] = {}, sig_seen[8][8] = {};  // per (src, dst) global rank pair
+  struct PeerMap {                                        // NCCL mode: CUDA IPC mappings of a peer
+    cudaIpcMemHandle_t h[5];                              // qr, kr, vr, orecv, flags
+    void* p[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  };
+  PeerMap peers[8];
+  void* ipc_dev = nullptr;                                // device staging of the handle exchange
+  long long a2a_peer = 0, a2a_plan = 0;                   // exchanges run each way (gs_stats)
 };

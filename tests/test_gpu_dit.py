@@ -218,3 +218,46 @@ def test_contract_errors(gs):
     assert ctx.run_steps([r], [0, 1], 2) == 2
     assert ctx.query(r)["state"] == gs.REQ_DONE
     ctx.close()
+
+
+# ----------------------------------------------------------------------------- fused exchange
+def _run_mode(gs, shape, sizes, p, k, a2a):
+    """Batch of requests (w, h, frames) placed on ranks 0..p-1, k steps with the given a2a mode;
+    returns (latents, stats)."""
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    ctx.set_option("a2a", a2a)
+    mid = _mk(ctx, shape)
+    ranks = list(range(p))
+    reqs = [ctx.submit(mid, w, h, f, 50, 1000 + i, ranks) for i, (w, h, f) in enumerate(sizes)]
+    ctx.run_steps([reqs[0]], ranks, 1)                   # different timesteps inside the batch
+    assert ctx.run_steps(reqs, ranks, k) == k
+    zs = [ctx.read_latent(r) for r in reqs]
+    st = ctx.stats()
+    ctx.close()
+    return zs, st
+
+
+@pytest.mark.parametrize("shape,sizes,p", [
+    (sm.WAN_1_3B.with_layers(2), [(416, 240, 5)], 2),
+    (sm.WAN_1_3B.with_layers(1), [(416, 240, 5), (256, 256, 1), (320, 192, 1)], 4),
+    (sm.WAN_14B.with_layers(1), [(320, 176, 5)], 8),
+])
+def test_fused_peer_exchange_bit_exact_vs_transfer_plans(gs, shape, sizes, p):
+    """Peer-store all-to-alls (pack kernel and attention epilogue writing the consumers' buffers,
+    flag barriers) give the same bytes as the transfer-plan exchange, and actually ran."""
+    z_peer, st_peer = _run_mode(gs, shape, sizes, p, 2, 1)
+    z_plan, st_plan = _run_mode(gs, shape, sizes, p, 2, 0)
+    assert st_peer["a2a_peer"] > 0 and st_peer["a2a_plan"] == 0
+    assert st_plan["a2a_plan"] > 0 and st_plan["a2a_peer"] == 0
+    for a, b in zip(z_peer, z_plan):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_fused_exchange_uneven_heads_uses_transfer_plans(gs):
+    """p = 8 does not divide Wan-1.3B's 12 heads: the batch falls back to the balanced-unit
+    transfer plans (reading 9), still bit-exact with SP = 1."""
+    shape = sm.WAN_1_3B.with_layers(1)
+    z8, st = _run_mode(gs, shape, [(416, 240, 5)], 8, 1, 1)
+    z1, _ = _run_mode(gs, shape, [(416, 240, 5)], 1, 1, 1)
+    assert st["a2a_plan"] > 0 and st["a2a_peer"] == 0
+    assert np.array_equal(z8[0].view(np.uint32), z1[0].view(np.uint32))

@@ -279,3 +279,138 @@ def test_two_process_gloo_exchange_and_reshard():
         errs.append(errq.get())
     assert not errs, "\n".join(errs)
     assert all(pr.exitcode == 0 for pr in procs)
+
+
+# ----------------------------------------------------------------------------- fused exchange
+def peer_stores(q, o, ns, p, me, H, d):
+    """Stores position `me` makes under the fused exchange (include/gs.h gs_plan_peer), as
+    (destination position, buffer, flat element offsets, values): the pack kernel's Q chunk of
+    every destination and its attention output rows scattered to their owners."""
+    rd, own_lo, o_base = gs.plan_peer(p, me, ns, H, d)
+    Hf, D = H // p, H * d
+    offs = np.cumsum([0] + ns[:-1])
+    out = []
+    # pack: local row m of request r -> full-batch row m + rd[r] of destination j's RECV
+    m = 0
+    for r, n in enumerate(ns):
+        lo, hi = shards(n, p)[me]
+        for t in range(lo, hi):
+            for j in range(p):
+                for hh in range(Hf):
+                    base = ((m + rd[r]) * Hf + hh) * d
+                    out.append((j, "recv", np.arange(base, base + d), q[offs[r] + t, j * Hf + hh]))
+            m += 1
+    # attention output of my heads for every row of the batch -> owner's ORECV
+    for r, n in enumerate(ns):
+        for t in range(n):
+            i = max(k for k in range(p) if own_lo[r, k] <= t)
+            for hh in range(Hf):
+                base = o_base[r, i] + t * D + hh * d
+                out.append((i, "orecv", np.arange(base, base + d), o[offs[r] + t, me * Hf + hh]))
+    return out
+
+
+PEER_CASES = [c for c in CASES if c[2] % c[0] == 0] + [(8, [75600 // 100, 37], 40, 2), (2, [1, 1, 3], 2, 3)]
+
+
+@pytest.mark.parametrize("p,ns,H,d", PEER_CASES)
+def test_peer_store_addressing_realises_ulysses_layouts(p, ns, H, d):
+    """Fused all-to-alls: the pack kernel's and the attention epilogue's peer stores fill every
+    RECV / ORECV element exactly once, with the same bytes the transfer plans deliver."""
+    g = np.random.default_rng(p * 77 + H)
+    N = sum(ns)
+    q = g.integers(-1000, 1000, (N, H, d)).astype(np.int64)
+    o = g.integers(-1000, 1000, (N, H, d)).astype(np.int64)
+    offs = np.cumsum([0] + ns[:-1])
+    rows = [sum(hi - lo for n in ns for lo, hi in [shards(n, p)[i]]) for i in range(p)]
+    recv = [np.full(recv_layout(q, ns, p, j, H, "q").size, -7, np.int64) for j in range(p)]
+    orecv = [np.full(rows[i] * H * d, -5, np.int64) for i in range(p)]
+    hits = [np.zeros(b.size, np.int64) for b in recv], [np.zeros(b.size, np.int64) for b in orecv]
+    for me in range(p):
+        for dst, buf, idx, val in peer_stores(q, o, ns, p, me, H, d):
+            (recv if buf == "recv" else orecv)[dst][idx] = val
+            hits[0 if buf == "recv" else 1][dst][idx] += 1
+    for j in range(p):
+        np.testing.assert_array_equal(recv[j], recv_layout(q, ns, p, j, H, "q"))
+        want = np.concatenate([o[of + lo:of + hi] for of, n in zip(offs, ns)
+                               for lo, hi in [shards(n, p)[j]]]).ravel()
+        np.testing.assert_array_equal(orecv[j], want)
+        assert (hits[0][j] == 1).all() and (hits[1][j] == 1).all()
+
+
+def test_peer_addressing_rejects_uneven_heads():
+    with pytest.raises(gs.GsError) as e:
+        gs.plan_peer(8, 0, [100], 12, 8)
+    assert e.value.code == gs.GS_EUNSUPPORTED
+    with pytest.raises(gs.GsError):
+        gs.plan_peer(2, 2, [100], 12, 8)
+
+
+def _peer_worker(rank, world, port, errq):
+    """Two processes: each computes its own peer stores and ships them to the destination over
+    gloo (standing in for NVLink stores); the receiver's buffers must equal the Ulysses layouts."""
+    try:
+        import torch
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        p, ns, H, d = 2, [37, 64, 5], 12, 4
+        N = sum(ns)
+        g = np.random.default_rng(11)
+        q = g.integers(-99, 99, (N, H, d)).astype(np.int64)
+        o = g.integers(-99, 99, (N, H, d)).astype(np.int64)
+        offs = np.cumsum([0] + ns[:-1])
+        me = rank
+        rows_me = sum(hi - lo for n in ns for lo, hi in [shards(n, p)[me]])
+        mine = {"recv": np.full(recv_layout(q, ns, p, me, H, "q").size, -7, np.int64),
+                "orecv": np.full(rows_me * H * d, -5, np.int64)}
+        outgoing = {"recv": ([], []), "orecv": ([], [])}
+        for dst, buf, idx, val in peer_stores(q, o, ns, p, me, H, d):
+            if dst == me:
+                mine[buf][idx] = val
+            else:
+                outgoing[buf][0].append(idx)
+                outgoing[buf][1].append(val)
+        for k, buf in enumerate(("recv", "orecv")):
+            idx = np.concatenate(outgoing[buf][0])
+            val = np.concatenate(outgoing[buf][1])
+            cnt = torch.tensor([idx.size])
+            peer_cnt = torch.zeros(1, dtype=torch.int64)
+            reqs = [dist.isend(cnt, dst=1 - me, tag=10 + k), dist.irecv(peer_cnt, src=1 - me, tag=10 + k)]
+            for r in reqs:
+                r.wait()
+            pi = torch.empty(int(peer_cnt), dtype=torch.int64)
+            pv = torch.empty(int(peer_cnt), dtype=torch.int64)
+            reqs = [dist.isend(torch.from_numpy(idx), dst=1 - me, tag=20 + k),
+                    dist.isend(torch.from_numpy(val), dst=1 - me, tag=30 + k),
+                    dist.irecv(pi, src=1 - me, tag=20 + k), dist.irecv(pv, src=1 - me, tag=30 + k)]
+            for r in reqs:
+                r.wait()
+            mine[buf][pi.numpy()] = pv.numpy()
+        np.testing.assert_array_equal(mine["recv"], recv_layout(q, ns, p, me, H, "q"))
+        want = np.concatenate([o[of + lo:of + hi] for of, n in zip(offs, ns)
+                               for lo, hi in [shards(n, p)[me]]]).ravel()
+        np.testing.assert_array_equal(mine["orecv"], want)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # noqa: BLE001
+        import traceback
+        errq.put(f"rank {rank}: {e!r}\n{traceback.format_exc()}")
+
+
+def test_two_process_gloo_peer_store_exchange():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, errq)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, "\n".join(errs)
+    assert all(pr.exitcode == 0 for pr in procs)
