@@ -33,37 +33,52 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return (red[0] + red[1]) + (red[2] + red[3]);
 }
 
+// Row kernels come in two shapes, chosen by D alone (so every row of a model takes the same
+// reduction order): TPR = 128 threads per row (one row per CTA, D > 2048: Wan-14B) or TPR = 32 (a
+// warp per row, 8 rows per CTA, shuffle-only reductions: D <= 2048, where one CTA per row left
+// HBM half idle -- 26% of peak at the config-2 T2I shape).
+template <int TPR>
+__device__ __forceinline__ float row_sum(float v, float* red) {
+  if (TPR == 32) return warp_sum(v);
+  return block_sum(v, red);
+}
+constexpr int kWarpRowMaxD = 2048;
+constexpr int kWarpRowsPerCta = 8;
+
 // ------------------------------------------------------------------ LN + modulate
-__global__ void __launch_bounds__(ROW_THREADS)
-    ln_modulate_kernel(const float* __restrict__ x, int D, const float* __restrict__ sh_a,
+template <int TPR>
+__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS)
+    ln_modulate_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ sh_a,
                        const float* __restrict__ sh_b, const float* __restrict__ sc_a,
                        const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
                        float eps, __nv_bfloat16* __restrict__ out) {
   __shared__ float red[4];
-  const long long row = blockIdx.x;
+  const long long row = TPR == 32 ? blockIdx.x * (long long)kWarpRowsPerCta + (threadIdx.x >> 5) : blockIdx.x;
+  const int tid = TPR == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  if (TPR == 32 && row >= M) return;
   const int nv = D >> 2;
   const float4* xr = reinterpret_cast<const float4*>(x + row * D);
   float4 v[MAXV];
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int c = threadIdx.x + i * ROW_THREADS;
+    const int c = tid + i * TPR;
     if (c < nv) {
       v[i] = xr[c];
       s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
     }
   }
-  const float mean = block_sum(s, red) / D;
+  const float mean = row_sum<TPR>(s, red) / D;
   float q = 0.f;
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int c = threadIdx.x + i * ROW_THREADS;
+    const int c = tid + i * TPR;
     if (c < nv) {
       const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
       q += (a * a + b * b) + (cc * cc + d * d);
     }
   }
-  const float rstd = rsqrtf(block_sum(q, red) / D + eps);
+  const float rstd = rsqrtf(row_sum<TPR>(q, red) / D + eps);
   const int r = row_req[row];
   const float4* sha = reinterpret_cast<const float4*>(sh_a);
   const float4* sca = reinterpret_cast<const float4*>(sc_a);
@@ -72,7 +87,7 @@ __global__ void __launch_bounds__(ROW_THREADS)
   uint2* o = reinterpret_cast<uint2*>(out + row * D);
 #pragma unroll
   for (int i = 0; i < MAXV; ++i) {
-    const int c = threadIdx.x + i * ROW_THREADS;
+    const int c = tid + i * TPR;
     if (c < nv) {
       const float4 a1 = __ldg(sha + c), b1 = __ldg(shb + c), a2 = __ldg(sca + c), b2 = __ldg(scb + c);
       const float y0 = (v[i].x - mean) * rstd * (1.f + (a2.x + b2.x)) + (a1.x + b1.x);
@@ -96,21 +111,24 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   }
 }
 
-__global__ void __launch_bounds__(ROW_THREADS)
-    qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int D, int d,
+template <int TPR>
+__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS)
+    qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
                              const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
                              float eps, const RopeParams rp, const PackParams pk,
                              __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
                              __nv_bfloat16* __restrict__ v_out) {
   __shared__ float red[4];
-  const long long row = blockIdx.x;
+  const long long row = TPR == 32 ? blockIdx.x * (long long)kWarpRowsPerCta + (threadIdx.x >> 5) : blockIdx.x;
+  const int tid = TPR == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  if (TPR == 32 && row >= M) return;
   const int nv = D >> 3;  // uint4 chunks (8 elements) per q/k/v row
   const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
   uint4 qv[MAXV / 2], kv[MAXV / 2];
   float sq = 0.f, sk = 0.f;
 #pragma unroll
   for (int i = 0; i < MAXV / 2; ++i) {
-    const int c = threadIdx.x + i * ROW_THREADS;
+    const int c = tid + i * TPR;
     if (c < nv) {
       qv[i] = src[c];
       kv[i] = src[nv + c];
@@ -123,8 +141,8 @@ __global__ void __launch_bounds__(ROW_THREADS)
             ((f[4] * f[4] + f[5] * f[5]) + (f[6] * f[6] + f[7] * f[7]));
     }
   }
-  const float rq = rsqrtf(block_sum(sq, red) / D + eps);
-  const float rk = rsqrtf(block_sum(sk, red) / D + eps);
+  const float rq = rsqrtf(row_sum<TPR>(sq, red) / D + eps);
+  const float rk = rsqrtf(row_sum<TPR>(sk, red) / D + eps);
 
   const int r = rp.row_req[row];
   const int tok = rp.row_tok[row];
@@ -135,7 +153,7 @@ __global__ void __launch_bounds__(ROW_THREADS)
   const uint4* gk = reinterpret_cast<const uint4*>(g_k);
 #pragma unroll
   for (int i = 0; i < MAXV / 2; ++i) {
-    const int c = threadIdx.x + i * ROW_THREADS;
+    const int c = tid + i * TPR;
     if (c < nv) {
       const int e0 = c * 8;
       const int h = e0 / d, i0 = e0 - h * d;
@@ -313,8 +331,12 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
                         float eps, __nv_bfloat16* out, cudaStream_t stream) {
   if (M == 0) return cudaSuccess;
   if (D % 4 || D > 4 * MAXV * ROW_THREADS) return cudaErrorInvalidValue;
-  ln_modulate_kernel<<<M, ROW_THREADS, 0, stream>>>(x, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req,
-                                                     eps, out);
+  if (D <= kWarpRowMaxD)
+    ln_modulate_kernel<32><<<(M + kWarpRowsPerCta - 1) / kWarpRowsPerCta, 32 * kWarpRowsPerCta, 0, stream>>>(
+        x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out);
+  else
+    ln_modulate_kernel<ROW_THREADS><<<M, ROW_THREADS, 0, stream>>>(x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride,
+                                                                   row_req, eps, out);
   return cudaGetLastError();
 }
 
@@ -326,8 +348,12 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   const int d = D / heads;
   if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > 16)
     return cudaErrorInvalidValue;
-  qk_norm_rope_pack_kernel<<<M, ROW_THREADS, 0, stream>>>(qkv, D, d, g_q, g_k, eps, rp, pk, q_out,
-                                                           k_out, v_out);
+  if (D <= kWarpRowMaxD)
+    qk_norm_rope_pack_kernel<32><<<(M + kWarpRowsPerCta - 1) / kWarpRowsPerCta, 32 * kWarpRowsPerCta, 0,
+                                   stream>>>(qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out);
+  else
+    qk_norm_rope_pack_kernel<ROW_THREADS><<<M, ROW_THREADS, 0, stream>>>(qkv, M, D, d, g_q, g_k, eps, rp, pk,
+                                                                         q_out, k_out, v_out);
   return cudaGetLastError();
 }
 
