@@ -46,8 +46,10 @@ constexpr int kWarpRowMaxD = 2048;
 constexpr int kWarpRowsPerCta = 8;
 
 // ------------------------------------------------------------------ LN + modulate
-template <int TPR>
-__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS)
+// VPL = float4 (LN) / uint4 per tensor (qk) per thread: sized exactly from D so the registers of
+// one row stay small and several CTAs share an SM (occupancy hides the DRAM latency of the row).
+template <int TPR, int VPL>
+__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, TPR == 32 ? 4 : 1)
     ln_modulate_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ sh_a,
                        const float* __restrict__ sh_b, const float* __restrict__ sc_a,
                        const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
@@ -58,10 +60,10 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
   if (TPR == 32 && row >= M) return;
   const int nv = D >> 2;
   const float4* xr = reinterpret_cast<const float4*>(x + row * D);
-  float4 v[MAXV];
+  float4 v[VPL];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
+  for (int i = 0; i < VPL; ++i) {
     const int c = tid + i * TPR;
     if (c < nv) {
       v[i] = xr[c];
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
   const float mean = row_sum<TPR>(s, red) / D;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
+  for (int i = 0; i < VPL; ++i) {
     const int c = tid + i * TPR;
     if (c < nv) {
       const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
   const float4* scb = reinterpret_cast<const float4*>(sc_b + (long long)r * b_stride);
   uint2* o = reinterpret_cast<uint2*>(out + row * D);
 #pragma unroll
-  for (int i = 0; i < MAXV; ++i) {
+  for (int i = 0; i < VPL; ++i) {
     const int c = tid + i * TPR;
     if (c < nv) {
       const float4 a1 = __ldg(sha + c), b1 = __ldg(shb + c), a2 = __ldg(sca + c), b2 = __ldg(scb + c);
@@ -111,8 +113,34 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   }
 }
 
-template <int TPR>
-__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS)
+// Element offset of (row, head h, element i0 of the head) in its pack chunk's destination: the
+// send layout [rows][H_j][d] at dest_off[j], or (peer mode) the full-batch row of the RECV buffer.
+__device__ __forceinline__ long long pack_offset(const PackParams& pk, long long row, int h, int i0, int d,
+                                                 int* jc_out, int& h0, int& h1) {
+  int jc = 0;
+  h0 = pk.head_off[0];
+  h1 = pk.head_off[1];
+#pragma unroll
+  for (int t = 1; t < 16; ++t) {
+    if (t < pk.ndest && h >= pk.head_off[t]) {
+      h0 = pk.head_off[t];
+      h1 = pk.head_off[t + 1];
+      jc = t;
+    }
+  }
+  *jc_out = jc;
+  if (pk.peer) {
+    int sq = 0;
+#pragma unroll
+    for (int t = 1; t < 16; ++t)
+      if (t < pk.nseq && row >= pk.seq_lo[t]) sq = t;
+    return ((row + pk.row_delta[sq]) * (h1 - h0) + (h - h0)) * (long long)d + i0;
+  }
+  return pk.dest_off[jc] + (row * (h1 - h0) + (h - h0)) * (long long)d + i0;
+}
+
+template <int TPR, int VPL>
+__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, TPR == 32 ? 3 : 1)
     qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
                              const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
                              float eps, const RopeParams rp, const PackParams pk,
@@ -124,10 +152,10 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
   if (TPR == 32 && row >= M) return;
   const int nv = D >> 3;  // uint4 chunks (8 elements) per q/k/v row
   const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
-  uint4 qv[MAXV / 2], kv[MAXV / 2];
+  uint4 qv[VPL], kv[VPL];
   float sq = 0.f, sk = 0.f;
 #pragma unroll
-  for (int i = 0; i < MAXV / 2; ++i) {
+  for (int i = 0; i < VPL; ++i) {
     const int c = tid + i * TPR;
     if (c < nv) {
       qv[i] = src[c];
@@ -152,33 +180,18 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
   const uint4* gq = reinterpret_cast<const uint4*>(g_q);
   const uint4* gk = reinterpret_cast<const uint4*>(g_k);
 #pragma unroll
-  for (int i = 0; i < MAXV / 2; ++i) {
+  for (int i = 0; i < VPL; ++i) {
     const int c = tid + i * TPR;
     if (c < nv) {
       const int e0 = c * 8;
       const int h = e0 / d, i0 = e0 - h * d;
-      int h0 = pk.head_off[0], h1 = pk.head_off[1], jc = 0;
-#pragma unroll
-      for (int t = 1; t < 16; ++t) {
-        if (t < pk.ndest && h >= pk.head_off[t]) {
-          h0 = pk.head_off[t];
-          h1 = pk.head_off[t + 1];
-          jc = t;
-        }
-      }
+      int jc = 0, h0 = 0, h1 = 0;
       __nv_bfloat16 *dq = q_out, *dk = k_out, *dv = v_out;
-      long long o;
-      if (pk.peer) {  // straight into the destination's RECV buffer (full-batch row)
-        int sq = 0;
-#pragma unroll
-        for (int t = 1; t < 16; ++t)
-          if (t < pk.nseq && row >= pk.seq_lo[t]) sq = t;
+      const long long o = pack_offset(pk, row, h, i0, d, &jc, h0, h1);
+      if (pk.peer) {
         dq = pk.dst_q[jc];
         dk = pk.dst_k[jc];
         dv = pk.dst_v[jc];
-        o = ((row + pk.row_delta[sq]) * (h1 - h0) + (h - h0)) * (long long)d + i0;
-      } else {
-        o = pk.dest_off[jc] + (row * (h1 - h0) + (h - h0)) * (long long)d + i0;
       }
       float fq[8], fk[8], wq[8], wk[8];
       unpack8(qv[i], fq);
@@ -331,12 +344,26 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
                         float eps, __nv_bfloat16* out, cudaStream_t stream) {
   if (M == 0) return cudaSuccess;
   if (D % 4 || D > 4 * MAXV * ROW_THREADS) return cudaErrorInvalidValue;
-  if (D <= kWarpRowMaxD)
-    ln_modulate_kernel<32><<<(M + kWarpRowsPerCta - 1) / kWarpRowsPerCta, 32 * kWarpRowsPerCta, 0, stream>>>(
-        x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out);
-  else
-    ln_modulate_kernel<ROW_THREADS><<<M, ROW_THREADS, 0, stream>>>(x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride,
-                                                                   row_req, eps, out);
+  const int tpr = D <= kWarpRowMaxD ? 32 : ROW_THREADS;
+  const int vpl = (D / 4 + tpr - 1) / tpr;  // 1..16
+  const dim3 grid(tpr == 32 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
+  const dim3 block(tpr == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS);
+#define GS_LN_CASE(T, V) \
+  case V: ln_modulate_kernel<T, V><<<grid, block, 0, stream>>>(x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out); break;
+#define GS_LN_SWITCH(T)                                                                                     \
+  switch (vpl) {                                                                                           \
+    GS_LN_CASE(T, 1) GS_LN_CASE(T, 2) GS_LN_CASE(T, 3) GS_LN_CASE(T, 4) GS_LN_CASE(T, 5) GS_LN_CASE(T, 6)  \
+    GS_LN_CASE(T, 7) GS_LN_CASE(T, 8) GS_LN_CASE(T, 9) GS_LN_CASE(T, 10) GS_LN_CASE(T, 11)                 \
+    GS_LN_CASE(T, 12) GS_LN_CASE(T, 13) GS_LN_CASE(T, 14) GS_LN_CASE(T, 15) GS_LN_CASE(T, 16)              \
+    default: return cudaErrorInvalidValue;                                                                 \
+  }
+  if (tpr == 32) {
+    GS_LN_SWITCH(32)
+  } else {
+    GS_LN_SWITCH(ROW_THREADS)
+  }
+#undef GS_LN_SWITCH
+#undef GS_LN_CASE
   return cudaGetLastError();
 }
 
@@ -348,12 +375,25 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   const int d = D / heads;
   if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > 16)
     return cudaErrorInvalidValue;
-  if (D <= kWarpRowMaxD)
-    qk_norm_rope_pack_kernel<32><<<(M + kWarpRowsPerCta - 1) / kWarpRowsPerCta, 32 * kWarpRowsPerCta, 0,
-                                   stream>>>(qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out);
-  else
-    qk_norm_rope_pack_kernel<ROW_THREADS><<<M, ROW_THREADS, 0, stream>>>(qkv, M, D, d, g_q, g_k, eps, rp, pk,
-                                                                         q_out, k_out, v_out);
+  const int tpr = D <= kWarpRowMaxD ? 32 : ROW_THREADS;
+  const int vpl = (D / 8 + tpr - 1) / tpr;  // 1..8
+  const dim3 grid(tpr == 32 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
+  const dim3 block(tpr == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS);
+#define GS_QK_CASE(T, V) \
+  case V: qk_norm_rope_pack_kernel<T, V><<<grid, block, 0, stream>>>(qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out); break;
+#define GS_QK_SWITCH(T)                                                                                         \
+  switch (vpl) {                                                                                               \
+    GS_QK_CASE(T, 1) GS_QK_CASE(T, 2) GS_QK_CASE(T, 3) GS_QK_CASE(T, 4) GS_QK_CASE(T, 5) GS_QK_CASE(T, 6)      \
+    GS_QK_CASE(T, 7) GS_QK_CASE(T, 8)                                                                          \
+    default: return cudaErrorInvalidValue;                                                                     \
+  }
+  if (tpr == 32) {
+    GS_QK_SWITCH(32)
+  } else {
+    GS_QK_SWITCH(ROW_THREADS)
+  }
+#undef GS_QK_SWITCH
+#undef GS_QK_CASE
   return cudaGetLastError();
 }
 
@@ -382,6 +422,35 @@ __global__ void peer_wait_kernel(const PeerFlags f) {
     asm volatile("fence.acq_rel.sys;" ::: "memory");
   }
   __syncthreads();
+}
+
+__global__ void peer_wait_probe_kernel(const PeerFlags f, long long timeout_ns, int* ok) {
+  __shared__ int good;
+  if (threadIdx.x == 0) good = 1;
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < f.n) {
+    unsigned long long v = 0, t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f.slot[t]) : "memory");
+      if (v >= f.val[t]) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (static_cast<long long>(now - t0) > timeout_ns) {
+        atomicExch(&good, 0);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ok = good;
+}
+
+cudaError_t peer_wait_probe(const PeerFlags& f, int timeout_ms, int* ok, cudaStream_t stream) {
+  if (f.n < 0 || f.n > 8 || !ok) return cudaErrorInvalidValue;
+  peer_wait_probe_kernel<<<1, 32, 0, stream>>>(f, static_cast<long long>(timeout_ms) * 1000000LL, ok);
+  return cudaGetLastError();
 }
 
 cudaError_t peer_signal(const PeerFlags& f, cudaStream_t stream) {

@@ -567,7 +567,8 @@ int peer_setup(gs_ctx* c, Plan& P) {
   P.orecv_of.assign(P.p, nullptr);
   P.flags_of.assign(P.p, nullptr);
   if (!c->flags) {
-    const size_t words = static_cast<size_t>(c->emulated ? c->world : 1) * 8;
+    // words [0, 8): barrier counters per source rank, [8, 16): mapping-probe counters
+    const size_t words = static_cast<size_t>(c->emulated ? c->world : 1) * 16;
     CK(cudaMalloc(&c->flags, words * 8));
     CK(cudaMemset(c->flags, 0, words * 8));
   }
@@ -578,7 +579,7 @@ int peer_setup(gs_ctx* c, Plan& P) {
       P.kr_of[j] = A.kr.as<bf16>();
       P.vr_of[j] = A.vr.as<bf16>();
       P.orecv_of[j] = A.orecv.as<bf16>();
-      P.flags_of[j] = c->flags + static_cast<size_t>(P.ranks[j]) * 8;
+      P.flags_of[j] = c->flags + static_cast<size_t>(P.ranks[j]) * 16;
     }
     P.peer = true;
     return GS_OK;
@@ -627,7 +628,28 @@ int peer_setup(gs_ctx* c, Plan& P) {
       }
     }
   }
-  // second round: peer stores only if every position mapped every peer (else all use the plans)
+  // probe the mappings: store a per-pair counter into every peer's probe word through them and
+  // wait (bounded) for every peer's store into ours; then agree -- peer stores only if every
+  // position mapped and reached every peer (else the whole group uses the transfer plans)
+  if (ok) {
+    PeerFlags sig{}, wt{};
+    for (int j = 0; j < P.p; ++j) {
+      if (j == me) continue;
+      const int gj = P.ranks[j];
+      sig.slot[sig.n] = static_cast<unsigned long long*>(c->peers[gj].p[4]) + 8 + c->my_rank;
+      sig.val[sig.n++] = ++c->probe_sent[gj];
+      wt.slot[wt.n] = c->flags + 8 + gj;
+      wt.val[wt.n++] = c->probe_seen[gj] + 1;
+    }
+    CK(peer_signal(sig, c->stream));
+    CK(peer_wait_probe(wt, 2000, c->d_flag + 12, c->stream));
+    CK(cudaMemcpyAsync(c->h_flag + 12, c->d_flag + 12, 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    ok = c->h_flag[12];
+    if (ok)
+      for (int j = 0; j < P.p; ++j)
+        if (j != me) ++c->probe_seen[P.ranks[j]];
+  }
   std::vector<IpcExport> agree(P.p);
   agree[me].ok = ok;
   RET(exchange(agree.data()));

@@ -127,6 +127,10 @@ struct PeerFlags {
 };
 cudaError_t peer_signal(const PeerFlags& f, cudaStream_t stream);
 cudaError_t peer_wait(const PeerFlags& f, cudaStream_t stream);
+// Probe variant of peer_wait: gives up after ~timeout_ms and stores 1 (all flags arrived) or 0 to
+// *ok (device int) instead of trapping -- used once per gs_run_steps to prove the IPC mappings
+// before any data-path kernel stores into peer memory.
+cudaError_t peer_wait_probe(const PeerFlags& f, int timeout_ms, int* ok, cudaStream_t stream);
 
 // ----------------------------------------------------------------- RNG (rng.cu)
 // Counter RNG of DESIGN.md "Input recipe" (independent re-implementation of synth/rng.py).

@@ -123,6 +123,7 @@ struct gs_ctx {
   int a2a_mode = 1;
   unsigned long long* flags = nullptr;                    // [world (emulated) or 1][8] barrier words
   unsigned long long sig_sent[8][8] = {}, sig_seen[8][8] = {};  // per (src, dst) global rank pair
+  unsigned long long probe_sent[8] = {}, probe_seen[8] = {};      // NCCL mode: mapping probes per peer
   struct PeerMap {                                        // NCCL mode: CUDA IPC mappings of a peer
     cudaIpcMemHandle_t h[5];                              // qr, kr, vr, orecv, flags
     void* p[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
