@@ -15,6 +15,10 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+
 #include "kernels.h"
 #include "ptx.cuh"
 #include "tma.h"
@@ -25,16 +29,26 @@ namespace {
 // CTA-pair (cta_group::2) tiles: the pair computes 256 x 256 outputs with M=256 N=256 K=16 MMAs
 // issued by the leader CTA; each CTA stages its 128 A rows and its 128-row half of W per stage,
 // and holds its 128 output rows x 256 fp32 columns in its own TMEM.
+// BN = 256 (default) or 192 (N % 192 == 0 and the 192-wide grid fills its waves enough better
+// to pay for its ~15% lower per-FLOP rate: small-M grids such as config 3 at SP 4 / 8, where
+// M = 4095 gives 96 256-wide tiles on 74 pairs).  Both issue
+// M=256 K=16 MMAs over the same K order; the N width does not change any output element's
+// accumulation (tests/test_gpu_kernels.py checks the two widths bit for bit), so the choice may
+// depend on M without breaking SP / batch invariance.  (128-wide tiles were measured 35% slower
+// per FLOP: 1.5x the L2 -> SM bytes; profiles/r01_notes.md.)
 constexpr int BM = 128;                     // output rows per CTA (pair tile: 256)
-constexpr int BN = 256;                     // output columns per pair tile
 constexpr int PM = 2 * BM;                  // pair tile rows
-constexpr int BK = 64, STAGES = 6;
+constexpr int BK = 64;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
-constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB: this CTA's half of the W tile
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int THREADS = 192;
-constexpr uint32_t TMEM_COLS = 512;         // 2 accumulators x 256 columns
+constexpr uint32_t TMEM_COLS = 512;         // 2 accumulators x (up to) 256 columns
+template <int BN>
+struct GCfg {
+  static constexpr int STAGES = BN == 256 ? 6 : 7;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the W tile
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
 
 __device__ __forceinline__ float gelu_tanh_f(float u) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -125,6 +139,10 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int row,
   }
 }
 
+// Per-FLOP rate of 192-wide relative to 256-wide pair tiles (kbench at large grids: c4 sp1 qkv
+// 1223 vs 1494, c4 sp8 qkv 1314 vs 1513 TFLOP/s; profiles/r01_notes.md).
+constexpr double kNarrowRate = 0.85;
+
 // Tile rasterisation: bands of GROUP_M M-tiles, N-major inside a band, so the ~148 tiles in
 // flight cover a GROUP_M x (148 / GROUP_M) block whose A and W panels stay resident in L2.
 constexpr int GROUP_M = 16;
@@ -137,10 +155,11 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
   nb = r / gm;
 }
 
-template <int EPI>
+template <int EPI, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    int M, int N, int K, const __grid_constant__ EpiParams ep) {
+  constexpr int STAGES = GCfg<BN>::STAGES, STAGE_BYTES = GCfg<BN>::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -258,25 +277,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int EPI>
-cudaError_t launch(int M, int N, int K, const void* A, int lda, const void* W, int ldw,
-                   const EpiParams& ep, int num_sms, cudaStream_t stream) {
+template <int EPI, int BN>
+cudaError_t launch_bn(int M, int N, int K, const void* A, int lda, const void* W, int ldw,
+                      const EpiParams& ep, int num_sms, cudaStream_t stream) {
   CUtensorMap ta, tb;
   if (!make_tma_2d_bf16(&ta, A, K, M, static_cast<uint64_t>(lda) * 2, BK, BM)) return cudaErrorInvalidValue;
   if (!make_tma_2d_bf16(&tb, W, K, N, static_cast<uint64_t>(ldw) * 2, BK, BN / 2)) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         GCfg<BN>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((M + PM - 1) / PM) * ((N + BN - 1) / BN);
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   const int grid = 2 * pairs;  // clusters of 2 (CTA pairs on one TPC)
-  gemm_tc_kernel<EPI><<<grid, THREADS, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+  gemm_tc_kernel<EPI, BN><<<grid, THREADS, GCfg<BN>::SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
   return cudaGetLastError();
 }
+
+int pick_bn(int M, int N, int num_sms) {
+  static const int env = [] {
+    const char* e = getenv("GS_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  const int forced = g_gemm_bn_override.load(std::memory_order_relaxed);
+  const int f = forced ? forced : env;
+  if (f == 192 && N % 192 == 0) return 192;
+  if (f == 256) return 256;
+  if (N % 192) return 256;
+  const double pairs = num_sms / 2;
+  const double mt = (M + PM - 1) / PM;
+  auto fill = [&](int bn) {  // fraction of the pair-slots x waves doing useful tiles
+    const double tiles = mt * (N / bn);
+    return tiles / (std::ceil(tiles / pairs) * pairs) * bn / 256.0 * (256.0 / bn);
+  };
+  return fill(192) * kNarrowRate > fill(256) ? 192 : 256;
+}
+
+template <int EPI>
+cudaError_t launch(int M, int N, int K, const void* A, int lda, const void* W, int ldw,
+                   const EpiParams& ep, int num_sms, cudaStream_t stream) {
+  if (pick_bn(M, N, num_sms) == 192) return launch_bn<EPI, 192>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+  return launch_bn<EPI, 256>(M, N, K, A, lda, W, ldw, ep, num_sms, stream);
+}
 }  // namespace
+std::atomic<int> g_gemm_bn_override{0};
 
 cudaError_t gemm_bf16_tc(int epi, int M, int N, int K, const void* A, int lda, const void* W,
                          int ldw, const EpiParams& ep, int num_sms, cudaStream_t stream) {

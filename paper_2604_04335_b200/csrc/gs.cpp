@@ -1172,6 +1172,11 @@ int gs_set_option(gs_ctx* c, const char* key, long long value) {
     c->a2a_mode = static_cast<int>(value);
     return GS_OK;
   }
+  if (strcmp(key, "gemm_bn") == 0) {
+    if (value != 0 && value != 192 && value != 256) return fail(c, GS_EINVAL, "gemm_bn %lld (0, 192, 256)", value);
+    g_gemm_bn_override.store(static_cast<int>(value));
+    return GS_OK;
+  }
   return fail(c, GS_EINVAL, "unknown option '%s'", key);
 }
 

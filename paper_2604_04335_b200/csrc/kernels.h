@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace gs {
 
 // ----------------------------------------------------------------- GEMM (gemm.cu)
@@ -30,6 +32,8 @@ struct EpiParams {
   float dsig[8];              // per-request sigma_{i+1} - sigma_i
 };
 
+// Process-wide GEMM pair-tile width override (0 = automatic, 192 or 256; gs_set_option "gemm_bn").
+extern std::atomic<int> g_gemm_bn_override;
 // Returns cudaError_t; builds the TMA descriptors on the host.
 cudaError_t gemm_bf16_tc(int epi, int M, int N, int K, const void* A, int lda, const void* W,
                          int ldw, const EpiParams& ep, int num_sms, cudaStream_t stream);

@@ -215,3 +215,29 @@ def test_time_embedding(ctx):
         r0, r = dit.time_embedding(np.float64(np.float32(t)), glob)
         assert rel_l2(e0[i], r0) < 1e-5
         assert rel_l2(e[i], r.reshape(-1)) < 1e-5
+
+
+@pytest.mark.parametrize("epi", [0, 1, 3])
+def test_gemm_pair_tile_width_does_not_change_bits(ctx, torch, epi):
+    """The 192- and 256-wide pair tiles (the choice depends on the grid size, i.e. on M) give
+    identical outputs, so SP degree / batch composition cannot change GEMM bits through it."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    M, N, K = 1000, 1536, 1536
+    A = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.03).to(torch.bfloat16)
+    b = (torch.randn(N, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    ga = torch.rand(N, device="cuda", generator=g)
+    gb = torch.rand(2, N, device="cuda", generator=g)
+    rr = (torch.arange(M, device="cuda") % 2).to(torch.int32)
+    outs = []
+    for bn in (192, 256):
+        ctx.set_option("gemm_bn", bn)
+        if epi == 3:
+            out = torch.randn(M, N, device="cuda", generator=torch.Generator(device="cuda").manual_seed(9))
+            ctx.debug_gemm(epi, M, N, K, A, W, b, out, ga, gb, N, rr)
+        else:
+            out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            ctx.debug_gemm(epi, M, N, K, A, W, b, out)
+        outs.append(out.view(torch.int16 if out.dtype == torch.bfloat16 else torch.int32).cpu())
+    ctx.set_option("gemm_bn", 0)
+    assert torch.equal(outs[0], outs[1])
