@@ -93,7 +93,9 @@ def load(path=LIB_PATH):
         raise RuntimeError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)
     for name, args in _SIG.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:  # an older libgs.so loaded for an A/B comparison (tools/kbench.py --lib)
+            continue
         fn.argtypes = args
         fn.restype = ctypes.c_char_p if name == "gs_last_error" else (None if name == "gs_destroy" else ctypes.c_int)
     _lib = lib

@@ -119,7 +119,9 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], floa
   return __fadd2_rn(acc0, acc1);
 }
 
-template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128)>
+// SCATTER: the fused head->seq exchange epilogue (OScatter); a separate instantiation so the plain
+// kernel keeps its register allocation (the scatter lookup in the shared epilogue cost ~5%).
+template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
@@ -154,6 +156,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int q_rows = min(256, tab.q_len[r] - pair * ROWS - static_cast<int>(rank) * 256);  // may be <= 0
   const int nkv = (kv_len + 127) / 128;
 
+  __shared__ int scat_meta[2];
+  if (SCATTER && threadIdx.x == 0) {
+    scat_meta[0] = r;
+    scat_meta[1] = q_row0 - tab.q_off[r];
+  }
   if (threadIdx.x == 0) {
     constexpr int NC = PAIR ? 2 : 1;  // leader-side full barriers count one arrival per CTA
     mbar_init(q_full, NC);
@@ -403,13 +410,16 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int row_in = w * 128 + quarter * 32 + lane;
     const float inv = 1.0f / l_run;
     __nv_bfloat16* orow;
-    if (osc.nown > 0) {  // fused head->seq exchange: straight into the token owner's O-proj input
-      const int t = q_row0 + row_in - tab.q_off[r];
+    if (SCATTER) {  // fused head->seq exchange: straight into the token owner's O-proj input
+      // segment and first token of this CTA come back from shared memory (kept out of the
+      // registers of the softmax loop)
+      const int rr = scat_meta[0];
+      const int t = scat_meta[1] + row_in;
       int i = 0;
 #pragma unroll
       for (int k = 1; k < 8; ++k)
-        if (k < osc.nown && t >= osc.lo[r][k]) i = k;
-      orow = osc.base[r][i] + static_cast<long long>(t) * o_rs + head * HD;
+        if (k < osc.nown && t >= osc.lo[rr][k]) i = k;
+      orow = osc.base[rr][i] + static_cast<long long>(t) * o_rs + head * HD;
     } else {
       orow = O + static_cast<long long>(q_row0 + row_in) * o_rs + head * HD;
     }
@@ -818,7 +828,9 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
       !make_tma_3d_bf16(&tv, V, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
   static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
-  auto kern = trace ? attn_tc_kernel<HD, POLY8, true> : attn_tc_kernel<HD, POLY8, false>;
+  auto kern = osc.nown > 0 ? attn_tc_kernel<HD, POLY8, false, PAIR, true>
+              : trace      ? attn_tc_kernel<HD, POLY8, true>
+                           : attn_tc_kernel<HD, POLY8, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));

@@ -64,7 +64,10 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--torch", action="store_true", help="also time torch SDPA / matmul yardsticks")
     ap.add_argument("--only", default=None, help="substring filter on the case label")
+    ap.add_argument("--lib", default=None, help="load this libgs.so instead of the in-tree one (A/B)")
     a = ap.parse_args()
+    if a.lib:
+        gs.load(a.lib)
     if not (a.attn or a.gemm):
         a.attn = a.gemm = True
     ctx = gs.Context(device=0)
