@@ -15,8 +15,10 @@ batch of synthetic input.  Workloads (BASELINE.json configs):
   t2i1024 config 2: 4 x 1024^2 images (4 x 4096 tokens), Wan-1.3B-shaped, SP = 1 per rank;
           N > 1 runs N independent image batches (replicas, "scaling": "weak")
 The metric is BASELINE.json's "DiT step ms & attn TFLOPS (% BF16 peak)": `value` is the DiT
-step time (ms, device-timed with CUDA events on the context's stream, max over ranks);
-attention TFLOPS and its fraction of the measured BF16 peak ride in `roofline`.
+step time (ms, device-timed with CUDA events on the context's stream, max over ranks; the timed
+steps carry only per-step events, whose spread gives `step_cv`); attention TFLOPS and its fraction
+of the measured BF16 peak ride in `roofline`, from per-kernel events of --prof-steps extra steps
+run after the timed region.
 Inputs are far larger than L2 (weights 19.7 GB / 2.6 GB, activations > 1 GB), so no explicit
 L2 flush is needed between timed steps ("l2": "inputs larger than L2" in config).
 
@@ -246,7 +248,7 @@ def run_gpu(args, rank, world, local_rank):
         pass
     mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed,
                            cross_attn=shape.cross_attn, text_len=shape.text_len, text_dim=shape.text_dim)
-    total_steps = max(50, args.warmup + args.steps + 1)
+    total_steps = max(50, args.warmup + args.steps + args.prof_steps + 1)
     cfg = CFG_SCALE.get(args.workload, 0.0)
     nb = 2 if cfg > 0 else 1
 
@@ -279,7 +281,7 @@ def run_gpu(args, rank, world, local_rank):
     reqs = submit_all()
     if args.warmup:
         ctx.run_steps(reqs, ranks, args.warmup)
-    ctx.profile(True, True)
+    ctx.profile(2, True)  # step events only: the timed steps carry no per-kernel events
     clocks = ClockSampler(local_rank) if rank == 0 else None
     barrier()
     if clocks:
@@ -294,8 +296,14 @@ def run_gpu(args, rank, world, local_rank):
     assert done == args.steps, f"ran {done} of {args.steps} steps"
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     ms_step = ms_total / args.steps
+    step_ms = ctx.stats().get("step_ms", [])
+    launches = ctx.stats().get("launches", 0)
+    # per-kernel-class breakdown (attention / GEMM TFLOP/s, roofline) from separate profiled
+    # steps, so the per-kernel events never sit inside the timed region
+    ctx.profile(1, True)
+    ctx.run_steps(reqs, ranks, args.prof_steps)
     st = ctx.stats()
-    ctx.profile(False, False)
+    ctx.profile(0, False)
     for q in reqs:
         ctx.release(q)
 
@@ -341,11 +349,11 @@ def run_gpu(args, rank, world, local_rank):
     rows = nb * sum(seqlens) / p
     cross_gemm = 4 * rows * shape.dim ** 2 if shape.cross_attn else 0  # cross q and o projections
     gemm_flops = shape.layers * (costmodel.gemm_flops_per_block(rows, shape.dim, shape.ffn) + cross_gemm)
-    gemm_tflops = gemm_flops * args.steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    gemm_tflops = gemm_flops * args.prof_steps / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
     cross_attn_flops = 4 * rows * shape.text_len * shape.dim if shape.cross_attn else 0
     step_flops = shape.layers * (costmodel.gemm_flops_per_block(rows, shape.dim, shape.ffn) + cross_gemm + af
                                  + cross_attn_flops)
-    breakdown = {k: round(v["ms"] / args.steps, 3) for k, v in st.items() if isinstance(v, dict)}
+    breakdown = {k: round(v["ms"] / args.prof_steps, 3) for k, v in st.items() if isinstance(v, dict)}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -377,7 +385,10 @@ def run_gpu(args, rank, world, local_rank):
         "gemm_tflops": round(gemm_tflops, 1),
         "step_tflops": round(step_flops / (ms_step * 1e-3) / 1e12, 1),
         "breakdown_ms_per_step": breakdown,
-        "gpu_launches": int(st.get("launches", 0)),
+        "breakdown_steps": args.prof_steps,
+        "step_ms_each": [round(x, 3) for x in step_ms],
+        "step_cv": round(float(np.std(step_ms) / np.mean(step_ms)), 5) if len(step_ms) > 1 else None,
+        "gpu_launches": int(launches),
         "e2e": {"value": round(e2e_v, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": lat_bytes, "steps": e2e_steps,
                 "how": "wall clock around gs_submit(host latent) + gs_run_steps(k=1) + "
@@ -400,6 +411,8 @@ def main():
     ap.add_argument("--workload", default="t2v720", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--prof-steps", type=int, default=1,
+                    help="extra per-kernel-profiled steps after the timed region (breakdown, roofline)")
     ap.add_argument("--ref-tokens", type=int, default=1200,
                     help="token budget of the oracle sample (bounded CPU time)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -146,9 +146,11 @@ int gs_read_latent(gs_ctx* ctx, gs_req req, float* host, size_t nfloats);
 int gs_release(gs_ctx* ctx, gs_req req);
 
 /* ------------------------------------------------------------------ measurement */
-/* Enable per-kernel-class CUDA-event timing inside gs_run_steps (events on the launching
- * stream); gs_stats writes a JSON object {"class": {"ms": total, "n": launches}, ...,
- * "a2a_peer": exchanges run as peer stores, "a2a_plan": exchanges run as transfer plans,
+/* enable = 1: per-kernel-class and per-step CUDA-event timing inside gs_run_steps (events on the
+ * launching stream); 2: per-step events only (two per step, no per-kernel events); 0: off.
+ * gs_stats writes a JSON object {"class": {"ms": total, "n": launches}, ...,
+ * "step_ms": [device time of each profiled step], "a2a_peer": exchanges run as peer stores,
+ * "a2a_plan": exchanges run as transfer plans,
  * "launches": total kernel launches} accumulated since the last reset (a2a counts: since init). */
 int gs_profile(gs_ctx* ctx, int enable, int reset);
 int gs_stats(gs_ctx* ctx, char* json, size_t len);

@@ -1393,9 +1393,23 @@ int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int n
     int stop = 0;
     rc = agree_stop(c, P, flag, &stop);
     if (rc != GS_OK || stop) break;
+    cudaEvent_t s0 = nullptr, s1 = nullptr;
+    if (c->prof_steps) {
+      s0 = get_event(c);
+      s1 = get_event(c);
+      cudaEventRecord(s0, c->stream);
+    }
     rc = run_one_step(c, P, mine);
+    if (c->prof_steps) cudaEventRecord(s1, c->stream);
     if (rc != GS_OK) break;
     cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (c->prof_steps) {  // whole-step device time (gs_stats "step_ms"): the step-time CV of §8(d)
+      float ms = 0;
+      cudaEventElapsedTime(&ms, s0, s1);
+      c->step_ms.push_back(ms);
+      c->event_pool.push_back(s0);
+      c->event_pool.push_back(s1);
+    }
     if (e != cudaSuccess) {
       rc = fail(c, GS_ECUDA, "step failed: %s", cudaGetErrorString(e));
       break;
@@ -1547,9 +1561,11 @@ int gs_release(gs_ctx* c, gs_req id) {
 
 int gs_profile(gs_ctx* c, int enable, int reset) {
   if (!c) return GS_EINVAL;
-  c->prof = enable != 0;
+  c->prof = enable == 1;
+  c->prof_steps = enable == 1 || enable == 2;
   if (reset) {
     c->prof_tab.clear();
+    c->step_ms.clear();
     c->launches = 0;
   }
   return GS_OK;
@@ -1563,6 +1579,13 @@ int gs_stats(gs_ctx* c, char* json, size_t len) {
     snprintf(buf, sizeof buf, "\"%s\": {\"ms\": %.6f, \"n\": %lld}, ", kv.first.c_str(), kv.second.ms, kv.second.n);
     s += buf;
   }
+  s += "\"step_ms\": [";
+  for (size_t i = 0; i < c->step_ms.size(); ++i) {
+    char sb[32];
+    snprintf(sb, sizeof sb, "%s%.4f", i ? ", " : "", c->step_ms[i]);
+    s += sb;
+  }
+  s += "], ";
   char buf[160];
   snprintf(buf, sizeof buf, "\"a2a_peer\": %lld, \"a2a_plan\": %lld, \"launches\": %lld}", c->a2a_peer,
            c->a2a_plan, c->launches);

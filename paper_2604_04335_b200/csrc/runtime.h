@@ -105,10 +105,12 @@ struct gs_ctx {
   std::mutex table_mu;  // guards reqs
   std::mutex run_mu;    // one run / resume at a time
   // measurement
-  bool prof = false;
+  bool prof = false;        // per-kernel-class events (gs_profile enable = 1)
+  bool prof_steps = false;  // per-step events (enable = 1 or 2)
   std::map<std::string, gs::Prof> prof_tab;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
   std::vector<cudaEvent_t> event_pool;
+  std::vector<float> step_ms;       // device time of each profiled step (gs_stats "step_ms")
   long long launches = 0;
   cudaEvent_t ev_order = nullptr;   // debug entry points: order after the legacy stream
   // caching allocator for per-request state (latent shards, text caches): released blocks are
