@@ -233,6 +233,10 @@ int gs_debug_block(gs_ctx* ctx, int model, int layer, float* x, int nreq, const 
  * head 0 when the environment has GS_ATTN_TRACE=1: [2 CTAs][16 events][32 KV tiles][2 softmax
  * groups]; n <= 2048 entries to host, -1 if larger. */
 int gs_debug_attention_trace(unsigned long long* host, size_t n);
+/* Development aid (GS_ATTN_TRACE=1): per attention CTA (linear id blockIdx.y * gridDim.x +
+ * blockIdx.x < 8192) of the last launch: [entry globaltimer ns, first S issued (leader CTAs),
+ * exit, SM id]; n <= 32768 entries to host, -1 if larger. */
+int gs_debug_attention_ctatime(unsigned long long* host, size_t n);
 /* Time embedding of nreq timesteps: e0 [nreq, D], e [nreq, 6D] fp32 (host outputs). */
 int gs_debug_time_embed(gs_ctx* ctx, int model, int nreq, const float* t, float* e0, float* e);
 

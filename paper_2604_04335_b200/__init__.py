@@ -74,6 +74,7 @@ _SIG = {
     "gs_debug_block": [_P, _I, _I, _FP, _I, _IP, _IP, _IP, _FP, _P],
     "gs_debug_time_embed": [_P, _I, _I, _FP, _FP, _FP],
     "gs_debug_attention_trace": [_P, ctypes.c_size_t],
+    "gs_debug_attention_ctatime": [_P, ctypes.c_size_t],
     "gs_plan_a2a": [_I, _I, _I, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP,
                     ctypes.POINTER(ctypes.c_longlong)],
     "gs_plan_reshard": [_I, _I, _IP, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP],
@@ -347,6 +348,13 @@ class Context:
         buf = np.zeros(2 * 16 * 64, dtype=np.uint64)
         self._ck(self._lib.gs_debug_attention_trace(buf.ctypes.data_as(ctypes.c_void_p), buf.size))
         return buf.reshape(2, 16, 32, 2)[cta]
+
+    def debug_attention_ctatime(self, n_ctas):
+        """[n_ctas, 4] per-CTA (entry ns, first-S ns, exit ns, SM id) of the last attention launch
+        (needs GS_ATTN_TRACE=1 at process start)."""
+        buf = np.zeros(n_ctas * 4, dtype=np.uint64)
+        self._ck(self._lib.gs_debug_attention_ctatime(buf.ctypes.data_as(ctypes.c_void_p), buf.size))
+        return buf.reshape(n_ctas, 4)
 
     def debug_time_embed(self, model, t, dim):
         e0 = np.zeros((len(t), dim), np.float32)

@@ -29,6 +29,19 @@
 namespace gs {
 // Development trace (GS_ATTN_TRACE=1): clock64 stamps of CTA (0,0) for the first 32 KV tiles.
 __device__ unsigned long long g_attn_trace[2 * 16 * 64];  // [CTA 0 / its pair peer][event][tile][group]
+// Development trace (GS_ATTN_TRACE=1): per CTA (linear id < 8192) globaltimer at entry / after the
+// prologue (first S issued) / exit, and the SM id -- per-CTA overhead and inter-CTA gaps.
+__device__ unsigned long long g_attn_ctatime[8192 * 4];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 namespace {
 #define TRACE_EV(ev, w, j) \
   if (TRACE && blockIdx.x < 2 && blockIdx.y == 0 && (j) < 32) \
@@ -128,6 +141,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                    const __grid_constant__ SeqTable tab, float scale_log2,
                    const __grid_constant__ OScatter osc) {
   using C = Cfg<HD, PAIR>;
+  const unsigned cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
+  if (TRACE && threadIdx.x == 0 && cta_lin < 8192) {
+    g_attn_ctatime[cta_lin * 4 + 0] = gtimer();
+    g_attn_ctatime[cta_lin * 4 + 3] = smid();
+  }
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -301,6 +319,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       mbar_wait_spin(&kfull[0], 0);
       tc_fence_after();
+      if (TRACE && cta_lin < 8192) g_attn_ctatime[cta_lin * 4 + 1] = gtimer();
       issue_s(0, 0);
       issue_s(1, 0);
       commit(&kempty[0]);
@@ -450,6 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     else
       tmem_dealloc(tmem, 512);
   }
+  if (TRACE && threadIdx.x == 0 && cta_lin < 8192) g_attn_ctatime[cta_lin * 4 + 2] = gtimer();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -916,6 +936,11 @@ cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, i
 }
 
 }  // namespace gs
+
+extern "C" int gs_debug_attention_ctatime(unsigned long long* host, size_t n) {
+  if (!host || n > sizeof(gs::g_attn_ctatime) / 8) return -1;
+  return cudaMemcpyFromSymbol(host, gs::g_attn_ctatime, n * 8) == cudaSuccess ? 0 : -4;
+}
 
 extern "C" int gs_debug_attention_trace(unsigned long long* host, size_t n) {
   if (!host || n > sizeof(gs::g_attn_trace) / 8) return -1;
