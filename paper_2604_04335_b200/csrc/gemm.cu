@@ -3,11 +3,12 @@
 //   (bias; GELU-tanh; fp32 gated residual x += g (.) (acc + b); Euler z += dsig (acc + b)).
 //
 // Design (B200-first):
-//   * persistent kernel, one CTA per SM, static tile schedule (tile t = blockIdx.x + i*grid);
-//   * warp 0: TMA producer (128B-swizzled K-major tiles, 4-stage mbarrier ring);
-//   * warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=16);
-//   * warps 2..5: epilogue (tcgen05.ld 32x32b -> registers -> fused epilogue -> global);
-//   * two TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps the
+//   * persistent CTA pairs (cta_group::2), static tile schedule (tile t = pair + i*npairs);
+//   * warp 0: TMA producer (128B-swizzled K-major tiles, 5-7-stage mbarrier ring);
+//   * warp 1: TMEM allocator + single-thread tcgen05.mma issuer (leader CTA, M=256, N=BN, K=16);
+//   * warps 2..5: epilogue (tcgen05.ld 32x32b -> registers -> fused epilogue -> global; fp32
+//     read-modify-write epilogues stream x through shared memory by TMA load / store);
+//   * two TMEM accumulators (2 x BN columns) so the epilogue of tile i overlaps the
 //     main loop of tile i+1.
 // Bit-exactness across M (SURVEY.md §8(a) invariant 1): no split-K, no atomics, the same
 // MMA shape and K order for every tile, each output row depends only on its own A row.
@@ -42,12 +43,35 @@ constexpr int BK = 64;
 constexpr int A_BYTES = BM * BK * 2;        // 16 KB
 constexpr int THREADS = 192;
 constexpr uint32_t TMEM_COLS = 512;         // 2 accumulators x (up to) 256 columns
-template <int BN>
+// Epilogues.  tcgen05.ld gives thread = row, 32 fp32 columns per load ("chunk").
+//  * bf16 / fp32 outputs (write-only): each warp re-distributes its 32 rows x 32 columns through a
+//    shared-memory transpose buffer so that 8 lanes cover one row's 32 columns and every global
+//    store is a contiguous row segment.  Row pitch 36 floats (144 B): the float4 writes (lane =
+//    row) and reads (8 lanes per row) are conflict-free per quarter-warp.
+//  * fp32 read-modify-write (gated residual x, ungated residual, Euler latent z): the 32 x 32
+//    chunk of x streams through a per-warp ring of XR_NB 4 KB shared-memory buffers by TMA
+//    (128B-swizzled boxes, XR_LOOK chunks ahead), each thread updates its own row in place, and a
+//    TMA store writes the chunk back.  No thread ever waits on a global load: the epilogue of a
+//    short-K GEMM (config-2 O-proj, K = 1536) was latency-bound on its x loads at ~20 us per tile
+//    against a ~6.5 us main loop (ncu: long-scoreboard stalls).
+// The arithmetic per element is the same in both paths.
+constexpr int EP_PITCH = 36;
+constexpr int EP_WARP_BYTES = 32 * EP_PITCH * 4;
+constexpr int EP_BYTES = 4 * EP_WARP_BYTES;  // 4 epilogue warps
+constexpr int XR_NB = 4, XR_LOOK = 2;        // ring depth, load lookahead (chunks)
+constexpr int XR_CHUNK = 32 * 32 * 4;        // 4 KB
+constexpr int XR_BYTES = 4 * XR_NB * XR_CHUNK;
+constexpr int BAR_BYTES = 1024;              // barriers + TMEM slot; keeps the ring 1024-aligned
+template <int EPI>
+constexpr bool kEpiReadsOut = EPI == EPI_RESID_F32 || EPI == EPI_ADD_F32 || EPI == EPI_EULER_F32;
+
+template <int BN, bool RMW>
 struct GCfg {
-  static constexpr int STAGES = BN == 256 ? 6 : 7;
+  static constexpr int STAGES = RMW ? 5 : (BN == 256 ? 6 : 7);
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the W tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + BAR_BYTES + (RMW ? XR_BYTES : EP_BYTES);
+  static_assert(SMEM_BYTES <= 232448, "shared memory");
 };
 
 __device__ __forceinline__ float gelu_tanh_f(float u) {
@@ -55,9 +79,67 @@ __device__ __forceinline__ float gelu_tanh_f(float u) {
   return 0.5f * u * (1.0f + tanh_approx(k0 * (u + k1 * u * u * u)));
 }
 
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+  a.x += b.x;
+  a.y += b.y;
+  a.z += b.z;
+  a.w += b.w;
+}
+
+// Write-only epilogue of one 32 x 32 chunk of a warp's rows (row0 .. row0 + 31), columns
+// col0 .. col0 + 31, through the warp's transpose buffer at shared address tw.
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int row, int col0,
+__device__ __forceinline__ void epilogue_chunk(uint32_t tw, const uint32_t (&r)[32], int row0, int col0, int M,
                                                const EpiParams& ep) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    sts_v4(tw + (lane * EP_PITCH + 4 * q) * 4,
+           make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                       __uint_as_float(r[4 * q + 3])));
+  __syncwarp();
+  const int rsub = lane >> 3, c4 = lane & 7;
+  const int col = col0 + 4 * c4;
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = lds_v4(tw + ((4 * i + rsub) * EP_PITCH + 4 * c4) * 4);
+  __syncwarp();  // the buffer is rewritten by the next chunk
+  if (ep.bias != nullptr) {
+    const uint2 braw = __ldg(reinterpret_cast<const uint2*>(ep.bias + col));
+    const float2 b01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&braw.x));
+    const float2 b23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&braw.y));
+    const float4 b = make_float4(b01.x, b01.y, b23.x, b23.y);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) add4(v[i], b);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int row = row0 + 4 * i + rsub;
+    if (row >= M) continue;
+    if constexpr (EPI == EPI_F32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col) = v[i];
+    } else {
+      float4 f = v[i];
+      if constexpr (EPI == EPI_GELU_BF16) {
+        f.x = gelu_tanh_f(f.x);
+        f.y = gelu_tanh_f(f.y);
+        f.z = gelu_tanh_f(f.z);
+        f.w = gelu_tanh_f(f.w);
+      }
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col) =
+          make_uint2(pack_bf16x2(f.x, f.y), pack_bf16x2(f.z, f.w));
+    }
+  }
+}
+
+// Read-modify-write epilogue of one chunk: this thread's row lives in the 128B-swizzled 32 x 32
+// fp32 box at shared address xb (16-byte unit j of row l at l * 128 + ((j ^ (l & 7)) << 4));
+// updated in place for the TMA store.
+template <int EPI>
+__device__ __forceinline__ void rmw_chunk(uint32_t xb, const uint32_t (&r)[32], int col0, int req,
+                                          const EpiParams& ep) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t rowb = xb + lane * 128;
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -75,67 +157,31 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], int row,
       }
     }
   }
-  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
-    uint32_t pk[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      float a = v[2 * i], b = v[2 * i + 1];
-      if constexpr (EPI == EPI_GELU_BF16) {
-        a = gelu_tanh_f(a);
-        b = gelu_tanh_f(b);
-      }
-      pk[i] = pack_bf16x2(a, b);
-    }
-    uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(ep.out) +
-                                          static_cast<size_t>(row) * ep.ldo + col0);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-  } else if constexpr (EPI == EPI_F32) {
-    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
-                                            static_cast<size_t>(row) * ep.ldo + col0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  } else if constexpr (EPI == EPI_RESID_F32) {
-    const int req = ep.row_req[row];
-    const float4* ga = reinterpret_cast<const float4*>(ep.gate_a + col0);
-    const float4* gb =
-        reinterpret_cast<const float4*>(ep.gate_b + static_cast<size_t>(req) * ep.gate_b_stride + col0);
-    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
-                                            static_cast<size_t>(row) * ep.ldo + col0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 a = __ldg(ga + q), b = __ldg(gb + q), x = dst[q];
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t addr = rowb + ((q ^ (lane & 7)) << 4);
+    float4 x = lds_v4(addr);
+    if constexpr (EPI == EPI_RESID_F32) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(ep.gate_a + col0) + q);
+      const float4 b =
+          __ldg(reinterpret_cast<const float4*>(ep.gate_b + static_cast<size_t>(req) * ep.gate_b_stride + col0) + q);
       x.x += (a.x + b.x) * v[4 * q + 0];
       x.y += (a.y + b.y) * v[4 * q + 1];
       x.z += (a.z + b.z) * v[4 * q + 2];
       x.w += (a.w + b.w) * v[4 * q + 3];
-      dst[q] = x;
-    }
-  } else if constexpr (EPI == EPI_ADD_F32) {
-    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
-                                            static_cast<size_t>(row) * ep.ldo + col0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 x = dst[q];
+    } else if constexpr (EPI == EPI_ADD_F32) {
       x.x += v[4 * q + 0];
       x.y += v[4 * q + 1];
       x.z += v[4 * q + 2];
       x.w += v[4 * q + 3];
-      dst[q] = x;
-    }
-  } else if constexpr (EPI == EPI_EULER_F32) {
-    const float ds = ep.dsig[ep.row_req[row]];
-    float4* dst = reinterpret_cast<float4*>(static_cast<float*>(ep.out) +
-                                            static_cast<size_t>(row) * ep.ldo + col0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float4 x = dst[q];
+    } else {  // EPI_EULER_F32
+      const float ds = ep.dsig[req];
       x.x += ds * v[4 * q + 0];
       x.y += ds * v[4 * q + 1];
       x.z += ds * v[4 * q + 2];
       x.w += ds * v[4 * q + 3];
-      dst[q] = x;
     }
+    sts_v4(addr, x);
   }
 }
 
@@ -158,8 +204,10 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb
 template <int EPI, int BN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   int M, int N, int K, const __grid_constant__ EpiParams ep) {
-  constexpr int STAGES = GCfg<BN>::STAGES, STAGE_BYTES = GCfg<BN>::STAGE_BYTES;
+                   const __grid_constant__ CUtensorMap tmX, int M, int N, int K,
+                   const __grid_constant__ EpiParams ep) {
+  constexpr bool RMW = kEpiReadsOut<EPI>;
+  constexpr int STAGES = GCfg<BN, RMW>::STAGES, STAGE_BYTES = GCfg<BN, RMW>::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -167,7 +215,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   uint64_t* empty = bars + STAGES;           // [STAGES] per CTA (multicast commit)
   uint64_t* tfull = bars + 2 * STAGES;       // [2] per CTA (multicast commit)
   uint64_t* tempty = bars + 2 * STAGES + 2;  // [2] leader's: 4 epilogue warps x 2 CTAs
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* xfull = bars + 2 * STAGES + 4;   // [4 warps][XR_NB] (RMW epilogues)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + 4 * XR_NB);
+  uint8_t* ep_smem = smem + STAGES * STAGE_BYTES + BAR_BYTES;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
@@ -184,11 +234,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 8);
     }
+    for (int s = 0; s < 4 * XR_NB; ++s) mbar_init(&xfull[s], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if constexpr (RMW) tma_prefetch(&tmX);
   }
   if (warp == 1) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
   tc_fence_before();
@@ -241,9 +293,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
     }
   } else {
-    // epilogue (both CTAs): warps 2..5 -> TMEM lane quarter (warp % 4) of this CTA's 128 rows
-    const int quarter = warp & 3;
+    // epilogue (both CTAs): warps 2..5 -> TMEM lane quarter (warp % 4) of this CTA's 128 rows.
+    // TMEM loads run one 32-column chunk ahead of the global-memory work; the accumulator is
+    // handed back to the MMA issuer as soon as its last chunk is in registers.
+    const int quarter = warp & 3, we = warp - 2;
+    const uint32_t tw = smem_u32(ep_smem) + we * EP_WARP_BYTES;              // write-only path
+    const uint32_t ring = smem_u32(ep_smem) + we * XR_NB * XR_CHUNK;         // RMW path
+    uint64_t* wxfull = xfull + we * XR_NB;
     const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    // RMW load cursor: the (tile, chunk) sequence this warp will consume, XR_LOOK chunks ahead.
+    int lt = pair, lc = 0, lnch = 0, lcol = 0, lrow = 0;
+    uint32_t nload = 0, ncons = 0;
+    auto load_tile = [&]() {
+      if (lt < num_tiles) {
+        int mb, nb;
+        tile_coords(lt, num_m, num_n, mb, nb);
+        lnch = min(BN, N - nb * BN) / 32;
+        lcol = nb * BN;
+        lrow = mb * PM + rank * BM + quarter * 32;
+      }
+    };
+    auto issue_load = [&]() {  // next chunk of the cursor into ring slot nload % XR_NB
+      if (lt >= num_tiles) return;
+      if (lane == 0) {
+        const int b = nload % XR_NB;
+        // slot b last held chunk nload - XR_NB, whose store is older than the newest
+        // XR_NB - XR_LOOK - 1 committed stores
+        bulk_wait_group_read<XR_NB - XR_LOOK - 1>();
+        mbar_arrive_expect_tx(&wxfull[b], XR_CHUNK);
+        tma_load_2d(&tmX, &wxfull[b], ep_smem + (we * XR_NB + b) * XR_CHUNK, lcol + lc * 32, lrow);
+      }
+      ++nload;
+      if (++lc == lnch) {
+        lc = 0;
+        lt += npairs;
+        load_tile();
+      }
+    };
+    if constexpr (RMW) {
+      load_tile();
+      for (int i = 0; i < XR_LOOK; ++i) issue_load();
+    }
+    auto do_chunk = [&](const uint32_t (&r)[32], int row0, int col0, int req) {
+      if constexpr (RMW) {
+        issue_load();
+        const int b = ncons % XR_NB;
+        mbar_wait(&wxfull[b], (ncons / XR_NB) & 1);
+        ++ncons;
+        const uint32_t xb = ring + b * XR_CHUNK;
+        rmw_chunk<EPI>(xb, r, col0, req, ep);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmX, ep_smem + (we * XR_NB + b) * XR_CHUNK, col0, row0);
+          bulk_commit_group();
+        }
+      } else {
+        epilogue_chunk<EPI>(tw, r, row0, col0, M, ep);
+      }
+    };
     int it = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
       int mb, nb;
@@ -252,21 +360,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
-      const int row = mb * PM + rank * BM + quarter * 32 + lane;
+      const int row0 = mb * PM + rank * BM + quarter * 32;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * BN;
+      const int nch = min(BN, N - nb * BN) / 32;  // N % 32 == 0
+      int req = 0;
+      if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_EULER_F32)
+        if (row0 + lane < M) req = __ldg(ep.row_req + row0 + lane);
+      uint32_t ra[32], rb[32];
+      GS_TMEM_LD32(tbase, ra);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int col0 = nb * BN + c * 32;
-        if (col0 >= N) break;  // warp-uniform
-        uint32_t r[32];
-        GS_TMEM_LD32(tbase + c * 32, r);
-        tmem_ld_wait();
-        if (row < M) epilogue_chunk<EPI>(r, row, col0, ep);
+      for (int c = 0; c < nch; c += 2) {
+        GS_TMEM_LD_WAIT_REGS32(ra);
+        if (c + 1 < nch) GS_TMEM_LD32(tbase + (c + 1) * 32, rb);
+        if (c + 1 >= nch) {  // all of this accumulator is in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader + as * 8);
+        }
+        do_chunk(ra, row0, nb * BN + c * 32, req);
+        if (c + 1 < nch) {
+          GS_TMEM_LD_WAIT_REGS32(rb);
+          if (c + 2 < nch) GS_TMEM_LD32(tbase + (c + 2) * 32, ra);
+          if (c + 2 >= nch) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + as * 8);
+          }
+          do_chunk(rb, row0, nb * BN + (c + 1) * 32, req);
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader + as * 8);
     }
+    if constexpr (RMW)
+      if (lane == 0) bulk_wait_group_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -280,20 +405,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 template <int EPI, int BN>
 cudaError_t launch_bn(int M, int N, int K, const void* A, int lda, const void* W, int ldw,
                       const EpiParams& ep, int num_sms, cudaStream_t stream) {
-  CUtensorMap ta, tb;
+  constexpr bool RMW = kEpiReadsOut<EPI>;
+  CUtensorMap ta, tb, tx;
   if (!make_tma_2d_bf16(&ta, A, K, M, static_cast<uint64_t>(lda) * 2, BK, BM)) return cudaErrorInvalidValue;
   if (!make_tma_2d_bf16(&tb, W, K, N, static_cast<uint64_t>(ldw) * 2, BK, BN / 2)) return cudaErrorInvalidValue;
+  if (RMW) {
+    if (ep.ldo % 4 || (reinterpret_cast<uintptr_t>(ep.out) & 15)) return cudaErrorInvalidValue;
+    if (!make_tma_2d_f32(&tx, ep.out, N, M, static_cast<uint64_t>(ep.ldo) * 4, 32, 32)) return cudaErrorInvalidValue;
+  } else {
+    tx = ta;  // unused
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GCfg<BN>::SMEM_BYTES);
+                                         GCfg<BN, RMW>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int tiles = ((M + PM - 1) / PM) * ((N + BN - 1) / BN);
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   const int grid = 2 * pairs;  // clusters of 2 (CTA pairs on one TPC)
-  gemm_tc_kernel<EPI, BN><<<grid, THREADS, GCfg<BN>::SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+  gemm_tc_kernel<EPI, BN><<<grid, THREADS, GCfg<BN, RMW>::SMEM_BYTES, stream>>>(ta, tb, tx, M, N, K, ep);
   return cudaGetLastError();
 }
 

@@ -65,6 +65,8 @@ def main():
     ap.add_argument("--torch", action="store_true", help="also time torch SDPA / matmul yardsticks")
     ap.add_argument("--only", default=None, help="substring filter on the case label")
     ap.add_argument("--lib", default=None, help="load this libgs.so instead of the in-tree one (A/B)")
+    ap.add_argument("--epi", default="bf16", choices=["bf16", "gelu", "resid"],
+                    help="GEMM epilogue: bf16 out, GELU bf16 out, or fp32 gated residual x += g (acc + b)")
     a = ap.parse_args()
     if a.lib:
         gs.load(a.lib)
@@ -111,8 +113,17 @@ def main():
             A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             W = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
             b = torch.zeros(N, device="cuda").to(torch.bfloat16)
-            out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-            ms = timeit(ctx, lambda: ctx.debug_gemm(gs.EPI_BF16, M, N, K, A, W, b, out), a.reps)
+            if a.epi == "resid":
+                out = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+                ga = torch.rand(N, device="cuda")
+                gb = torch.rand(4, N, device="cuda")
+                rr = (torch.arange(M, device="cuda", dtype=torch.int32) * 4) // M
+                fn = lambda: ctx.debug_gemm(gs.EPI_RESID_F32, M, N, K, A, W, b, out, ga, gb, N, rr)
+            else:
+                out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+                e = gs.EPI_GELU_BF16 if a.epi == "gelu" else gs.EPI_BF16
+                fn = lambda: ctx.debug_gemm(e, M, N, K, A, W, b, out)
+            ms = timeit(ctx, fn, a.reps)
             tf = 2 * M * N * K / ms / 1e9
             line = f"gemm {label:24s} {ms:9.3f} ms {tf:8.1f} TFLOP/s {tf / PEAK:6.1%} of peak"
             if a.torch:
