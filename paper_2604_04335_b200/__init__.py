@@ -90,6 +90,7 @@ def load(path=LIB_PATH):
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("GS_LIB", path)  # A/B runs against another build (tools/*_ab.sh)
     if not os.path.exists(path):
         raise RuntimeError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = ctypes.CDLL(path)

@@ -48,19 +48,10 @@ constexpr int kWarpRowsPerCta = 8;
 // ------------------------------------------------------------------ LN + modulate
 // VPL = float4 (LN) / uint4 per tensor (qk) per thread: sized exactly from D so the registers of
 // one row stay small and several CTAs share an SM (occupancy hides the DRAM latency of the row).
+// Each row op is split into a load-and-sum half and a finish half (a persistent variant that
+// streamed rows through shared memory by bulk copies reused them; it was slower, notes r01g).
 template <int TPR, int VPL>
-__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, TPR == 32 ? 4 : 1)
-    ln_modulate_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ sh_a,
-                       const float* __restrict__ sh_b, const float* __restrict__ sc_a,
-                       const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
-                       float eps, __nv_bfloat16* __restrict__ out) {
-  __shared__ float red[4];
-  const long long row = TPR == 32 ? blockIdx.x * (long long)kWarpRowsPerCta + (threadIdx.x >> 5) : blockIdx.x;
-  const int tid = TPR == 32 ? (threadIdx.x & 31) : threadIdx.x;
-  if (TPR == 32 && row >= M) return;
-  const int nv = D >> 2;
-  const float4* xr = reinterpret_cast<const float4*>(x + row * D);
-  float4 v[VPL];
+__device__ __forceinline__ float ln_load(const float4* xr, int tid, int nv, float4 (&v)[VPL]) {
   float s = 0.f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
@@ -70,6 +61,17 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
       s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
     }
   }
+  return s;
+}
+
+template <int TPR, int VPL, bool STAGED = false>
+__device__ __forceinline__ void ln_finish(const float4 (&v)[VPL], float s, long long row, int tid, int D,
+                                          const float* __restrict__ sh_a, const float* __restrict__ sh_b,
+                                          const float* __restrict__ sc_a, const float* __restrict__ sc_b,
+                                          int b_stride, const int* __restrict__ row_req, float eps,
+                                          __nv_bfloat16* __restrict__ out, float* red,
+                                          const float4* shs = nullptr, const float4* scs = nullptr) {
+  const int nv = D >> 2;
   const float mean = row_sum<TPR>(s, red) / D;
   float q = 0.f;
 #pragma unroll
@@ -91,14 +93,73 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
   for (int i = 0; i < VPL; ++i) {
     const int c = tid + i * TPR;
     if (c < nv) {
-      const float4 a1 = __ldg(sha + c), b1 = __ldg(shb + c), a2 = __ldg(sca + c), b2 = __ldg(scb + c);
-      const float y0 = (v[i].x - mean) * rstd * (1.f + (a2.x + b2.x)) + (a1.x + b1.x);
-      const float y1 = (v[i].y - mean) * rstd * (1.f + (a2.y + b2.y)) + (a1.y + b1.y);
-      const float y2 = (v[i].z - mean) * rstd * (1.f + (a2.z + b2.z)) + (a1.z + b1.z);
-      const float y3 = (v[i].w - mean) * rstd * (1.f + (a2.w + b2.w)) + (a1.w + b1.w);
+      float4 sh, sc;  // sh_a + sh_b[r], 1 + (sc_a + sc_b[r]): from the CTA's shared copy when staged
+      if (STAGED) {
+        sh = shs[c];
+        sc = scs[c];
+      } else {
+        const float4 a1 = __ldg(sha + c), b1 = __ldg(shb + c), a2 = __ldg(sca + c), b2 = __ldg(scb + c);
+        sh = make_float4(a1.x + b1.x, a1.y + b1.y, a1.z + b1.z, a1.w + b1.w);
+        sc = make_float4(1.f + (a2.x + b2.x), 1.f + (a2.y + b2.y), 1.f + (a2.z + b2.z), 1.f + (a2.w + b2.w));
+      }
+      const float y0 = (v[i].x - mean) * rstd * sc.x + sh.x;
+      const float y1 = (v[i].y - mean) * rstd * sc.y + sh.y;
+      const float y2 = (v[i].z - mean) * rstd * sc.z + sh.z;
+      const float y3 = (v[i].w - mean) * rstd * sc.w + sh.w;
       __nv_bfloat162 p0 = __floats2bfloat162_rn(y0, y1), p1 = __floats2bfloat162_rn(y2, y3);
       o[c] = make_uint2(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1));
     }
+  }
+}
+
+template <int TPR, int VPL, int MINB>
+__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, MINB)
+    ln_modulate_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ sh_a,
+                       const float* __restrict__ sh_b, const float* __restrict__ sc_a,
+                       const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
+                       float eps, __nv_bfloat16* __restrict__ out) {
+  __shared__ float red[4];
+  if (TPR == 32) {
+    // Warp per row, 8 rows per CTA.  When the CTA's rows belong to one request (rows are request
+    // segments, so all but the boundary CTAs), the combined shift / 1 + scale vectors are formed
+    // once per CTA in shared memory: per row 2 shared-memory float4 reads per 4 elements instead
+    // of 4 L1 loads and 8 adds (the same fp32 operations, hence the same bits).  Three CTAs per SM
+    // (80 registers): at four (64) the row's 48 values spilled.  Config 2 (r01h, same-box A/B):
+    // 3.26 -> 2.72 ms per step, bit-identical.
+    __shared__ float4 s_sh[kWarpRowMaxD / 4], s_sc[kWarpRowMaxD / 4];
+    const long long row0 = blockIdx.x * (long long)kWarpRowsPerCta;
+    const long long row = row0 + (threadIdx.x >> 5);
+    const long long rlast = row0 + kWarpRowsPerCta - 1 < M ? row0 + kWarpRowsPerCta - 1 : M - 1;
+    const int tid = threadIdx.x & 31;
+    const int nv = D >> 2;
+    float4 v[VPL];
+    float s = 0.f;
+    if (row < M) s = ln_load<TPR, VPL>(reinterpret_cast<const float4*>(x + row * D), tid, nv, v);
+    const int r0 = row_req[row0];
+    const bool staged = r0 == row_req[rlast];
+    if (staged) {
+      const float4* sha = reinterpret_cast<const float4*>(sh_a);
+      const float4* sca = reinterpret_cast<const float4*>(sc_a);
+      const float4* shb = reinterpret_cast<const float4*>(sh_b + (long long)r0 * b_stride);
+      const float4* scb = reinterpret_cast<const float4*>(sc_b + (long long)r0 * b_stride);
+      for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+        const float4 a1 = __ldg(sha + c), b1 = __ldg(shb + c), a2 = __ldg(sca + c), b2 = __ldg(scb + c);
+        s_sh[c] = make_float4(a1.x + b1.x, a1.y + b1.y, a1.z + b1.z, a1.w + b1.w);
+        s_sc[c] = make_float4(1.f + (a2.x + b2.x), 1.f + (a2.y + b2.y), 1.f + (a2.z + b2.z), 1.f + (a2.w + b2.w));
+      }
+      __syncthreads();
+    }
+    if (row >= M) return;
+    if (staged)
+      ln_finish<TPR, VPL, true>(v, s, row, tid, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red, s_sh,
+                                s_sc);
+    else
+      ln_finish<TPR, VPL>(v, s, row, tid, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red);
+  } else {
+    const long long row = blockIdx.x;
+    float4 v[VPL];
+    const float s = ln_load<TPR, VPL>(reinterpret_cast<const float4*>(x + row * D), threadIdx.x, D >> 2, v);
+    ln_finish<TPR, VPL>(v, s, row, threadIdx.x, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red);
   }
 }
 
@@ -113,47 +174,35 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   }
 }
 
-// Element offset of (row, head h, element i0 of the head) in its pack chunk's destination: the
-// send layout [rows][H_j][d] at dest_off[j], or (peer mode) the full-batch row of the RECV buffer.
-__device__ __forceinline__ long long pack_offset(const PackParams& pk, long long row, int h, int i0, int d,
-                                                 int* jc_out, int& h0, int& h1) {
-  int jc = 0;
-  h0 = pk.head_off[0];
-  h1 = pk.head_off[1];
-#pragma unroll
-  for (int t = 1; t < 16; ++t) {
-    if (t < pk.ndest && h >= pk.head_off[t]) {
-      h0 = pk.head_off[t];
-      h1 = pk.head_off[t + 1];
-      jc = t;
-    }
+// Per-CTA lookup tables of the pack / RoPE mapping, built once per CTA instead of searched per
+// 8-element chunk (the qk kernel is instruction-bound: ncu issue-active 36% at 12% warps active):
+// head h -> pack chunk jc, heads in the chunk hn, head index within the chunk hr; RoPE pair slot ->
+// axis (0 = f, 1 = h, 2 = w).
+constexpr int kMaxHeads = 128;  // D <= 8192, d >= 64
+constexpr int kMaxSlots = 64;   // d / 2, d <= 128
+struct QkTables {
+  uint8_t jc[kMaxHeads], hn[kMaxHeads], hr[kMaxHeads], ax[kMaxSlots];
+};
+
+__device__ __forceinline__ void qk_tables_build(QkTables& t, const PackParams& pk, const RopeParams& rp, int H,
+                                                int half) {
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    int jc = 0;
+    for (int j = 1; j < pk.ndest; ++j)
+      if (h >= pk.head_off[j]) jc = j;
+    t.jc[h] = (uint8_t)jc;
+    t.hn[h] = (uint8_t)(pk.head_off[jc + 1] - pk.head_off[jc]);
+    t.hr[h] = (uint8_t)(h - pk.head_off[jc]);
   }
-  *jc_out = jc;
-  if (pk.peer) {
-    int sq = 0;
-#pragma unroll
-    for (int t = 1; t < 16; ++t)
-      if (t < pk.nseq && row >= pk.seq_lo[t]) sq = t;
-    return ((row + pk.row_delta[sq]) * (h1 - h0) + (h - h0)) * (long long)d + i0;
-  }
-  return pk.dest_off[jc] + (row * (h1 - h0) + (h - h0)) * (long long)d + i0;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) t.ax[j] = (uint8_t)rp.slot_axis[j];
+  __syncthreads();
 }
 
 template <int TPR, int VPL>
-__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, TPR == 32 ? 3 : 1)
-    qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
-                             const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
-                             float eps, const RopeParams rp, const PackParams pk,
-                             __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
-                             __nv_bfloat16* __restrict__ v_out) {
-  __shared__ float red[4];
-  const long long row = TPR == 32 ? blockIdx.x * (long long)kWarpRowsPerCta + (threadIdx.x >> 5) : blockIdx.x;
-  const int tid = TPR == 32 ? (threadIdx.x & 31) : threadIdx.x;
-  if (TPR == 32 && row >= M) return;
-  const int nv = D >> 3;  // uint4 chunks (8 elements) per q/k/v row
-  const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
-  uint4 qv[VPL], kv[VPL];
-  float sq = 0.f, sk = 0.f;
+__device__ __forceinline__ void qk_load(const uint4* src, int tid, int nv, uint4 (&qv)[VPL], uint4 (&kv)[VPL],
+                                        float& sq, float& sk) {
+  sq = 0.f;
+  sk = 0.f;
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     const int c = tid + i * TPR;
@@ -169,14 +218,39 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
             ((f[4] * f[4] + f[5] * f[5]) + (f[6] * f[6] + f[7] * f[7]));
     }
   }
+}
+
+// src = the row's q|k|v (global or a shared-memory stage); v is copied from src[2 nv + c].
+// Destination of (row, head h, element i0): the send layout [rows][H_j][d] at dest_off[j], or (peer
+// mode) row + row_delta[seq] of the receiving position's [rows_full][H_j][d] buffer.
+template <int TPR, int VPL>
+__device__ __forceinline__ void qk_finish(const QkTables& tb, const uint4* src, const uint4 (&qv)[VPL],
+                                          const uint4 (&kv)[VPL], float sq, float sk, long long row, int tid, int D,
+                                          int d, const __nv_bfloat16* __restrict__ g_q,
+                                          const __nv_bfloat16* __restrict__ g_k, float eps, const RopeParams& rp,
+                                          const PackParams& pk, __nv_bfloat16* __restrict__ q_out,
+                                          __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out,
+                                          float* red) {
+  const int nv = D >> 3;
   const float rq = rsqrtf(row_sum<TPR>(sq, red) / D + eps);
   const float rk = rsqrtf(row_sum<TPR>(sk, red) / D + eps);
 
   const int r = rp.row_req[row];
   const int tok = rp.row_tok[row];
   const int Ht = rp.req_grid[3 * r + 1], Wt = rp.req_grid[3 * r + 2];
-  const int pf = tok / (Ht * Wt), ph = (tok / Wt) % Ht, pw = tok % Wt;
   const int half = d >> 1;
+  const int pf = tok / (Ht * Wt), ph = (tok / Wt) % Ht, pw = tok % Wt;
+  const float2* cs_f = rp.cs_tab + (long long)pf * half;
+  const float2* cs_h = rp.cs_tab + (long long)ph * half;
+  const float2* cs_w = rp.cs_tab + (long long)pw * half;
+  long long prow = row;  // destination row
+  if (pk.peer) {
+    int sqi = 0;
+    for (int t = 1; t < pk.nseq; ++t)
+      if (row >= pk.seq_lo[t]) sqi = t;
+    prow = row + pk.row_delta[sqi];
+  }
+  const int lgd = __ffs(d) - 1;  // d in {64, 128}
   const uint4* gq = reinterpret_cast<const uint4*>(g_q);
   const uint4* gk = reinterpret_cast<const uint4*>(g_k);
 #pragma unroll
@@ -184,14 +258,16 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
     const int c = tid + i * TPR;
     if (c < nv) {
       const int e0 = c * 8;
-      const int h = e0 / d, i0 = e0 - h * d;
-      int jc = 0, h0 = 0, h1 = 0;
+      const int h = e0 >> lgd, i0 = e0 & (d - 1);
+      const int jc = tb.jc[h], hn = tb.hn[h], hr = tb.hr[h];
       __nv_bfloat16 *dq = q_out, *dk = k_out, *dv = v_out;
-      const long long o = pack_offset(pk, row, h, i0, d, &jc, h0, h1);
+      long long o = (prow * hn + hr) * (long long)d + i0;
       if (pk.peer) {
         dq = pk.dst_q[jc];
         dk = pk.dst_k[jc];
         dv = pk.dst_v[jc];
+      } else {
+        o += pk.dest_off[jc];
       }
       float fq[8], fk[8], wq[8], wk[8];
       unpack8(qv[i], fq);
@@ -202,9 +278,8 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
         const int slot = (i0 >> 1) + p;
-        const int ax = __ldg(rp.slot_axis + slot);
-        const int pa = ax == 0 ? pf : (ax == 1 ? ph : pw);
-        const float2 cs = __ldg(rp.cs_tab + (long long)pa * half + slot);
+        const int ax = tb.ax[slot];
+        const float2 cs = __ldg((ax == 0 ? cs_f : (ax == 1 ? cs_h : cs_w)) + slot);
         const float q0 = fq[2 * p] * rq * wq[2 * p], q1 = fq[2 * p + 1] * rq * wq[2 * p + 1];
         const float k0 = fk[2 * p] * rk * wk[2 * p], k1 = fk[2 * p + 1] * rk * wk[2 * p + 1];
         oq[p] = pack_bf16x2(q0 * cs.x - q1 * cs.y, q0 * cs.y + q1 * cs.x);
@@ -215,6 +290,26 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
       *reinterpret_cast<uint4*>(dv + o) = src[2 * nv + c];
     }
   }
+}
+
+template <int TPR, int VPL, int MINB>
+__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, MINB)
+    qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
+                             const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
+                             float eps, const RopeParams rp, const PackParams pk,
+                             __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
+                             __nv_bfloat16* __restrict__ v_out) {
+  __shared__ float red[4];
+  __shared__ QkTables tb;
+  qk_tables_build(tb, pk, rp, D / d, d >> 1);
+  const long long row = TPR == 32 ? blockIdx.x * (long long)kWarpRowsPerCta + (threadIdx.x >> 5) : blockIdx.x;
+  const int tid = TPR == 32 ? (threadIdx.x & 31) : threadIdx.x;
+  if (TPR == 32 && row >= M) return;
+  const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
+  uint4 qv[VPL], kv[VPL];
+  float sq, sk;
+  qk_load<TPR, VPL>(src, tid, D >> 3, qv, kv, sq, sk);
+  qk_finish<TPR, VPL>(tb, src, qv, kv, sq, sk, row, tid, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out, red);
 }
 
 // ------------------------------------------------------------------ time embedding
@@ -348,8 +443,11 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
   const int vpl = (D / 4 + tpr - 1) / tpr;  // 1..16
   const dim3 grid(tpr == 32 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
   const dim3 block(tpr == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS);
-#define GS_LN_CASE(T, V) \
-  case V: ln_modulate_kernel<T, V><<<grid, block, 0, stream>>>(x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out); break;
+#define GS_LN_CASE(T, V)                                                                                       \
+  case V:                                                                                                      \
+    ln_modulate_kernel<T, V, T == 32 ? 3 : 1><<<grid, block, 0, stream>>>(x, M, D, sh_a, sh_b, sc_a, sc_b,      \
+                                                                       b_stride, row_req, eps, out);           \
+    break;
 #define GS_LN_SWITCH(T)                                                                                     \
   switch (vpl) {                                                                                           \
     GS_LN_CASE(T, 1) GS_LN_CASE(T, 2) GS_LN_CASE(T, 3) GS_LN_CASE(T, 4) GS_LN_CASE(T, 5) GS_LN_CASE(T, 6)  \
@@ -379,8 +477,11 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   const int vpl = (D / 8 + tpr - 1) / tpr;  // 1..8
   const dim3 grid(tpr == 32 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
   const dim3 block(tpr == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS);
-#define GS_QK_CASE(T, V) \
-  case V: qk_norm_rope_pack_kernel<T, V><<<grid, block, 0, stream>>>(qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out); break;
+#define GS_QK_CASE(T, V)                                                                                     \
+  case V:                                                                                                    \
+    qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : 1><<<grid, block, 0, stream>>>(qkv, M, D, d, g_q, g_k, eps,   \
+                                                                             rp, pk, q_out, k_out, v_out);     \
+    break;
 #define GS_QK_SWITCH(T)                                                                                         \
   switch (vpl) {                                                                                               \
     GS_QK_CASE(T, 1) GS_QK_CASE(T, 2) GS_QK_CASE(T, 3) GS_QK_CASE(T, 4) GS_QK_CASE(T, 5) GS_QK_CASE(T, 6)      \

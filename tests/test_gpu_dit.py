@@ -261,3 +261,4 @@ def test_fused_exchange_uneven_heads_uses_transfer_plans(gs):
     z1, _ = _run_mode(gs, shape, [(416, 240, 5)], 1, 1, 1)
     assert st["a2a_plan"] > 0 and st["a2a_peer"] == 0
     assert np.array_equal(z8[0].view(np.uint32), z1[0].view(np.uint32))
+
