@@ -354,6 +354,31 @@ def run_gpu(args, rank, world, local_rank):
     step_flops = shape.layers * (costmodel.gemm_flops_per_block(rows, shape.dim, shape.ffn) + cross_gemm + af
                                  + cross_attn_flops)
     breakdown = {k: round(v["ms"] / args.prof_steps, 3) for k, v in st.items() if isinstance(v, dict)}
+    # per kernel class: algorithmic work per launch / average launch time vs its roofline
+    # (DESIGN.md §6): GEMMs against the bf16 tensor peak, row kernels against HBM bandwidth
+    D, F = shape.dim, shape.ffn
+    work = {"gemm_qkv": ("tensor", 2 * rows * D * 3 * D), "gemm_o": ("tensor", 2 * rows * D * D),
+            "gemm_mlp_up": ("tensor", 2 * rows * D * F), "gemm_mlp_down": ("tensor", 2 * rows * F * D),
+            "ln_mod": ("hbm", rows * D * (4 + 2)),            # x fp32 in, a bf16 out
+            "qk_norm_rope": ("hbm", rows * 3 * D * 2 * 2)}    # q|k|v bf16 in, packed q, k, v out
+    kernels = {}
+    for k, (bound, per_launch) in work.items():
+        v = st.get(k)
+        if not isinstance(v, dict) or v["n"] == 0 or v["ms"] <= 0:
+            continue
+        avg_s = v["ms"] / v["n"] * 1e-3
+        if bound == "tensor":
+            ach, unit, pkv = per_launch / avg_s / 1e12, "TFLOP/s", pk["bf16_sustained"]
+        else:
+            ach, unit, pkv = per_launch / avg_s / 1e9, "GB/s", pk["hbm"]
+        kernels[k] = {"bound": bound, "achieved": round(ach, 1), "peak": pkv, "unit": unit,
+                      "frac": round(ach / pkv, 4), "avg_launch_us": round(avg_s * 1e6, 1),
+                      "peak_src": ("measured bf16 sustained; frac_of_burst vs " + str(pk["bf16"]))
+                      if bound == "tensor" else "measured HBM copy bandwidth",
+                      "launches_per_step": v["n"] // args.prof_steps,
+                      ("flops" if bound == "tensor" else "bytes") + "_per_launch": int(per_launch)}
+        if bound == "tensor":
+            kernels[k]["frac_of_burst"] = round(ach / pk["bf16"], 4)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -386,6 +411,7 @@ def run_gpu(args, rank, world, local_rank):
         "step_tflops": round(step_flops / (ms_step * 1e-3) / 1e12, 1),
         "breakdown_ms_per_step": breakdown,
         "breakdown_steps": args.prof_steps,
+        "kernels": kernels,
         "step_ms_each": [round(x, 3) for x in step_ms],
         "step_cv": round(float(np.std(step_ms) / np.mean(step_ms)), 5) if len(step_ms) > 1 else None,
         "gpu_launches": int(launches),

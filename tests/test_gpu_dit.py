@@ -262,3 +262,42 @@ def test_fused_exchange_uneven_heads_uses_transfer_plans(gs):
     assert st["a2a_plan"] > 0 and st["a2a_peer"] == 0
     assert np.array_equal(z8[0].view(np.uint32), z1[0].view(np.uint32))
 
+
+
+# ----------------------------------------------------------------------------- degenerate sizes
+def test_degenerate_sizes_tiny_requests_and_empty_shards(gs):
+    """Degenerate cases: a 16x16 image is ONE token (attention returns v: pin P2 n=1), a 32x16
+    image is two; at SP 4 / 8 most ranks hold zero rows of them (empty shards: M = 0 kernels are
+    skipped, the exchange moves nothing for them).  The batch still matches the fp64 oracle and
+    is bit-exact across SP degree and against each request run alone."""
+    shape = sm.TINY.with_layers(2)
+    sizes = [(16, 16, 1), (32, 16, 1), (48, 48, 1), (256, 256, 1)]
+    glob = sm.as_f64(sm.global_params(shape))
+    blocks = [sm.as_f64(sm.block_params(shape, l)) for l in range(shape.layers)]
+    zs = {}
+    for p in (1, 2, 4, 8):
+        ctx = gs.Context(device=0, world_size=8, emulated=True)
+        mid = _mk(ctx, shape)
+        ranks = list(range(p))
+        reqs = [ctx.submit(mid, w, h, f, 50, 1000 + i, ranks) for i, (w, h, f) in enumerate(sizes)]
+        z0 = [ctx.read_latent(r) for r in reqs]
+        assert ctx.run_steps(reqs, ranks, 1) == 1
+        zs[p] = [ctx.read_latent(r) for r in reqs]
+        ctx.close()
+        if p == 1:
+            grids = [sm.token_grid(w, h) for w, h, _ in sizes]
+            assert [int(np.prod(g)) for g in grids] == [1, 2, 9, 256]
+            ref = dit.dit_steps([z.astype(np.float64) for z in z0], grids, [0] * len(sizes), 50, 1, glob, blocks,
+                                shape.heads)
+            for a, b, r in zip(z0, zs[1], ref):
+                assert rel_l2(b.astype(np.float64) - a, r - a) < TOL
+    for p in (2, 4, 8):
+        for a, b in zip(zs[p], zs[1]):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), f"p={p}"
+    ctx = gs.Context(device=0)
+    mid = _mk(ctx, shape)
+    one = ctx.submit(mid, 16, 16, 1, 50, 1000, [0])
+    ctx.run_steps([one], [0], 1)
+    z_alone = ctx.read_latent(one)
+    ctx.close()
+    assert np.array_equal(z_alone.view(np.uint32), zs[1][0].view(np.uint32))
