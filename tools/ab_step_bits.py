@@ -10,12 +10,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CASES = [
-    ("tiny", 2, [(256, 256, 1), (320, 192, 1), (160, 96, 1)], 1),
-    ("wan-1.3b", 2, [(256, 256, 1), (320, 192, 1), (416, 240, 5)], 1),
-    ("wan-1.3b", 1, [(416, 240, 5), (256, 256, 1)], 2),
-    ("wan-1.3b", 1, [(416, 240, 5)], 8),
-    ("wan-14b", 1, [(320, 176, 5), (256, 256, 1)], 2),
+CASES = [  # (model, layers, requests (w, h, frames), SP degree, a2a mode: 1 peer stores, 0 transfer plans)
+    ("tiny", 2, [(256, 256, 1), (320, 192, 1), (160, 96, 1)], 1, 1),
+    ("wan-1.3b", 2, [(256, 256, 1), (320, 192, 1), (416, 240, 5)], 1, 1),
+    ("wan-1.3b", 1, [(416, 240, 5), (256, 256, 1)], 2, 1),
+    ("wan-1.3b", 1, [(416, 240, 5), (256, 256, 1)], 4, 0),
+    ("wan-1.3b", 1, [(416, 240, 5)], 8, 1),
+    ("wan-14b", 1, [(320, 176, 5), (256, 256, 1)], 2, 1),
+    ("wan-14b", 1, [(320, 176, 5), (16, 16, 1)], 8, 0),
 ]
 
 
@@ -23,10 +25,10 @@ def dump(path):
     import paper_2604_04335_b200 as gs
     from synth import models as sm
     out = {}
-    for ci, (name, layers, sizes, p) in enumerate(CASES):
+    for ci, (name, layers, sizes, p, a2a) in enumerate(CASES):
         shape = sm.MODELS[name].with_layers(layers)
         ctx = gs.Context(device=0, world_size=8, emulated=True)
-        ctx.set_option("a2a", 1)
+        ctx.set_option("a2a", a2a)
         mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed)
         ranks = list(range(p))
         reqs = [ctx.submit(mid, w, h, f, 50, 1000 + i, ranks) for i, (w, h, f) in enumerate(sizes)]
