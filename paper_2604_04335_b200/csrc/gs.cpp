@@ -134,6 +134,20 @@ struct Scope {
 };
 
 void prof_flush(gs_ctx* c) {
+  // "_gaps": device time between consecutive scopes (launch latency, kernel ramp / drain outside
+  // any kernel, host-side stalls), = span(first start .. last end) - sum of the scopes.
+  if (c->prof_pending.size() > 1) {
+    float span = 0, inside = 0;
+    cudaEventElapsedTime(&span, c->prof_pending.front().second.first, c->prof_pending.back().second.second);
+    for (auto& pe : c->prof_pending) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe.second.first, pe.second.second);
+      inside += ms;
+    }
+    auto& g = c->prof_tab["_gaps"];
+    g.ms += span - inside;
+    g.n += 1;
+  }
   for (auto& pe : c->prof_pending) {
     float ms = 0;
     cudaEventElapsedTime(&ms, pe.second.first, pe.second.second);
