@@ -33,13 +33,27 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return (red[0] + red[1]) + (red[2] + red[3]);
 }
 
-// Row kernels come in two shapes, chosen by D alone (so every row of a model takes the same
-// reduction order): TPR = 128 threads per row (one row per CTA, D > 2048: Wan-14B) or TPR = 32 (a
-// warp per row, 8 rows per CTA, shuffle-only reductions: D <= 2048, where one CTA per row left
-// HBM half idle -- 26% of peak at the config-2 T2I shape).
+// Row kernels come in three shapes, chosen by D alone (so every row of a model takes the same
+// reduction order): TPR = 128 threads per row (one row per CTA, D > 2048: Wan-14B), TPR = 64 (two
+// warps per row, 8 rows per CTA, 1024 < D <= 2048: Wan-1.3B) or TPR = 32 (a warp per row, 8 rows
+// per CTA, shuffle-only reductions, D <= 1024).  One CTA per row left HBM half idle at the
+// config-2 T2I shape (26% of peak).
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+// TPR = 64 (two warps per row, 8 rows per CTA): warp sums exchanged through red[2 * slot + w]
+// (warp order), one named barrier per row slot.  red holds >= 16 floats.
 template <int TPR>
 __device__ __forceinline__ float row_sum(float v, float* red) {
   if (TPR == 32) return warp_sum(v);
+  if (TPR == 64) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, slot = w >> 1;
+    named_bar_sync(1 + slot, 64);  // the partner has read the previous exchange
+    if ((threadIdx.x & 31) == 0) red[2 * slot + (w & 1)] = v;
+    named_bar_sync(1 + slot, 64);
+    return red[2 * slot] + red[2 * slot + 1];
+  }
   return block_sum(v, red);
 }
 constexpr int kWarpRowMaxD = 2048;
@@ -113,13 +127,13 @@ __device__ __forceinline__ void ln_finish(const float4 (&v)[VPL], float s, long 
 }
 
 template <int TPR, int VPL, int MINB>
-__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, MINB)
+__global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : ROW_THREADS, MINB)
     ln_modulate_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ sh_a,
                        const float* __restrict__ sh_b, const float* __restrict__ sc_a,
                        const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
                        float eps, __nv_bfloat16* __restrict__ out) {
-  __shared__ float red[4];
-  if (TPR == 32) {
+  __shared__ float red[16];
+  if (TPR < 128) {
     // Warp per row, 8 rows per CTA.  When the CTA's rows belong to one request (rows are request
     // segments, so all but the boundary CTAs), the combined shift / 1 + scale vectors are formed
     // once per CTA in shared memory: per row 2 shared-memory float4 reads per 4 elements instead
@@ -128,9 +142,9 @@ __global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS
     // 3.26 -> 2.72 ms per step, bit-identical.
     __shared__ float4 s_sh[kWarpRowMaxD / 4], s_sc[kWarpRowMaxD / 4];
     const long long row0 = blockIdx.x * (long long)kWarpRowsPerCta;
-    const long long row = row0 + (threadIdx.x >> 5);
+    const long long row = row0 + threadIdx.x / TPR;
     const long long rlast = row0 + kWarpRowsPerCta - 1 < M ? row0 + kWarpRowsPerCta - 1 : M - 1;
-    const int tid = threadIdx.x & 31;
+    const int tid = threadIdx.x & (TPR - 1);
     const int nv = D >> 2;
     float4 v[VPL];
     float s = 0.f;
@@ -293,18 +307,18 @@ __device__ __forceinline__ void qk_finish(const QkTables& tb, const uint4* src, 
 }
 
 template <int TPR, int VPL, int MINB>
-__global__ void __launch_bounds__(TPR == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS, MINB)
+__global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : ROW_THREADS, MINB)
     qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
                              const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
                              float eps, const RopeParams rp, const PackParams pk,
                              __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
                              __nv_bfloat16* __restrict__ v_out) {
-  __shared__ float red[4];
+  __shared__ float red[16];
   __shared__ QkTables tb;
   qk_tables_build(tb, pk, rp, D / d, d >> 1);
-  const long long row = TPR == 32 ? blockIdx.x * (long long)kWarpRowsPerCta + (threadIdx.x >> 5) : blockIdx.x;
-  const int tid = TPR == 32 ? (threadIdx.x & 31) : threadIdx.x;
-  if (TPR == 32 && row >= M) return;
+  const long long row = TPR < 128 ? blockIdx.x * (long long)kWarpRowsPerCta + threadIdx.x / TPR : blockIdx.x;
+  const int tid = TPR < 128 ? (threadIdx.x & (TPR - 1)) : threadIdx.x;
+  if (TPR < 128 && row >= M) return;
   const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
   uint4 qv[VPL], kv[VPL];
   float sq, sk;
@@ -434,19 +448,29 @@ cudaError_t cfg_euler(float* z, float* z2, const float* vc, const float* vu, lon
   return cudaGetLastError();
 }
 
+namespace {
+// Threads per row, from D alone (every row of a model takes the same reduction order).  Two warps
+// per row for 1024 < D <= 2048 (Wan-1.3B): half the registers per thread, 32 instead of 24
+// resident warps per SM; config 2 (r01k, same box) LN 2.72 -> 2.41, qk 2.54 -> 2.37 ms per step.
+int row_tpr(int D) {
+  if (D > kWarpRowMaxD) return ROW_THREADS;
+  return D > 1024 ? 64 : 32;
+}
+}  // namespace
+
 cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const float* sh_b,
                         const float* sc_a, const float* sc_b, int b_stride, const int* row_req,
                         float eps, __nv_bfloat16* out, cudaStream_t stream) {
   if (M == 0) return cudaSuccess;
   if (D % 4 || D > 4 * MAXV * ROW_THREADS) return cudaErrorInvalidValue;
-  const int tpr = D <= kWarpRowMaxD ? 32 : ROW_THREADS;
+  const int tpr = row_tpr(D);
   const int vpl = (D / 4 + tpr - 1) / tpr;  // 1..16
-  const dim3 grid(tpr == 32 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
-  const dim3 block(tpr == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS);
+  const dim3 grid(tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
+  const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : ROW_THREADS);
 #define GS_LN_CASE(T, V)                                                                                       \
   case V:                                                                                                      \
-    ln_modulate_kernel<T, V, T == 32 ? 3 : 1><<<grid, block, 0, stream>>>(x, M, D, sh_a, sh_b, sc_a, sc_b,      \
-                                                                       b_stride, row_req, eps, out);           \
+    ln_modulate_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)><<<grid, block, 0, stream>>>(                      \
+        x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out);                                         \
     break;
 #define GS_LN_SWITCH(T)                                                                                     \
   switch (vpl) {                                                                                           \
@@ -457,6 +481,12 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
   }
   if (tpr == 32) {
     GS_LN_SWITCH(32)
+  } else if (tpr == 64) {
+    switch (vpl) {
+      GS_LN_CASE(64, 1) GS_LN_CASE(64, 2) GS_LN_CASE(64, 3) GS_LN_CASE(64, 4) GS_LN_CASE(64, 5)
+      GS_LN_CASE(64, 6) GS_LN_CASE(64, 7) GS_LN_CASE(64, 8)
+      default: return cudaErrorInvalidValue;
+    }
   } else {
     GS_LN_SWITCH(ROW_THREADS)
   }
@@ -473,14 +503,14 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   const int d = D / heads;
   if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > 16)
     return cudaErrorInvalidValue;
-  const int tpr = D <= kWarpRowMaxD ? 32 : ROW_THREADS;
+  const int tpr = row_tpr(D);
   const int vpl = (D / 8 + tpr - 1) / tpr;  // 1..8
-  const dim3 grid(tpr == 32 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
-  const dim3 block(tpr == 32 ? 32 * kWarpRowsPerCta : ROW_THREADS);
+  const dim3 grid(tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
+  const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : ROW_THREADS);
 #define GS_QK_CASE(T, V)                                                                                     \
   case V:                                                                                                    \
-    qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : 1><<<grid, block, 0, stream>>>(qkv, M, D, d, g_q, g_k, eps,   \
-                                                                             rp, pk, q_out, k_out, v_out);     \
+    qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)><<<grid, block, 0, stream>>>(              \
+        qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out);                                           \
     break;
 #define GS_QK_SWITCH(T)                                                                                         \
   switch (vpl) {                                                                                               \
@@ -490,6 +520,11 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   }
   if (tpr == 32) {
     GS_QK_SWITCH(32)
+  } else if (tpr == 64) {
+    switch (vpl) {
+      GS_QK_CASE(64, 1) GS_QK_CASE(64, 2) GS_QK_CASE(64, 3) GS_QK_CASE(64, 4)
+      default: return cudaErrorInvalidValue;
+    }
   } else {
     GS_QK_SWITCH(ROW_THREADS)
   }
