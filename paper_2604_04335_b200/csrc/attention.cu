@@ -215,6 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the setup above overlaps the previous kernel's tail; global memory only from here
+  pdl_launch_dependents();
 
   // register split: producer / MMA warpgroup shrinks, the two softmax warpgroups grow.  The CTA
   // pool is 384 x 168 (launch allocation): 4 warps x 32 x (168 - 80) = 11264 freed >= 8 warps x
@@ -861,13 +863,15 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = PAIR ? 2 : 1;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = PAIR ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2, osc);
 }
 

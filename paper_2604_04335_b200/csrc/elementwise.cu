@@ -8,6 +8,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -133,6 +135,8 @@ __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : ROW_THREAD
                        const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
                        float eps, __nv_bfloat16* __restrict__ out) {
   __shared__ float red[16];
+  pdl_wait();
+  pdl_launch_dependents();
   if (TPR < 128) {
     // Warp per row, 8 rows per CTA.  When the CTA's rows belong to one request (rows are request
     // segments, so all but the boundary CTAs), the combined shift / 1 + scale vectors are formed
@@ -315,6 +319,8 @@ __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : ROW_THREAD
                              __nv_bfloat16* __restrict__ v_out) {
   __shared__ float red[16];
   __shared__ QkTables tb;
+  pdl_wait();
+  pdl_launch_dependents();
   qk_tables_build(tb, pk, rp, D / d, d >> 1);
   const long long row = TPR < 128 ? blockIdx.x * (long long)kWarpRowsPerCta + threadIdx.x / TPR : blockIdx.x;
   const int tid = TPR < 128 ? (threadIdx.x & (TPR - 1)) : threadIdx.x;
@@ -448,7 +454,28 @@ cudaError_t cfg_euler(float* z, float* z2, const float* vc, const float* vu, lon
   return cudaGetLastError();
 }
 
+bool pdl_enabled() {
+  static const bool on = !(getenv("GS_PDL") && getenv("GS_PDL")[0] == '0');
+  return on;
+}
+
 namespace {
+// Launch with the programmatic-dependent-launch attribute (when enabled).
+template <class K, class... Args>
+cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // Threads per row, from D alone (every row of a model takes the same reduction order).  Two warps
 // per row for 1024 < D <= 2048 (Wan-1.3B): half the registers per thread, 32 instead of 24
 // resident warps per SM; config 2 (r01k, same box) LN 2.72 -> 2.41, qk 2.54 -> 2.37 ms per step.
@@ -469,8 +496,9 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
   const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : ROW_THREADS);
 #define GS_LN_CASE(T, V)                                                                                       \
   case V:                                                                                                      \
-    ln_modulate_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)><<<grid, block, 0, stream>>>(                      \
-        x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out);                                         \
+    if (cudaError_t e = launch_pdl(ln_modulate_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)>, grid, block, stream, \
+                                   x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out))                 \
+      return e;                                                                                                 \
     break;
 #define GS_LN_SWITCH(T)                                                                                     \
   switch (vpl) {                                                                                           \
@@ -509,8 +537,9 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : ROW_THREADS);
 #define GS_QK_CASE(T, V)                                                                                     \
   case V:                                                                                                    \
-    qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)><<<grid, block, 0, stream>>>(              \
-        qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out);                                           \
+    if (cudaError_t e = launch_pdl(qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)>, grid, block,  \
+                                   stream, qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out))            \
+      return e;                                                                                               \
     break;
 #define GS_QK_SWITCH(T)                                                                                         \
   switch (vpl) {                                                                                               \

@@ -247,6 +247,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();  // barriers of both CTAs initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the setup above overlaps the previous kernel's tail; global memory only from here
+  pdl_launch_dependents();
 
   if (warp == 0) {
     if (lane == 0) {  // producer (both CTAs): this CTA's A rows and W half, bytes counted by the leader
@@ -425,8 +427,17 @@ cudaError_t launch_bn(int M, int N, int K, const void* A, int lda, const void* W
   const int tiles = ((M + PM - 1) / PM) * ((N + BN - 1) / BN);
   const int pairs = tiles < num_sms / 2 ? tiles : num_sms / 2;
   const int grid = 2 * pairs;  // clusters of 2 (CTA pairs on one TPC)
-  gemm_tc_kernel<EPI, BN><<<grid, THREADS, GCfg<BN, RMW>::SMEM_BYTES, stream>>>(ta, tb, tx, M, N, K, ep);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = GCfg<BN, RMW>::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN>, ta, tb, tx, M, N, K, ep);
 }
 
 int pick_bn(int M, int N, int num_sms) {

@@ -32,6 +32,9 @@ struct EpiParams {
   float dsig[8];              // per-request sigma_{i+1} - sigma_i
 };
 
+// Programmatic dependent launch for the step's GEMM / attention / row kernels (env GS_PDL=0 turns
+// it off; elementwise.cu).
+bool pdl_enabled();
 // Process-wide GEMM pair-tile width override (0 = automatic, 192 or 256; gs_set_option "gemm_bn").
 extern std::atomic<int> g_gemm_bn_override;
 // Returns cudaError_t; builds the TMA descriptors on the host.
