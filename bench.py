@@ -86,17 +86,26 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.mark = 0
 
     def start(self):
+        """Start sampling (every 100 ms) and wait for the first sample, so that a short timed
+        region (a config-2 step is ~50 ms) still has samples; call mark() where it begins."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+
+    def mark_start(self):
+        self.mark = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -111,8 +120,12 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
+        # samples taken inside the timed region; if it was shorter than the sampling interval, the
+        # samples nearest to it (the last one before and the first one after)
+        inside = self.lines[self.mark:]
+        near = inside if inside else self.lines[max(self.mark - 1, 0):self.mark + 1]
         sms, maxs, reasons = [], [], set()
-        for ln in self.lines:
+        for ln in near:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -127,7 +140,7 @@ class ClockSampler:
         if not sms:
             return None
         return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": max(maxs),
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "reasons": sorted(reasons), "samples": len(sms), "in_region": bool(inside)}
 
 
 # ----------------------------------------------------------------------------- oracle sample
@@ -283,11 +296,13 @@ def run_gpu(args, rank, world, local_rank):
         ctx.run_steps(reqs, ranks, args.warmup)
     ctx.profile(2, True)  # step events only: the timed steps carry no per-kernel events
     clocks = ClockSampler(local_rank) if rank == 0 else None
-    barrier()
     if clocks:
-        clocks.start()
+        clocks.start()  # before the barrier: waiting for its first sample must not skew the ranks
+    barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    if clocks:
+        clocks.mark_start()
     ev0.record(stream)
     done = ctx.run_steps(reqs, ranks, args.steps)
     ev1.record(stream)
