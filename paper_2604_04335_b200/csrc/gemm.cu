@@ -192,11 +192,11 @@ constexpr double kNarrowRate = 0.85;
 // Tile rasterisation: bands of GROUP_M M-tiles, N-major inside a band, so the ~148 tiles in
 // flight cover a GROUP_M x (148 / GROUP_M) block whose A and W panels stay resident in L2.
 constexpr int GROUP_M = 16;
-__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int& mb, int& nb) {
-  const int per_group = GROUP_M * num_n;
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int group_m, int& mb, int& nb) {
+  const int per_group = group_m * num_n;
   const int g = t / per_group, r = t - g * per_group;
-  const int m0 = g * GROUP_M;
-  const int gm = min(GROUP_M, num_m - m0);
+  const int m0 = g * group_m;
+  const int gm = min(group_m, num_m - m0);
   mb = m0 + r % gm;
   nb = r / gm;
 }
@@ -256,7 +256,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       for (int t = pair; t < num_tiles; t += npairs) {
         int mb, nb;
-        tile_coords(t, num_m, num_n, mb, nb);
+        tile_coords(t, num_m, num_n, ep.group_m, mb, nb);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -309,7 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto load_tile = [&]() {
       if (lt < num_tiles) {
         int mb, nb;
-        tile_coords(lt, num_m, num_n, mb, nb);
+        tile_coords(lt, num_m, num_n, ep.group_m, mb, nb);
         lnch = min(BN, N - nb * BN) / 32;
         lcol = nb * BN;
         lrow = mb * PM + rank * BM + quarter * 32;
@@ -357,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int it = 0;
     for (int t = pair; t < num_tiles; t += npairs, ++it) {
       int mb, nb;
-      tile_coords(t, num_m, num_n, mb, nb);
+      tile_coords(t, num_m, num_n, ep.group_m, mb, nb);
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
       mbar_wait(&tfull[as], aphase);
@@ -437,7 +437,14 @@ cudaError_t launch_bn(int M, int N, int K, const void* A, int lda, const void* W
   attr.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN>, ta, tb, tx, M, N, K, ep);
+  static const int group_m = [] {
+    const char* e = getenv("GS_GEMM_GROUP_M");  // development aid (A/B of the rasterisation band)
+    const int g = e ? atoi(e) : GROUP_M;
+    return g > 0 ? g : GROUP_M;
+  }();
+  EpiParams epg = ep;
+  epg.group_m = group_m;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BN>, ta, tb, tx, M, N, K, epg);
 }
 
 int pick_bn(int M, int N, int num_sms) {

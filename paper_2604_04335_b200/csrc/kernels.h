@@ -30,6 +30,7 @@ struct EpiParams {
   int gate_b_stride;
   const int* row_req;         // [M] request index of each row
   float dsig[8];              // per-request sigma_{i+1} - sigma_i
+  int group_m;                // tile rasterisation band (M-tiles); set by the launcher
 };
 
 // Programmatic dependent launch for the step's GEMM / attention / row kernels (env GS_PDL=0 turns

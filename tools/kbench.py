@@ -36,7 +36,8 @@ GEMM = [
     ("c2 down", 16384, 1536, 8960),
     ("c4 sp8 qkv", 9450, 15360, 5120), ("c4 sp8 o", 9450, 5120, 5120),
     ("c4 sp8 up", 9450, 13824, 5120), ("c4 sp8 down", 9450, 5120, 13824),
-    ("c4 sp1 qkv", 75600, 15360, 5120),
+    ("c4 sp1 qkv", 75600, 15360, 5120), ("c4 cfg qkv", 151200, 15360, 5120), ("c4 sp1 up", 75600, 13824, 5120),
+    ("c4 cfg up", 151200, 13824, 5120),
     ("c3 sp8 qkv", 4095, 4608, 1536), ("c3 sp8 o", 4095, 1536, 1536), ("c3 sp8 up", 4095, 8960, 1536),
     ("c3 sp8 down", 4095, 1536, 8960), ("c3 sp4 o", 8190, 1536, 1536), ("c3 sp4 down", 8190, 1536, 8960),
 ]
