@@ -99,10 +99,11 @@ def main():
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     f()
                     e0.record()
-                    f()
+                    for _ in range(a.reps):
+                        f()
                     e1.record()
                     torch.cuda.synchronize()
-                    tms = e0.elapsed_time(e1)
+                    tms = e0.elapsed_time(e1) / a.reps
                     line += f" | torch sdpa {tms:8.3f} ms {fl / tms / 1e9:7.1f}"
             print(line, flush=True)
             res[label] = tf
