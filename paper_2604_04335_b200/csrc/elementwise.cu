@@ -25,18 +25,21 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// Sum over the 128 threads of the CTA in a fixed order; result broadcast to all threads.
+// Sum over the NW warps of the CTA in a fixed order (pairwise tree in warp order); result
+// broadcast to all threads.
+template <int NW = 4>
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5;
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[w] = v;
   __syncthreads();
-  return (red[0] + red[1]) + (red[2] + red[3]);
+  if (NW == 4) return (red[0] + red[1]) + (red[2] + red[3]);
+  return ((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7]));
 }
 
 // Row kernels come in three shapes, chosen by D alone (so every row of a model takes the same
-// reduction order): TPR = 128 threads per row (one row per CTA, D > 2048: Wan-14B), TPR = 64 (two
+// reduction order): TPR = 256 threads per row (one row per CTA, D > 2048: Wan-14B), TPR = 64 (two
 // warps per row, 8 rows per CTA, 1024 < D <= 2048: Wan-1.3B) or TPR = 32 (a warp per row, 8 rows
 // per CTA, shuffle-only reductions, D <= 1024).  One CTA per row left HBM half idle at the
 // config-2 T2I shape (26% of peak).
@@ -56,7 +59,7 @@ __device__ __forceinline__ float row_sum(float v, float* red) {
     named_bar_sync(1 + slot, 64);
     return red[2 * slot] + red[2 * slot + 1];
   }
-  return block_sum(v, red);
+  return block_sum<TPR / 32>(v, red);
 }
 constexpr int kWarpRowMaxD = 2048;
 constexpr int kWarpRowsPerCta = 8;
@@ -129,7 +132,7 @@ __device__ __forceinline__ void ln_finish(const float4 (&v)[VPL], float s, long 
 }
 
 template <int TPR, int VPL, int MINB>
-__global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : ROW_THREADS, MINB)
+__global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
     ln_modulate_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ sh_a,
                        const float* __restrict__ sh_b, const float* __restrict__ sc_a,
                        const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
@@ -311,7 +314,7 @@ __device__ __forceinline__ void qk_finish(const QkTables& tb, const uint4* src, 
 }
 
 template <int TPR, int VPL, int MINB>
-__global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : ROW_THREADS, MINB)
+__global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
     qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
                              const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
                              float eps, const RopeParams rp, const PackParams pk,
@@ -480,7 +483,8 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t stream, Arg
 // per row for 1024 < D <= 2048 (Wan-1.3B): half the registers per thread, 32 instead of 24
 // resident warps per SM; config 2 (r01k, same box) LN 2.72 -> 2.41, qk 2.54 -> 2.37 ms per step.
 int row_tpr(int D) {
-  if (D > kWarpRowMaxD) return ROW_THREADS;
+  // D > 2048 (Wan-14B): 256 threads per row (r01p: config 4 LN 41.3 -> 40.2, qk 58.6 -> 56.2 ms/step)
+  if (D > kWarpRowMaxD) return 256;
   return D > 1024 ? 64 : 32;
 }
 }  // namespace
@@ -493,10 +497,10 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
   const int tpr = row_tpr(D);
   const int vpl = (D / 4 + tpr - 1) / tpr;  // 1..16
   const dim3 grid(tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
-  const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : ROW_THREADS);
+  const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : tpr);
 #define GS_LN_CASE(T, V)                                                                                       \
   case V:                                                                                                      \
-    if (cudaError_t e = launch_pdl(ln_modulate_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)>, grid, block, stream, \
+    if (cudaError_t e = launch_pdl(ln_modulate_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : (T == 256 ? 3 : 1))>, grid, block, stream, \
                                    x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out))                 \
       return e;                                                                                                 \
     break;
@@ -515,8 +519,14 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
       GS_LN_CASE(64, 6) GS_LN_CASE(64, 7) GS_LN_CASE(64, 8)
       default: return cudaErrorInvalidValue;
     }
-  } else {
+  } else if (tpr == ROW_THREADS) {
     GS_LN_SWITCH(ROW_THREADS)
+  } else if (tpr == 256) {
+    switch (vpl) {
+      GS_LN_CASE(256, 1) GS_LN_CASE(256, 2) GS_LN_CASE(256, 3) GS_LN_CASE(256, 4) GS_LN_CASE(256, 5)
+      GS_LN_CASE(256, 6) GS_LN_CASE(256, 7) GS_LN_CASE(256, 8)
+      default: return cudaErrorInvalidValue;
+    }
   }
 #undef GS_LN_SWITCH
 #undef GS_LN_CASE
@@ -534,10 +544,10 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   const int tpr = row_tpr(D);
   const int vpl = (D / 8 + tpr - 1) / tpr;  // 1..8
   const dim3 grid(tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
-  const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : ROW_THREADS);
+  const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : tpr);
 #define GS_QK_CASE(T, V)                                                                                     \
   case V:                                                                                                    \
-    if (cudaError_t e = launch_pdl(qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : 1)>, grid, block,  \
+    if (cudaError_t e = launch_pdl(qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : (T == 256 ? 3 : 1))>, grid, block,  \
                                    stream, qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out))            \
       return e;                                                                                               \
     break;
@@ -554,8 +564,13 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
       GS_QK_CASE(64, 1) GS_QK_CASE(64, 2) GS_QK_CASE(64, 3) GS_QK_CASE(64, 4)
       default: return cudaErrorInvalidValue;
     }
-  } else {
+  } else if (tpr == ROW_THREADS) {
     GS_QK_SWITCH(ROW_THREADS)
+  } else if (tpr == 256) {
+    switch (vpl) {
+      GS_QK_CASE(256, 1) GS_QK_CASE(256, 2) GS_QK_CASE(256, 3) GS_QK_CASE(256, 4)
+      default: return cudaErrorInvalidValue;
+    }
   }
 #undef GS_QK_SWITCH
 #undef GS_QK_CASE
