@@ -452,7 +452,7 @@ def main():
     ap.add_argument("--workload", default="t2v720", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--prof-steps", type=int, default=1,
+    ap.add_argument("--prof-steps", type=int, default=2,
                     help="extra per-kernel-profiled steps after the timed region (breakdown, roofline)")
     ap.add_argument("--ref-tokens", type=int, default=1200,
                     help="token budget of the oracle sample (bounded CPU time)")
