@@ -1,8 +1,8 @@
 #!/bin/bash
-# Final round-1 validation at HEAD: GPU tests, smoke, bench lines (all workloads + reference arm),
+# Round validation at HEAD (TAG names the round): GPU tests, smoke, bench lines (all workloads + reference arm),
 # the launch list of the default bench command, ncu --set full of attention and the top GEMM.
 set -x
-TAG=${TAG:-r01m}
+TAG=${TAG:-r01s}
 NCU=/usr/local/cuda/bin/ncu
 python paper_2604_04335_b200/build.py > gpurun_out/${TAG}_build.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.log
