@@ -52,6 +52,26 @@ def test_block_config1_tiny(gs):
     assert err < TOL, err
 
 
+@pytest.mark.parametrize("shape", [
+    sm.ModelShape("d1024-h64", 1024, 16, 4096, 1),    # row kernels: a warp per row (VPL 8 / 4)
+    sm.ModelShape("d2048-h128", 2048, 16, 2048, 1),   # two warps per row, largest VPL of that regime
+    sm.ModelShape("d3072-h128", 3072, 24, 1024, 1),   # 256 threads per row (Wan2.2-5B width [ext])
+    pytest.param(sm.ModelShape("d8192-h128", 8192, 64, 256, 1), marks=pytest.mark.slow),  # largest D
+])
+def test_block_row_kernel_regimes(gs, shape):
+    """Block parity at model widths outside configs 1-4, covering every row-kernel shape (threads
+    per row 32 / 64 / 256 and their largest register tiles); two ragged requests so some 8-row CTAs
+    straddle a request boundary (per-row modulation loads) and others stage it per CTA."""
+    ctx = gs.Context(device=0)
+    grids = [sm.token_grid(96, 80), sm.token_grid(48, 48)]   # 30 + 9 rows
+    x, out, ref = _block_case(ctx, shape, grids, [700.0, 120.0])
+    ctx.close()
+    offs = np.cumsum([0] + [int(np.prod(g)) for g in grids])
+    for a, b in zip(offs[:-1], offs[1:]):
+        err = rel_l2(out[a:b].astype(np.float64) - x[a:b], ref[a:b] - x[a:b])
+        assert err < TOL, (shape.name, err)
+
+
 def test_block_config2_wan13b_varlen(gs):
     # config 2b: varlen 4-image batch {1024^2, 1280x768, 768x1280, 1152x896}, Wan-1.3B block
     grids = [sm.token_grid(1024, 1024), sm.token_grid(1280, 768), sm.token_grid(768, 1280),
