@@ -1,4 +1,6 @@
 #!/bin/bash
+# Historical (kept for the record in profiles/r01_notes.md): the env knob it toggles was removed once
+# the variant became the default, so today both arms run the same kernels.
 # D > 2048 row kernels: 256 threads per row (GS_ROWK_TPR256=1) vs 128; GPU parity tests under 256,
 # t2v720 bench breakdowns.
 set -x
