@@ -92,7 +92,9 @@ const char* gs_last_error(gs_ctx* ctx);
  * device copies in emulated mode).  Both give bit-identical results.  Every process of an SP
  * group must use the same setting.  "gemm_bn": GEMM pair-tile width, 0 (default: 256, or 192 when
  * N % 192 == 0 and the narrower tiles fill a small grid's last wave better), 192 or 256 forced
- * (process-wide; both give identical bits).  GS_EINVAL for an unknown key or value. */
+ * (process-wide; both give identical bits).  "pdl": 1 (default) launches the step's kernels with
+ * programmatic dependent launch (each kernel's setup overlaps the previous kernel's drain), 0 plain
+ * stream order (process-wide; identical bits).  GS_EINVAL for an unknown key or value. */
 int gs_set_option(gs_ctx* ctx, const char* key, long long value);
 /* Number of SMs of the context's device, world size, ranks owned by this process. */
 int gs_info(gs_ctx* ctx, int* num_sms, int* world_size, int* nlocal);

@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -457,9 +458,15 @@ cudaError_t cfg_euler(float* z, float* z2, const float* vc, const float* vu, lon
   return cudaGetLastError();
 }
 
+std::atomic<int> g_pdl{-1};  // -1: not yet read from GS_PDL (default on)
+
 bool pdl_enabled() {
-  static const bool on = !(getenv("GS_PDL") && getenv("GS_PDL")[0] == '0');
-  return on;
+  int v = g_pdl.load(std::memory_order_relaxed);
+  if (v < 0) {
+    v = (getenv("GS_PDL") && getenv("GS_PDL")[0] == '0') ? 0 : 1;
+    g_pdl.store(v);
+  }
+  return v != 0;
 }
 
 namespace {

@@ -1191,6 +1191,11 @@ int gs_set_option(gs_ctx* c, const char* key, long long value) {
     g_gemm_bn_override.store(static_cast<int>(value));
     return GS_OK;
   }
+  if (strcmp(key, "pdl") == 0) {
+    if (value != 0 && value != 1) return fail(c, GS_EINVAL, "pdl %lld (0, 1)", value);
+    g_pdl.store(static_cast<int>(value));
+    return GS_OK;
+  }
   return fail(c, GS_EINVAL, "unknown option '%s'", key);
 }
 

@@ -33,9 +33,10 @@ struct EpiParams {
   int group_m;                // tile rasterisation band (M-tiles); set by the launcher
 };
 
-// Programmatic dependent launch for the step's GEMM / attention / row kernels (env GS_PDL=0 turns
-// it off; elementwise.cu).
+// Programmatic dependent launch for the step's GEMM / attention / row kernels (elementwise.cu):
+// on by default; env GS_PDL=0 or gs_set_option "pdl" 0 turns it off (process-wide).
 bool pdl_enabled();
+extern std::atomic<int> g_pdl;
 // Process-wide GEMM pair-tile width override (0 = automatic, 192 or 256; gs_set_option "gemm_bn").
 extern std::atomic<int> g_gemm_bn_override;
 // Returns cudaError_t; builds the TMA descriptors on the host.
