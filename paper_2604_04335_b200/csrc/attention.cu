@@ -2,10 +2,13 @@
 //   O_h = softmax(Q_h K_h^T / sqrt(d)) V_h per request (oracle: oracle/dit.py attention()).
 //
 // Design (B200-first; FlashAttention-4-style structure, written from scratch):
-//   * one CTA = one head x two 128-row Q tiles of one request (256 query rows);
+//   * one CTA = one head x two 128-row Q tiles of one request (256 query rows); for d = 128 two
+//     CTAs form a pair (cta_group::2, M = 256 MMAs issued by the leader, see Cfg);
 //   * warps 0..3 / 4..7: softmax warpgroups WG0 / WG1, one thread per query row;
-//   * warp 8: TMA producer (Q once; K_j into a 3-slot ring, V_j into a 2-slot ring, 128B swizzle);
-//   * warp 9: TMEM owner + single-thread tcgen05.mma issuer;
+//   * warp 8: TMA producer (Q once; K_j and V_j into rings of Cfg::KST / Cfg::VST slots, 128B
+//     swizzle);
+//   * warp 9: TMEM owner + single-thread tcgen05.mma issuer (warps 10, 11 idle);
+//   * griddepcontrol.wait after the setup (programmatic dependent launch, ptx.cuh);
 //   * TMEM (512 cols): S_w = Q_w K_j^T at cols [128w, 128w+128) (fp32), P_w (bf16 pairs)
 //     written over S_w cols [128w, 128w+64), O_w at cols [256+128w, 256+128w+d);
 //   * MMA issue order S0_0, S1_0, {PV0_j, S0_{j+1}, PV1_j, S1_{j+1}}: WG0's softmax of tile j+1

@@ -9,7 +9,9 @@
 //   * warps 2..5: epilogue (tcgen05.ld 32x32b -> registers -> fused epilogue -> global; fp32
 //     read-modify-write epilogues stream x through shared memory by TMA load / store);
 //   * two TMEM accumulators (2 x BN columns) so the epilogue of tile i overlaps the
-//     main loop of tile i+1.
+//     main loop of tile i+1;
+//   * tiles in bands of GROUP_M M-tiles (L2 reuse of A / W panels); griddepcontrol.wait after the
+//     setup (programmatic dependent launch).
 // Bit-exactness across M (SURVEY.md §8(a) invariant 1): no split-K, no atomics, the same
 // MMA shape and K order for every tile, each output row depends only on its own A row.
 #include <cuda.h>
