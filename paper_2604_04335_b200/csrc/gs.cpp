@@ -1126,6 +1126,12 @@ int gs_init(int device, int world_size, int rank, const void* nccl_uid, gs_ctx**
       *out = c;
       return fail(c, GS_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
     }
+    // Our kernels release their dependents early (griddepcontrol.launch_dependents); a collective
+    // launched right after one must not start before it completes.  NCCL's own kernels are not
+    // known to wait on griddepcontrol, so multi-process contexts run in plain stream order unless
+    // GS_PDL=1 asks otherwise (this path has not been measured on two physical GPUs).
+    const char* e = getenv("GS_PDL");
+    if (!(e && e[0] == '1')) g_pdl.store(0);
   }
   *out = c;
   return GS_OK;
