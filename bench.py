@@ -124,7 +124,7 @@ class ClockSampler:
         # samples nearest to it (the last one before and the first one after)
         inside = self.lines[self.mark:]
         near = inside if inside else self.lines[max(self.mark - 1, 0):self.mark + 1]
-        sms, maxs, reasons = [], [], set()
+        sms, maxs, pw, reasons = [], [], [], set()
         for ln in near:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
@@ -134,12 +134,17 @@ class ClockSampler:
                 maxs.append(float(f[2]))
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[3]))
+            except ValueError:
+                pass
             for name, v in zip(self.REASONS, f[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
         if not sms:
             return None
         return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": max(maxs),
+                "power_w": float(np.median(pw)) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sms), "in_region": bool(inside)}
 
 
