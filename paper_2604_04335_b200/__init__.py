@@ -289,10 +289,15 @@ class Context:
         return {"steps_done": v[0].value, "steps_total": v[1].value,
                 "ranks": list(ranks[:v[2].value]), "state": v[3].value, "n_tokens": v[4].value}
 
-    def read_latent(self, req, n_tokens=None, lat=64):
+    def read_latent(self, req, n_tokens=None, lat=64, out=None):
+        """Gather the request's latent [n_tokens, lat] fp32 into `out` (e.g. a pinned host buffer)
+        or a new array."""
         if n_tokens is None:
             n_tokens = self.query(req)["n_tokens"]
-        out = np.zeros((n_tokens, lat), dtype=np.float32)
+        if out is None:
+            out = np.zeros((n_tokens, lat), dtype=np.float32)
+        elif out.dtype != np.float32 or not out.flags.c_contiguous or out.size != n_tokens * lat:
+            raise ValueError("out must be a C-contiguous float32 array of n_tokens * lat elements")
         self._ck(self._lib.gs_read_latent(self._h, req, out.ctypes.data_as(_FP), out.size))
         return out
 
