@@ -68,7 +68,11 @@ struct SeqTable {
 // half of every K tile (64 keys, the B operand's N half) and half of every V tile (64 of the d
 // columns), halving per-SM shared-memory B reads and L2 -> SM traffic (tools/micro: the UMMA smem
 // read path is 128 B/clk).
-template <int HD, bool PAIR>
+// PS (round-2 experiment, GS_ATTN_PS=1): P goes to shared memory (PV as an SS MMA) so S_{j+1} can
+// be issued as soon as the softmax has loaded S_j, breaking the per-group chain S -> softmax -> P ->
+// PV -> S of v5 (profiles/r01_notes.md; tools/micro/attn_pv_smem_bench.cu: the SS-PV + P-store mix
+// runs at the MMA floor).  Costs 2 x 32 KB of P buffers, paid for with K / V rings of 3 / 2.
+template <int HD, bool PAIR, bool PS = false>
 struct Cfg {
   static constexpr int BOXES = HD / 64;                  // 64-element (128 B) column boxes
   static constexpr int TILE_BYTES = 128 * HD * 2;        // one 128-row Q tile
@@ -76,12 +80,13 @@ struct Cfg {
   static constexpr int KBOX_BYTES = (PAIR ? 64 : 128) * 128;       // one [rows][64] K box
   static constexpr int VT_BYTES = 128 * (PAIR ? HD / 2 : HD) * 2;  // this CTA's part of a V tile
   // K ring deeper than V: a K slot frees after both S MMAs, a V slot only after both PV MMAs
-  static constexpr int KST = PAIR ? 4 : (HD == 128 ? 3 : 4);
-  static constexpr int VST = PAIR ? 4 : (HD == 128 ? 2 : 4);
+  static constexpr int KST = PS ? 3 : PAIR ? 4 : (HD == 128 ? 3 : 4);
+  static constexpr int VST = PS ? 2 : PAIR ? 4 : (HD == 128 ? 2 : 4);
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = 2 * TILE_BYTES;
   static constexpr int V_OFF = K_OFF + KST * KT_BYTES;
-  static constexpr int BAR_OFF = V_OFF + VST * VT_BYTES;
+  static constexpr int P_OFF = V_OFF + VST * VT_BYTES;          // PS: P_w, 128 rows x 128 keys bf16
+  static constexpr int BAR_OFF = P_OFF + (PS ? 2 * 128 * 128 * 2 : 0);
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
 };
 
@@ -135,15 +140,61 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], floa
   return __fadd2_rn(acc0, acc1);
 }
 
+// PS: the same arithmetic, P stored to this thread's row of the shared-memory P tile in the UMMA
+// K-major 128B-swizzled layout (box b = keys [64 b, 64 b + 64) at b * 16384, row r at r * 128,
+// 16-byte chunk c at (c ^ (r & 7)) * 16), the layout TMA gives Q.
+template <int POLY8, bool FULL, int NCOL>
+__device__ __forceinline__ float2 exp_pack_regs(const uint32_t (&v)[NCOL], float2 sc2, float2 nm2, int kv_valid,
+                                               uint32_t (&pkall)[NCOL / 2]) {
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < NCOL / 32; ++c) {
+    uint32_t* pk = pkall + 16 * c;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int col = c * 32 + 2 * i;
+      const float2 x =
+          __ffma2_rn(make_float2(__uint_as_float(v[col]), __uint_as_float(v[col + 1])), sc2, nm2);
+      float2 p;
+      if (poly_pair<POLY8>(i & 7)) {
+        p = exp2_poly2(x);
+      } else {
+        p.x = ex2_approx(x.x);
+        p.y = ex2_approx(x.y);
+      }
+      if (!FULL) {
+        p.x = col < kv_valid ? p.x : 0.f;
+        p.y = col + 1 < kv_valid ? p.y : 0.f;
+      }
+      if (i & 1)
+        acc1 = __fadd2_rn(acc1, p);
+      else
+        acc0 = __fadd2_rn(acc0, p);
+      pk[i] = pack_bf16x2(p.x, p.y);
+    }
+  }
+  return __fadd2_rn(acc0, acc1);
+}
+template <int NPK>
+__device__ __forceinline__ void store_p_smem(const uint32_t (&pk)[NPK], uint32_t prow, int rsw) {
+#pragma unroll
+  for (int ch = 0; ch < NPK / 4; ++ch) {  // keys [8 ch, 8 ch + 8)
+    const uint32_t a = prow + (ch >> 3) * 16384 + (((ch & 7) ^ rsw) << 4);
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[4 * ch]), "r"(pk[4 * ch + 1]),
+                 "r"(pk[4 * ch + 2]), "r"(pk[4 * ch + 3])
+                 : "memory");
+  }
+}
+
 // SCATTER: the fused head->seq exchange epilogue (OScatter); a separate instantiation so the plain
 // kernel keeps its register allocation (the scatter lookup in the shared epilogue cost ~5%).
-template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false>
+template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false, bool PS = false>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
                    const __grid_constant__ SeqTable tab, float scale_log2,
                    const __grid_constant__ OScatter osc) {
-  using C = Cfg<HD, PAIR>;
+  using C = Cfg<HD, PAIR, PS>;
   const unsigned cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
   if (TRACE && threadIdx.x == 0 && cta_lin < 8192) {
     g_attn_ctatime[cta_lin * 4 + 0] = gtimer();
@@ -160,7 +211,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* sfull = vempty + C::VST;    // [2]
   uint64_t* pfull = sfull + 2;        // [2]
   uint64_t* ofull = pfull + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 2);
+  uint64_t* sfree = ofull + 2;        // [2] PS: the softmax group has loaded S_j (leader's, 4 x NC arrivals)
+  uint64_t* pfree = sfree + 2;        // [2] PS: PV_j done (P_w buffer and O_w free; multicast commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfree + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y;
@@ -197,6 +250,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&sfull[w], 1);
       mbar_init(&pfull[w], 4 * NC);
       mbar_init(&ofull[w], 1);
+      mbar_init(&sfree[w], 4 * NC);
+      mbar_init(&pfree[w], 1);
     }
     fence_barrier_init();
   }
@@ -286,6 +341,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t qdesc0 = sdesc_sw128(sq, 16, 1024);
       const uint64_t kdesc0 = sdesc_sw128(sk0, 16, 1024);
       const uint64_t vdesc0 = sdesc_sw128(sv0, 16384, 1024);
+      const uint64_t pdesc0 = sdesc_sw128(smem_u32(smem + C::P_OFF), 16, 1024);  // PS only
       auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T -> TMEM cols [128 w, 128 w + 128)
         TRACE_EV(0, w, j);
         const uint64_t qa = qdesc0 + ((w * C::TILE_BYTES) >> 4);
@@ -307,7 +363,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint64_t vb = vdesc0 + (((j % C::VST) * C::VT_BYTES) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          if (PAIR)
+          if (PS) {  // A = P_w from shared memory (K-major, the Q layout)
+            const uint32_t poff = ((w * 32768) + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+            if (PAIR)
+              mma_ss_2sm(tmem + 256 + w * 128, pdesc0 + poff, vb + ((kk * 2048) >> 4), idesc_o, (j > 0) || (kk > 0));
+            else
+              mma_ss(tmem + 256 + w * 128, pdesc0 + poff, vb + ((kk * 2048) >> 4), idesc_o, (j > 0) || (kk > 0));
+          } else if (PAIR)
             mma_ts_2sm(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, vb + ((kk * 2048) >> 4), idesc_o,
                        (j > 0) || (kk > 0));
           else
@@ -328,7 +390,35 @@ __global__ void __launch_bounds__(THREADS, 1)
       issue_s(0, 0);
       issue_s(1, 0);
       commit(&kempty[0]);
-      for (int j = 0; j < nkv; ++j) {
+      if (PS) {
+        // Per tile j: S_0,j+1 and S_1,j+1 as soon as each group has loaded its S_j (sfree, early in
+        // the group's softmax), then PV_0,j and PV_1,j as each P_j lands in shared memory.  All
+        // waits suspend (try_wait): a polling issuer takes issue slots from the softmax warps.
+        for (int j = 0; j < nkv; ++j) {
+          const bool more = j + 1 < nkv;
+          if (more) {
+            mbar_wait(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
+            mbar_wait(&sfree[0], j & 1);
+            tc_fence_after();
+            issue_s(0, j + 1);
+            mbar_wait(&sfree[1], j & 1);
+            tc_fence_after();
+            issue_s(1, j + 1);
+            commit(&kempty[(j + 1) % C::KST]);
+          }
+          mbar_wait(&vfull[j % C::VST], (j / C::VST) & 1);
+          mbar_wait(&pfull[0], j & 1);
+          tc_fence_after();
+          issue_pv(0, j);
+          commit(&pfree[0]);
+          mbar_wait(&pfull[1], j & 1);
+          tc_fence_after();
+          issue_pv(1, j);
+          commit(&pfree[1]);
+          commit(&vempty[j % C::VST]);
+        }
+      }
+      for (int j = 0; j < (PS ? 0 : nkv); ++j) {
         const bool more = j + 1 < nkv;
         // V_j and K_{j+1} landed long ago in steady state: check them before waiting on P (folding
         // these checks into P0's barrier via a helper warp was measured: no gain, see r01_notes.md)
@@ -372,6 +462,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       GS_TMEM_LD32(tS + 64, (*reinterpret_cast<uint32_t(*)[32]>(v + 64)));
       GS_TMEM_LD32(tS + 96, (*reinterpret_cast<uint32_t(*)[32]>(v + 96)));
       tmem_ld_wait();
+      if (PS) {  // S_w,j is in registers: its TMEM columns are free for S_w,j+1
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(mapa_shared(smem_u32(&sfree[w]), 0));
+          else
+            mbar_arrive(&sfree[w]);
+        }
+      }
       if (quarter == 0 && lane == 0) TRACE_EV(3, w, j);
       const bool full = kv_valid == 128;  // warp-uniform: only a request's last tile is partial
       if (!full) {
@@ -397,6 +497,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool need = m_tile > m_run + 8.0f;
       const float alpha = need ? ex2_approx(m_run - m_tile) : 1.0f;
       if (need) m_run = m_tile;
+      uint32_t pk_ps[64];  // PS only
+      float2 acc_ps = make_float2(0.f, 0.f);
+      if constexpr (PS) {  // exp first (registers), then wait for PV_w,j-1 before touching P_w buffer / O_w
+        if (full)
+          acc_ps = exp_pack_regs<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, pk_ps);
+        else
+          acc_ps = exp_pack_regs<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, pk_ps);
+        if (j > 0) {
+          mbar_wait(&pfree[w], (j - 1) & 1);
+          tc_fence_after();
+        }
+      }
       if (j > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
@@ -410,7 +522,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       l_run *= alpha;
       float2 acc;
-      if (full)
+      if (PS) {
+        const int prow_i = quarter * 32 + lane;  // this thread's row of the 128-row tile w
+        store_p_smem(pk_ps, smem_u32(smem + C::P_OFF) + w * 32768 + prow_i * 128, prow_i & 7);
+        fence_proxy_async_smem();  // generic st.shared -> visible to the MMA (async proxy)
+        acc = acc_ps;
+      } else if (full)
         acc = exp_pack_store<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
       else
         acc = exp_pack_store<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
@@ -853,10 +970,17 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
       !make_tma_3d_bf16(&tv, V, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
   static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
+  static const bool ps = [] {  // round-2 experiment: P in shared memory (Cfg PS), d = 128 only
+    const char* e = getenv("GS_ATTN_PS");
+    return e && e[0] == '1';
+  }();
+  const bool use_ps = ps && HD == 128 && osc.nown == 0 && !trace;
   auto kern = osc.nown > 0 ? attn_tc_kernel<HD, POLY8, false, PAIR, true>
               : trace      ? attn_tc_kernel<HD, POLY8, true>
+              : use_ps     ? attn_tc_kernel<HD, POLY8, false, PAIR, false, HD == 128>
                            : attn_tc_kernel<HD, POLY8, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  const int smem_bytes = use_ps ? Cfg<HD, PAIR, HD == 128>::SMEM : C::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
   const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
   dim3 grid(tab.tile_start[tab.nreq] * (PAIR ? 2 : 1), heads);
@@ -864,7 +988,7 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.dynamicSmemBytes = smem_bytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
