@@ -391,30 +391,26 @@ __global__ void __launch_bounds__(THREADS, 1)
       issue_s(1, 0);
       commit(&kempty[0]);
       if (PS) {
-        // Per tile j: S_0,j+1 and S_1,j+1 as soon as each group has loaded its S_j (sfree, early in
-        // the group's softmax), then PV_0,j and PV_1,j as each P_j lands in shared memory.  All
-        // waits suspend (try_wait): a polling issuer takes issue slots from the softmax warps.
+        // Per tile j and group w: S_w,j+1 as soon as the group has loaded S_w,j (sfree, early in its
+        // softmax), then PV_w,j as soon as P_w,j is in shared memory -- group 0 then group 1, so a
+        // group's PV never waits for the other group's softmax.  Waits suspend (try_wait).
         for (int j = 0; j < nkv; ++j) {
           const bool more = j + 1 < nkv;
-          if (more) {
-            mbar_wait(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
-            mbar_wait(&sfree[0], j & 1);
-            tc_fence_after();
-            issue_s(0, j + 1);
-            mbar_wait(&sfree[1], j & 1);
-            tc_fence_after();
-            issue_s(1, j + 1);
-            commit(&kempty[(j + 1) % C::KST]);
-          }
+          if (more) mbar_wait(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
           mbar_wait(&vfull[j % C::VST], (j / C::VST) & 1);
-          mbar_wait(&pfull[0], j & 1);
-          tc_fence_after();
-          issue_pv(0, j);
-          commit(&pfree[0]);
-          mbar_wait(&pfull[1], j & 1);
-          tc_fence_after();
-          issue_pv(1, j);
-          commit(&pfree[1]);
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            if (more) {
+              mbar_wait(&sfree[w], j & 1);
+              tc_fence_after();
+              issue_s(w, j + 1);
+              if (w == 1) commit(&kempty[(j + 1) % C::KST]);
+            }
+            mbar_wait(&pfull[w], j & 1);
+            tc_fence_after();
+            issue_pv(w, j);
+            commit(&pfree[w]);
+          }
           commit(&vempty[j % C::VST]);
         }
       }
@@ -974,11 +970,12 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
     const char* e = getenv("GS_ATTN_PS");
     return e && e[0] == '1';
   }();
-  const bool use_ps = ps && HD == 128 && osc.nown == 0 && !trace;
-  auto kern = osc.nown > 0 ? attn_tc_kernel<HD, POLY8, false, PAIR, true>
-              : trace      ? attn_tc_kernel<HD, POLY8, true>
-              : use_ps     ? attn_tc_kernel<HD, POLY8, false, PAIR, false, HD == 128>
-                           : attn_tc_kernel<HD, POLY8, false>;
+  const bool use_ps = ps && HD == 128 && osc.nown == 0;
+  auto kern = osc.nown > 0        ? attn_tc_kernel<HD, POLY8, false, PAIR, true>
+              : trace && use_ps ? attn_tc_kernel<HD, POLY8, true, PAIR, false, HD == 128>
+              : trace           ? attn_tc_kernel<HD, POLY8, true>
+              : use_ps          ? attn_tc_kernel<HD, POLY8, false, PAIR, false, HD == 128>
+                                : attn_tc_kernel<HD, POLY8, false>;
   const int smem_bytes = use_ps ? Cfg<HD, PAIR, HD == 128>::SMEM : C::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
