@@ -10,6 +10,14 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
+def max_row_rel_l2(a, b):
+    """Largest per-row relative L2 error max_r |a_r - b_r| / |b_r| (rows = tokens), reported beside
+    the whole-tensor rel-L2 of the north star."""
+    a = np.asarray(a, np.float64).reshape(len(a), -1)
+    b = np.asarray(b, np.float64).reshape(len(b), -1)
+    return float(np.max(np.linalg.norm(a - b, axis=1) / np.maximum(np.linalg.norm(b, axis=1), 1e-300)))
+
+
 def bf16_bits(x):
     """fp64/fp32 array -> bf16 bit patterns (RNE)."""
     return rng.f32_to_bf16_bits(np.asarray(x, np.float32))

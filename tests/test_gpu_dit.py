@@ -10,7 +10,7 @@ import pytest
 from oracle import dit
 from synth import models as sm
 from synth import rng
-from tests.gpu_util import rel_l2
+from tests.gpu_util import max_row_rel_l2, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -122,6 +122,33 @@ def test_step_batched_varlen_images_match_oracle(gs):
                         shape.heads)
     for a, b, r in zip(z0, z1, ref):
         assert rel_l2(b.astype(np.float64) - a, r - a) < TOL
+
+
+@pytest.mark.slow
+def test_step_config2_wan13b_full_depth(gs):
+    """"Full-step parity at full depth is done at configs 1-2".  Config 2a: four
+    1024^2 images (4 x 4096 tokens) batched at different timesteps through all 30 Wan-1.3B-shaped
+    layers, one step, latent delta vs oracle dit_steps (48.7 TFLOP fp64 on the host)."""
+    shape = sm.WAN_1_3B
+    ctx = gs.Context(device=0)
+    mid = _mk(ctx, shape)
+    reqs = [ctx.submit(mid, 1024, 1024, 1, 50, 1000 + i, [0]) for i in range(4)]
+    ctx.run_steps([reqs[1]], [0], 2)            # requests at step indices 0, 2, 0, 0 ...
+    ctx.run_steps([reqs[3]], [0], 7)            # ... and 7
+    z0 = [ctx.read_latent(r) for r in reqs]
+    assert ctx.run_steps(reqs, [0], 1) == 1
+    z1 = [ctx.read_latent(r) for r in reqs]
+    ctx.close()
+    glob = sm.as_f64(sm.global_params(shape))
+    blocks = [sm.as_f64(sm.block_params(shape, l)) for l in range(shape.layers)]
+    grids = [sm.token_grid(1024, 1024)] * 4
+    ref = dit.dit_steps([z.astype(np.float64) for z in z0], grids, [0, 2, 0, 7], 50, 1, glob, blocks,
+                        shape.heads)
+    for i, (a, b, r) in enumerate(zip(z0, z1, ref)):
+        err = rel_l2(b.astype(np.float64) - a, r - a)
+        worst = max_row_rel_l2(b.astype(np.float64) - a, r - a)
+        print(f"config2 step request {i}: rel-L2 {err:.3e}, worst row {worst:.3e}")
+        assert err < TOL, (i, err)
 
 
 # ----------------------------------------------------------------------------- T4 bit-exactness

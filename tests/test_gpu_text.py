@@ -159,10 +159,24 @@ def test_multi_step_cfg_matches_oracle(gs):
     glob, blocks = _oracle_params(shape)
     pc = rng.bf16_bits_to_f64(sm.prompt_embeds(shape, 78, 0))
     pu = rng.bf16_bits_to_f64(sm.prompt_embeds(shape, 78, 1))
+    g = 2.0
+    ctxc, ctxu = dit.text_embedding(pc, glob), dit.text_embedding(pu, glob)
+    sig = dit.sigmas(50)
+    z, bound = z0.astype(np.float64), 0.0
+    for i in range(3):
+        # DESIGN.md reading 21: the latent delta is sum_i dsig_i (g v_c,i - (g-1) v_u,i), so
+        # per-branch velocity errors <= TOL |v| add up to TOL * sum_i |dsig_i| (g |v_c,i| +
+        # |g-1| |v_u,i|): the bar is TOL * kappa with kappa that sum over |z3 - z0|.
+        vc = dit.dit_velocity([z], [(1, 16, 16)], [1000.0 * sig[i]], glob, blocks, shape.heads, [ctxc])[0]
+        vu = dit.dit_velocity([z], [(1, 16, 16)], [1000.0 * sig[i]], glob, blocks, shape.heads, [ctxu])[0]
+        bound += abs(sig[i + 1] - sig[i]) * (g * np.linalg.norm(vc) + abs(g - 1) * np.linalg.norm(vu))
+        z = dit.euler(z, dit.cfg_velocity(vc, vu, g), sig[i], sig[i + 1])
     ref = dit.dit_steps([z0.astype(np.float64)], [(1, 16, 16)], [0], 50, 3, glob, blocks, shape.heads,
-                        prompts=[(pc, pu)], cfg=[2.0])[0]
+                        prompts=[(pc, pu)], cfg=[g])[0]
+    np.testing.assert_allclose(z, ref, rtol=0, atol=1e-12)   # the unrolled loop is dit_steps
+    kappa = bound / np.linalg.norm(ref - z0)
     err = rel_l2(z3.astype(np.float64) - z0, ref - z0)
-    assert err < 2 * TOL, err
+    assert err < TOL * kappa, (err, kappa)
 
 
 def test_submit_contract_for_text_models(gs):

@@ -485,3 +485,122 @@ def test_steps_with_cfg_scale_one_equals_cond_only():
     g0 = dit.dit_steps([z], [(1, 3, 4)], [3], 50, 1, glob, blocks, shape.heads, prompts=[(pc, pu)],
                        cfg=[0.0])[0]
     np.testing.assert_allclose(g0, c, rtol=0, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- whole-block / time-MLP brute force
+# Scalar math.fsum re-statements of SURVEY.md §8(c) "Block" steps 1-7 and "Step" (time MLP),
+# written from the text, not from oracle/dit.py: they pin the q/k branch (RMSNorm over the FULL
+# D, the gains g_q / g_k applied before RoPE, the per-axis RoPE slot split and frequencies, the
+# request-local (f, h, w) positions) and the time MLP's first Linear + SiLU.
+def _fs_ln(row):
+    mu = math.fsum(row) / len(row)
+    var = math.fsum((t - mu) ** 2 for t in row) / len(row)
+    return [(t - mu) / math.sqrt(var + 1e-6) for t in row]
+
+
+def _fs_lin(row, w, b):
+    return [math.fsum(row[c] * w[o][c] for c in range(len(row))) + b[o] for o in range(len(w))]
+
+
+def _fs_rope(vec, pos, d):
+    """Consecutive pairs (2j, 2j+1) rotated by theta = pos_a * 10000^(-2j'/m_a); slots
+    [d/2 - 2 floor(d/6), floor(d/6), floor(d/6)] for axes (f, h, w), j' the slot within its axis,
+    m_a = 2 * slots_a (SURVEY.md §8(c) Block step 4)."""
+    s = d // 6
+    slots = [d // 2 - 2 * s, s, s]
+    out, pair = list(vec), 0
+    for a in range(3):
+        for jj in range(slots[a]):
+            th = pos[a] * 10000.0 ** (-2.0 * jj / (2 * slots[a]))
+            x0, x1 = vec[2 * pair], vec[2 * pair + 1]
+            out[2 * pair] = x0 * math.cos(th) - x1 * math.sin(th)
+            out[2 * pair + 1] = x0 * math.sin(th) + x1 * math.cos(th)
+            pair += 1
+    return out
+
+
+def _fs_gelu(u):
+    return 0.5 * u * (1.0 + math.tanh(math.sqrt(2.0 / math.pi) * (u + 0.044715 * u ** 3)))
+
+
+def _fs_block(x, blk, e_req, reqs, H):
+    N, D = len(x), len(x[0])
+    d = D // H
+    w_qkv, b_qkv = blk["w_qkv"].tolist(), blk["b_qkv"].tolist()
+    gq, gk = blk["g_q"].tolist(), blk["g_k"].tolist()
+    out = [None] * N
+    for r, (off, n, grid) in enumerate(reqs):
+        F_, Ht, Wt = grid
+        mod = [[blk["mod"][c][i] + e_req[r][c][i] for i in range(D)] for c in range(6)]
+        sh1, sc1, g1, sh2, sc2, g2 = mod
+        q, k, v = [], [], []
+        for t in range(n):
+            a = [ln * (1 + sc1[i]) + sh1[i] for i, ln in enumerate(_fs_ln(x[off + t]))]
+            y = _fs_lin(a, w_qkv, b_qkv)
+            pos = (t // (Ht * Wt), (t // Wt) % Ht, t % Wt)   # request-local index -> (f, h, w)
+            qr, kr = y[:D], y[D:2 * D]
+            rq = math.sqrt(math.fsum(c * c for c in qr) / D + 1e-6)   # RMS over the full D
+            rk = math.sqrt(math.fsum(c * c for c in kr) / D + 1e-6)
+            qn = [qr[i] / rq * gq[i] for i in range(D)]
+            kn = [kr[i] / rk * gk[i] for i in range(D)]
+            q.append([_fs_rope(qn[h * d:(h + 1) * d], pos, d) for h in range(H)])
+            k.append([_fs_rope(kn[h * d:(h + 1) * d], pos, d) for h in range(H)])
+            v.append([y[2 * D + h * d:2 * D + (h + 1) * d] for h in range(H)])
+        for t in range(n):
+            o = []
+            for h in range(H):
+                lg = [math.fsum(q[t][h][c] * k[u][h][c] for c in range(d)) / math.sqrt(d) for u in range(n)]
+                m = max(lg)
+                p = [math.exp(s - m) for s in lg]
+                z = math.fsum(p)
+                o += [math.fsum(p[u] * v[u][h][c] for u in range(n)) / z for c in range(d)]
+            ao = _fs_lin(o, blk["w_o"].tolist(), blk["b_o"].tolist())
+            x1 = [x[off + t][i] + g1[i] * ao[i] for i in range(D)]
+            a2 = [ln * (1 + sc2[i]) + sh2[i] for i, ln in enumerate(_fs_ln(x1))]
+            hdn = [_fs_gelu(u) for u in _fs_lin(a2, blk["w_1"].tolist(), blk["b_1"].tolist())]
+            mo = _fs_lin(hdn, blk["w_2"].tolist(), blk["b_2"].tolist())
+            out[off + t] = [x1[i] + g2[i] * mo[i] for i in range(D)]
+    return np.array(out)
+
+
+def test_block_against_fsum_bruteforce_with_rope_and_gains():
+    """Whole tiny block (D = 24, H = 2, d = 12: RoPE slots (2, 2, 2), frequencies 1 and 1/100)
+    over two requests with non-trivial positions on every axis, strongly non-uniform gains and
+    per-request modulation: catches RMSNorm per head instead of over D, gains after RoPE or
+    dropped, a wrong slot split / frequency / position, batch-global instead of request-local
+    positions, and a swapped modulation chunk."""
+    D, H = 24, 2
+    shape = sm.ModelShape("bf", D, H, 40, 1, weight_seed=17)
+    blk = sm.as_f64(sm.block_params(shape, 0))
+    g = np.random.default_rng(5)
+    blk["g_q"] = 1.0 + g.standard_normal(D)          # gains far from 1: order / scope visible
+    blk["g_k"] = 1.0 + g.standard_normal(D)
+    blk["w_qkv"][:2 * D] *= 3.0                       # sharper logits: RoPE errors move the softmax
+    grids = [(2, 2, 3), (1, 2, 2)]
+    reqs, N = _reqs(grids)
+    x = g.standard_normal((N, D)) * 1.5 + 0.3
+    e = g.standard_normal((2, 6, D)) * 0.4
+    ref = _fs_block(x.tolist(), blk, e.tolist(), reqs, H)
+    np.testing.assert_allclose(dit.dit_block(x, blk, e, reqs, H), ref, rtol=0, atol=1e-12)
+
+
+def test_time_embedding_against_fsum_bruteforce():
+    """e0 = W_t2 SiLU(W_t1 s(t) + b_t1) + b_t2, e = W_tp SiLU(e0) + b_tp with every weight
+    non-zero (SURVEY.md §8(c) "Step"): pins the first Linear and both SiLUs."""
+    shape = sm.ModelShape("t", 16, 2, 32, 1, weight_seed=23)
+    gl = sm.as_f64(sm.global_params(shape))
+    t = 731.25
+    half = 128
+    s = [math.cos(t * 10000.0 ** (-j / half)) for j in range(half)] + \
+        [math.sin(t * 10000.0 ** (-j / half)) for j in range(half)]
+    silu = lambda u: u / (1.0 + math.exp(-u))   # noqa: E731
+    h1 = [silu(u) for u in _fs_lin(s, gl["w_t1"].tolist(), gl["b_t1"].tolist())]
+    e0 = _fs_lin(h1, gl["w_t2"].tolist(), gl["b_t2"].tolist())
+    e = _fs_lin([silu(u) for u in e0], gl["w_tp"].tolist(), gl["b_tp"].tolist())
+    got_e0, got_e = dit.time_embedding(t, gl)
+    np.testing.assert_allclose(got_e0, e0, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(got_e.reshape(-1), e, rtol=0, atol=1e-12)
+    # the first SiLU matters: dropping it changes e0 by far more than the tolerance
+    no_silu = _fs_lin(_fs_lin(s, gl["w_t1"].tolist(), gl["b_t1"].tolist()), gl["w_t2"].tolist(),
+                      gl["b_t2"].tolist())
+    assert np.max(np.abs(np.array(no_silu) - got_e0)) > 1e-3
