@@ -149,48 +149,56 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle sample
-def oracle_sample(workload, reps=1, budget_tokens=None):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: one full DiT
-    block of layer 0 on a single-latent-frame request of the workload's resolution (fewer
-    tokens, same model dims), then extrapolate to one full step by the paper's FLOP model
-    (PAPER.md Tab. arithmetic_intensity; costmodel.py).  Returns (ms_per_full_step, info)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def oracle_sample(workload, rows=32):
+    """Time the fp64 oracle (oracle/dit.py, as it stands) on SURVEY.md §8(d)'s bounded sample of the
+    workload: the row-sampled block of §8(c) "Large configs" on the workload's FULL token grid --
+    LN1 and the K/V projections for all n tokens of the (first) request, then the rest of the block
+    (q, RMSNorm, RoPE, attention over all n keys, O-proj, MLP) for `rows` seed-chosen query rows
+    (first, last and evenly spread rows).  Returns (seconds as run, info); `info` also carries the
+    full-step time extrapolated from the measured fp64 rate (labelled as such)."""
     from oracle import dit
     shape, reqs, _ = WORKLOADS[workload]
-    w, h, _f = reqs[0]
-    grid = sm.token_grid(w, h, 1)
-    if budget_tokens is not None and grid[1] * grid[2] > budget_tokens:
-        rows = max(1, budget_tokens // grid[2])
-        grid = (1, rows, grid[2])
+    w, h, f = reqs[0]
+    grid = sm.token_grid(w, h, f)
     n = grid[0] * grid[1] * grid[2]
     blk = sm.as_f64(sm.block_params(shape, 0))
     g = np.random.default_rng(5)
     x = g.standard_normal((n, shape.dim))
-    e_req = g.uniform(-0.5, 0.5, (1, 6, shape.dim))
-    ctxs = [g.standard_normal((shape.text_len, shape.dim))] if shape.cross_attn else None
-    times = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        dit.dit_block(x, blk, e_req, [(0, n, grid)], shape.heads, ctxs)
-        times.append(time.perf_counter() - t0)
-    t = float(np.median(times))
-
-    def block_flops(ns):
-        f = costmodel.flops_per_block(ns, shape.dim, shape.ffn)
-        if shape.cross_attn:  # cross q/o projections + attention over the text tokens
-            f += sum(4 * m * shape.dim ** 2 + 4 * m * shape.text_len * shape.dim for m in ns)
-        return f
-    f_sample = block_flops([n])
-    full_seqs = [sm.token_grid(*r) for r in reqs]
-    full_n = [a * b * c for a, b, c in full_seqs]
+    e = g.uniform(-0.5, 0.5, (6, shape.dim))
+    sel = np.unique(np.concatenate([[0, n - 1], np.linspace(0, n - 1, rows - 2).astype(int)]))
+    ctx = g.standard_normal((shape.text_len, shape.dim)) if shape.cross_attn else None
+    t0 = time.perf_counter()
+    dit.dit_block_rows(x, blk, e, grid, shape.heads, sel, ctx)
+    t = time.perf_counter() - t0
+    D, F = shape.dim, shape.ffn
+    f_kv = 2 * n * 2 * D * D                                 # K and V projections of all tokens
+    f_rows = len(sel) * (2 * D * D + 4 * n * D + 2 * D * D + 4 * D * F)   # q, attention, O, MLP
+    f_sample = f_kv + f_rows
+    full_n = [int(np.prod(sm.token_grid(*r))) for r in reqs]
     nb = 2 if CFG_SCALE.get(workload, 0.0) > 0 else 1
-    f_step = nb * shape.layers * block_flops(full_n)
-    ms_step = t * 1e3 * f_step / f_sample
-    info = {"sample": (f"oracle dit_block (fp64 numpy) layer 0 of {shape.name} on a {grid} "
-                       f"token grid ({n} tokens, {f_sample / 1e9:.1f} GFLOP) in {t:.2f} s; "
-                       f"extrapolated by FLOPs to one full {shape.layers}-layer step of "
-                       f"{sum(full_n)} tokens ({f_step / 1e12:.1f} TFLOP)"),
-            "sample_s": t, "gflops_fp64": f_sample / t / 1e9}
-    return ms_step, info
+    f_block = costmodel.flops_per_block(full_n, D, F)
+    if shape.cross_attn:
+        f_block += sum(4 * m * D * D + 4 * m * shape.text_len * D for m in full_n)
+    f_step = nb * shape.layers * f_block
+    rate = f_sample / t
+    info = {"sample": (f"oracle dit_block_rows (fp64 numpy, as run) of layer 0 of {shape.name} on the "
+                       f"full {grid} grid ({n} tokens): LN1 + K/V projections of all tokens + the rest "
+                       f"of the block for {len(sel)} sampled query rows ({f_sample / 1e12:.2f} TFLOP)"),
+            "sample_s": round(t, 3), "gflops_fp64": round(rate / 1e9, 2),
+            "extrapolated_full_step_ms": round(f_step / rate * 1e3, 1),
+            "extrapolation": (f"full {shape.layers}-layer step = {f_step / 1e12:.1f} TFLOP at the "
+                              "measured fp64 rate (labelled extrapolation, not a measurement)")}
+    return t, info
 
 
 def host_cores():
@@ -201,25 +209,31 @@ def host_cores():
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle on the host cores, rank 0 only."""
+    """--impl reference: the oracle on the host cores, rank 0 only (other ranks exit 0).  Each
+    step is the bounded sample of oracle_sample() (the same quantity as the GPU arm's
+    cpu_baseline), timed as run: `value` is the measured ms of one sample, so
+    value x steps fits inside the run's own wall clock."""
     if rank != 0:
         return
     times, info = [], None
     for i in range(args.warmup + args.steps):
-        ms, info = oracle_sample(args.workload, reps=1, budget_tokens=args.ref_tokens)
+        t, info = oracle_sample(args.workload)
         if i >= args.warmup:
-            times.append(ms)
+            times.append(t * 1e3)
     v = float(np.mean(times))
-    shape, reqs, _ = WORKLOADS[args.workload]
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms",
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "ms",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": v, "higher_is_better": False,
+            "ms_per_step": round(v, 1), "higher_is_better": False,
             "scaling": "strong" if WORKLOADS[args.workload][2] else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded splitmix64)",
-            "config": {"workload": CONFIG_NAME[args.workload], "sp": 1},
-            "cpu_baseline": {"value": v, "unit": "ms", "cores": host_cores(), "kind": "oracle",
-                             "sample": info["sample"]},
-            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": CONFIG_NAME[args.workload], "sp": 1,
+                       "step": "one bounded oracle sample (see cpu_baseline.sample)"},
+            "cpu_baseline": {"value": round(v, 1), "unit": "ms", "cores": host_cores(), "kind": "oracle",
+                             "cpu_model": cpu_model(), "sample": info["sample"],
+                             "gflops_fp64": info["gflops_fp64"],
+                             "extrapolated_full_step_ms": info["extrapolated_full_step_ms"],
+                             "extrapolation": info["extrapolation"]},
+            "e2e": {"value": round(v, 1), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -240,6 +254,177 @@ def load_traffic(workload, p):
             return json.load(f).get(f"{workload}_sp{p}")
     except Exception:
         return None
+
+
+def kernel_class_rates(st, steps, shape, rows_per_pos, seqlens, heads_local, nb=1):
+    """Attention and GEMM TFLOP/s of the profiled steps from gs_stats per-class events."""
+    attn = st.get("attention", {"ms": 0.0, "n": 0})
+    gemm_ms = sum(v["ms"] for k, v in st.items() if isinstance(v, dict) and k.startswith("gemm"))
+    gemm_n = sum(v["n"] for k, v in st.items() if isinstance(v, dict) and k.startswith("gemm"))
+    af = attn_flops_per_launch(shape, list(seqlens) * nb, heads_local)
+    attn_avg = attn["ms"] / max(attn["n"], 1)
+    gf = shape.layers * costmodel.gemm_flops_per_block(rows_per_pos, shape.dim, shape.ffn)
+    return {"attn_tflops": round(af / (attn_avg * 1e-3) / 1e12, 1) if attn_avg > 0 else None,
+            "attn_ms_per_step": round(attn["ms"] / steps, 3),
+            "attn_launch_ms": round(attn_avg, 4),
+            "gemm_ms_per_step": round(gemm_ms / steps, 3),
+            "gemm_launches_per_step": gemm_n // max(steps, 1),
+            "gemm_flops_per_position_step": gf}
+
+
+def t2i_secondary(gs, torch, pk, steps=25, warmup=3):
+    """The T2I half of the headline metric (BASELINE.json: "... 720p T2V + 1024px T2I"): config 2,
+    4 x 1024^2 images batched on one GPU (Wan-1.3B-shaped, L = 30), device-timed steps with the
+    clocks sampled through a >= 1 s timed region, then one per-kernel-profiled step."""
+    shape, reqs_spec, _ = WORKLOADS["t2i1024"]
+    ctx = gs.Context(device=0)
+    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed)
+    reqs = [ctx.submit(mid, w, h, f, 100, 1000 + r, [0]) for r, (w, h, f) in enumerate(reqs_spec)]
+    ctx.run_steps(reqs, [0], warmup)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(0))
+    ctx.profile(2, True)
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark_start()
+    e0.record(stream)
+    ctx.run_steps(reqs, [0], steps)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / steps
+    step_ms = ctx.stats().get("step_ms", [])
+    ctx.profile(1, True)
+    ctx.run_steps(reqs, [0], 2)
+    st = ctx.stats()
+    ctx.profile(0, False)
+    ctx.close()
+    seqlens = [int(np.prod(sm.token_grid(*r))) for r in reqs_spec]
+    rates = kernel_class_rates(st, 2, shape, sum(seqlens), seqlens, shape.heads)
+    gt = rates["gemm_flops_per_position_step"] / (rates["gemm_ms_per_step"] * 1e-3) / 1e12
+    return {"workload": CONFIG_NAME["t2i1024"], "ms_per_step": round(ms, 3), "steps": steps,
+            "warmup": warmup, "step_cv": round(float(np.std(step_ms) / np.mean(step_ms)), 5),
+            "attn_tflops": rates["attn_tflops"],
+            "attn_frac_sustained": round(rates["attn_tflops"] / pk["bf16_sustained"], 4),
+            "gemm_tflops": round(gt, 1), "gemm_frac_sustained": round(gt / pk["bf16_sustained"], 4),
+            "attn_ms_per_step": rates["attn_ms_per_step"], "gemm_ms_per_step": rates["gemm_ms_per_step"],
+            "clocks": clk}
+
+
+def vae_decode_720p(gs, torch, pk, reps=2):
+    """NEXT-4: the VAE decode stage of config 4's request on ONE GPU (the VAE stage always
+    runs on a single GPU, decoupled from the DiT): a 720x1280 / 81-frame latent (DiT grid 21 x 45 x 80)
+    through the Wan2.1-VAE-shaped decoder to 81 x 720 x 1280 x 3, inputs and outputs
+    resident on the device; device-timed with CUDA events.  TFLOP/s counts the algorithmic conv work
+    (unpadded channels; costmodel.vae_decode_flops).  Paper context (Tab. stage_breakdown):
+    2.47 s VAE decode at 720p for Wan2.2-5B on its own GPU -- another VAE and GPU."""
+    grid = (21, 45, 80)
+    ctx = gs.Context(device=0)
+    vid = ctx.vae_create()
+    lat = torch.randn(int(np.prod(grid)) * 64, device="cuda", dtype=torch.float32)
+    shape = ctx.vae_out_shape(grid)
+    out = torch.empty(shape, device="cuda", dtype=torch.float32)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(0))
+    ctx.vae_decode(vid, lat, grid, out=out)          # warm-up (first-use allocations)
+    ts = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.vae_decode(vid, lat, grid, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ok = bool(torch.isfinite(out).all().item()) and float(out.abs().max().item()) <= 1.0
+    ctx.close()
+    ms = float(np.median(ts))
+    fl = costmodel.vae_decode_flops(grid)
+    tf = fl / (ms * 1e-3) / 1e12
+    return {"workload": "Wan2.1-VAE-shaped decode of config 4's latent: 21x90x160x16 -> 81x720x1280x3, 1 GPU",
+            "ms": round(ms, 2), "reps": reps, "tflops_algorithmic": round(tf, 1),
+            "frac_sustained": round(tf / pk["bf16_sustained"], 4), "flops": fl,
+            "output_in_range": ok,
+            "note": "includes activation-buffer allocation per call and the 96 -> 128 channel padding of the "
+                    "last stage (+33% K and N there); conv work runs on tcgen05 implicit-GEMM kernels",
+            "paper_context": "Tab. stage_breakdown: VAE Dec. 2.47 s at 720p/81f (Wan2.2-5B, RTX PRO 6000)"}
+
+
+def sp8_emulated(gs, torch, pk):
+    """Config 4 at the north-star shape on one GPU: the 720p/81f Wan-14B-shaped request at SP = 8 in
+    the emulated context (8 virtual ranks, each position = 9,450 rows and 5 of the 40 heads; the
+    positions run one after another on this GPU and the all-to-alls are device copies), so the
+    per-position kernels run at exactly the per-GPU shape of an 8-GPU run.  Reports the step time
+    (all 8 positions), the per-position attention / GEMM rates and fractions of the step, then
+    config 4's preempt -> re-shard -> resume at SP = 2 on GPUs {0, 1}: the gs_preempt call, the
+    wait until the in-flight step's boundary, and the SP8 -> SP2 re-shard (gs_resume) with the
+    bytes the plan moves (PAPER.md Tab. preemption_scaling P:794-797 is context: other GPUs, PCIe)."""
+    shape = sm.WAN_14B
+    p, n = 8, int(np.prod(sm.token_grid(1280, 720, 81)))
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed)
+    ranks = list(range(p))
+    req = ctx.submit(mid, 1280, 720, 81, 50, 1000, ranks)
+    ctx.run_steps([req], ranks, 1)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr(0))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    ctx.run_steps([req], ranks, 1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1)
+    ctx.profile(1, True)
+    ctx.run_steps([req], ranks, 1)
+    st = ctx.stats()
+    ctx.profile(0, False)
+    rates = kernel_class_rates(st, 1, shape, n // p, [n], shape.heads // p)
+    gt = rates["gemm_flops_per_position_step"] * p / (rates["gemm_ms_per_step"] * 1e-3) / 1e12
+    a2a_ms = sum(v["ms"] for k, v in st.items() if isinstance(v, dict) and k.startswith("a2a"))
+    # preempt a run in flight: the call itself, then the wait for the step boundary
+    t = ctx.run_steps_async([req], ranks, 2)
+    time.sleep(0.5)
+    c0 = time.perf_counter()
+    ctx.preempt(req)
+    c1 = time.perf_counter()
+    ran = ctx.wait(t)
+    c2 = time.perf_counter()
+    assert ctx.query(req)["state"] == gs.REQ_PAUSED
+    calls = []
+    for _ in range(200):  # the call on a paused request (flag + state under the table lock)
+        a = time.perf_counter()
+        ctx.preempt(req)
+        calls.append(time.perf_counter() - a)
+    plan_bytes, into_one = 0, 0
+    for me in range(8):
+        xs = gs.plan_reshard(n, 64, ranks, [0, 1], me)
+        plan_bytes += sum(x["width"] * 4 for x in xs if x["op"] == gs.XFER_SEND)
+        into_one = max(into_one, sum(x["width"] * 4 for x in xs if x["op"] == gs.XFER_RECV))
+    torch.cuda.synchronize()
+    r0 = time.perf_counter()
+    ctx.resume(req, [0, 1])
+    r1 = time.perf_counter()
+    ok = ctx.run_steps([req], [0, 1], 1) == 1
+    ctx.close()
+    return {"workload": "config4 720x1280 81f Wan-14B-shaped at SP=8, emulated on 1 GPU "
+                        "(per-position shapes of the 8-GPU run; exchanges as device copies)",
+            "step_ms_all_positions": round(step_ms, 2),
+            "position_step_ms_est": round(step_ms / p, 2),
+            "attn_tflops_per_launch": rates["attn_tflops"],
+            "attn_frac_sustained": round(rates["attn_tflops"] / pk["bf16_sustained"], 4),
+            "attn_frac_of_step": round(rates["attn_ms_per_step"] / step_ms, 4),
+            "gemm_tflops": round(gt, 1), "gemm_frac_sustained": round(gt / pk["bf16_sustained"], 4),
+            "gemm_frac_of_step": round(rates["gemm_ms_per_step"] / step_ms, 4),
+            "a2a_copy_ms_per_step": round(a2a_ms, 3),
+            "preempt": {"call_us_in_flight": round((c1 - c0) * 1e6, 1),
+                        "call_us_median": round(float(np.median(calls)) * 1e6, 2),
+                        "until_step_boundary_ms": round((c2 - c1) * 1e3, 1), "steps_run_before_pause": ran,
+                        "paper_context": "Tab. preemption_scaling: pause 3.0-3.4 us (P:794-797)"},
+            "resume_sp8_to_sp2": {"ms": round((r1 - r0) * 1e3, 3), "bytes_moved": plan_bytes,
+                                  "max_bytes_into_one_gpu": into_one, "run_after_ok": ok,
+                                  "nvlink_lower_bound_us": round(into_one / 900e9 * 1e6, 1),
+                                  "how": "gs_resume wall clock (plan + device copies on one GPU, synchronised)",
+                                  "paper_context": "Tab. preemption_scaling: resume 0.036-0.868 ms (P:794-797)"}}
 
 
 def run_gpu(args, rank, world, local_rank):
@@ -408,11 +593,22 @@ def run_gpu(args, rank, world, local_rank):
         if bound == "tensor":
             kernels[k]["frac_of_burst"] = round(ach / pk["bf16"], 4)
 
+    extra = {}
+    if world == 1 and not args.no_secondary:
+        ctx.close()
+        ctx = None
+        torch.cuda.empty_cache()
+        extra["t2i1024"] = t2i_secondary(gs, torch, pk)
+        extra["sp8_emulated"] = sp8_emulated(gs, torch, pk)
+        extra["vae_decode_720p"] = vae_decode_720p(gs, torch, pk)
+
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        ms_cpu, info = oracle_sample(args.workload, reps=1, budget_tokens=args.ref_tokens)
-        cpu = {"value": ms_cpu, "unit": "ms", "cores": host_cores(), "kind": "oracle",
-               "sample": info["sample"], "gflops_fp64": round(info["gflops_fp64"], 2)}
+        t_cpu, info = oracle_sample(args.workload)
+        cpu = {"value": round(t_cpu * 1e3, 1), "unit": "ms", "cores": host_cores(), "kind": "oracle",
+               "cpu_model": cpu_model(), "sample": info["sample"], "gflops_fp64": info["gflops_fp64"],
+               "extrapolated_full_step_ms": info["extrapolated_full_step_ms"],
+               "extrapolation": info["extrapolation"]}
 
     line = {
         "metric": METRIC, "value": round(ms_step, 3), "unit": "ms", "n_gpus": world,
@@ -450,11 +646,13 @@ def run_gpu(args, rank, world, local_rank):
         "clocks": clk,
         "cpu_baseline": cpu,
     }
+    line.update(extra)
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
-    ctx.close()
+    if ctx is not None:
+        ctx.close()
 
 
 def main():
@@ -467,9 +665,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--prof-steps", type=int, default=2,
                     help="extra per-kernel-profiled steps after the timed region (breakdown, roofline)")
-    ap.add_argument("--ref-tokens", type=int, default=1200,
-                    help="token budget of the oracle sample (bounded CPU time)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the N=1 secondary objects (t2i1024, sp8_emulated with preempt/resume)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -38,6 +38,7 @@ extern "C" {
 
 typedef struct gs_ctx gs_ctx;
 typedef uint64_t gs_req;
+typedef uint64_t gs_ticket; /* an asynchronous run (gs_run_steps_async / gs_wait) */
 
 enum {
   GS_OK = 0,
@@ -49,7 +50,10 @@ enum {
   GS_EUNSUPPORTED = -6   /* configuration not supported by this build                       */
 };
 
-enum { GS_REQ_PLACED = 0, GS_REQ_RUNNING = 1, GS_REQ_PAUSED = 2, GS_REQ_DONE = 3 };
+/* Request states.  QUEUED: submitted, holds no GPU (|X_r| = 0) until gs_place; PLACED: its
+ * latent is sharded on a GPU set and it may run; RUNNING: inside a run; PAUSED: preempted at a step
+ * boundary, latent kept in device memory (§4.2) until gs_resume; DONE: all steps run. */
+enum { GS_REQ_PLACED = 0, GS_REQ_RUNNING = 1, GS_REQ_PAUSED = 2, GS_REQ_DONE = 3, GS_REQ_QUEUED = 4 };
 
 /* DiT model shape (SURVEY.md §8 shape table; Wan2.1-style block, reading 1).
  * Weights are generated on the device from the counter RNG:
@@ -109,11 +113,19 @@ int gs_model_create(gs_ctx* ctx, const gs_model_desc* desc, int* model_id);
 int gs_get_weight(gs_ctx* ctx, int model, int layer, const char* name, void* host, size_t bytes);
 
 /* ------------------------------------------------------------------ requests */
-/* Submit a request: resolution w x h (multiples of 16), frames (1 for images, = 1 mod 4),
- * `steps` denoising steps (sigma schedule of DESIGN.md reading 5).  The initial latent
- * z_T [n, lat] fp32 (token-major, n = (1 + (frames-1)/4) * (h/16) * (w/16)) is generated
- * from noise_seed, or copied from init_latent (host, n*lat floats) if non-NULL.  The request
- * is placed token-sharded on `ranks` (p = nranks in {1,2,4,8}, distinct, in SP order). */
+/* Submit a request: "submit a request's resolution, frames and steps" (BASELINE.json north_star);
+ * a request is a fixed number of reverse-diffusion steps (§2.1 Eq. reverse).  Resolution
+ * w x h (multiples of 16), frames (1 for images, = 1 mod 4), `steps` denoising steps (sigma
+ * schedule of DESIGN.md reading 5).  The initial latent z_T [n, lat] fp32 (token-major,
+ * n = (1 + (frames-1)/4) * (h/16) * (w/16)) is generated from noise_seed, or copied from
+ * init_latent (host, exactly n*lat floats, borrowed for the call) if non-NULL.
+ * Placement: with ranks != NULL the request is placed at once, token-sharded on `ranks`
+ * (p = nranks in {1,2,4,8}, distinct, in SP order; = gs_submit + gs_place).  With ranks == NULL and
+ * nranks == 0 it is QUEUED: it holds no GPU until gs_place (the scheduler's start action).
+ * Multi-process (NCCL) contexts: gs_submit is collective over the WHOLE job (every process submits
+ * every request, so request ids agree job-wide and any process can later receive a shard on
+ * resume; checked with one all-reduce, GS_ESTATE on a mismatch).  Errors: GS_EINVAL bad shape /
+ * ranks, GS_ENOMEM, GS_ECUDA. */
 int gs_submit(gs_ctx* ctx, int model, int width, int height, int frames, int steps,
               uint64_t noise_seed, const float* init_latent, const int* ranks, int nranks,
               gs_req* out);
@@ -121,31 +133,102 @@ int gs_submit(gs_ctx* ctx, int model, int width, int height, int frames, int ste
  * VideoState keeps the prompt embeddings).  cfg_scale > 0 runs classifier-free guidance with
  * guidance g = cfg_scale (a cond and an uncond branch per step, v = v_u + g (v_c - v_u), DESIGN.md
  * reading 21); cfg_scale <= 0 runs the cond branch only.  prompt_embeds: host bf16
- * [nb][text_len][text_dim] (nb = 2 with CFG: cond, then uncond), or NULL for the synthetic prompt of
- * prompt_seed.  Other arguments as gs_submit. */
+ * [nb][text_len][text_dim] (nb = 2 with CFG: cond, then uncond; exactly that many elements are
+ * read), or NULL for the synthetic prompt of prompt_seed.  Other
+ * arguments as gs_submit. */
 int gs_submit_text(gs_ctx* ctx, int model, int width, int height, int frames, int steps,
                    uint64_t noise_seed, uint64_t prompt_seed, float cfg_scale,
                    const float* init_latent, const void* prompt_embeds, const int* ranks,
                    int nranks, gs_req* out);
-/* Run k steps of a batch of requests (all placed on exactly `ranks`, same model, not paused,
- * k <= remaining steps of each).  Returns after the last step completed or after the step
- * boundary at which a preemption was requested (steps actually run -> *steps_run).
- * Bit-exact w.r.t. SP degree, batch composition and preempt/resume. */
+/* First placement of a QUEUED request on `ranks` (the "start" action of X_r(t): |X_r| goes from 0
+ * to p, §4.4; images on one GPU, videos on p in {1,2,4,8}): allocates the latent
+ * shards and writes z_T.  Collective over the processes owning `ranks`.  GS_ESTATE if the request
+ * is not QUEUED or a rank belongs to an in-flight run; GS_EINVAL bad ranks. */
+int gs_place(gs_ctx* ctx, gs_req req, const int* ranks, int nranks);
+/* Run k steps of a batch of requests: the "start / continue" actions for one scheduling round
+ * (§4.4); one step = one DiT forward + Euler update (§2.1).  Preconditions
+ * (GS_ESTATE otherwise): every request is PLACED on exactly `ranks`, all use the same model, no
+ * rank belongs to another in-flight run (capacity / no-overlap rule, Eq. capacity, Alg.1
+ * P:498), and in multi-process mode this process owns one of `ranks`; k <= remaining steps of each
+ * (GS_EINVAL).  Returns after the last step, or after the step boundary at which a preemption was
+ * requested (§1: preemption only at step boundaries); steps actually run -> *steps_run.
+ * Bit-exact w.r.t. SP degree, batch composition and preempt/resume.
+ * = gs_run_steps_async + gs_wait. */
 int gs_run_steps(gs_ctx* ctx, const gs_req* reqs, int nreq, const int* ranks, int nranks, int k,
                  int* steps_run);
-/* Request preemption; effective at the next step boundary (or immediately if idle).  Safe to
- * call from another thread while gs_run_steps is running. steps_done_out may be NULL. */
+/* Asynchronous gs_run_steps: validates and claims the GPU set, then runs the k steps on a worker
+ * thread of the context (on the stream of ranks[0]) and returns at once with a ticket.  Runs on
+ * disjoint GPU sets proceed concurrently ("each GPU either processes one batch or is idle",
+ * P:390-398 §4.3; disjoint SP groups).  Validation errors are returned here (no ticket);
+ * errors of the run itself are returned by gs_wait.  Every ticket must be waited for. */
+int gs_run_steps_async(gs_ctx* ctx, const gs_req* reqs, int nreq, const int* ranks, int nranks,
+                       int k, gs_ticket* ticket);
+/* Wait for a run: returns its status (first error of the run, message in gs_last_error) and the
+ * steps it ran (steps_run may be NULL); releases its GPU set.  GS_EINVAL for an unknown ticket. */
+int gs_wait(gs_ctx* ctx, gs_ticket ticket, int* steps_run);
+/* 1 if the run has finished (gs_wait will not block), 0 if it is still running, GS_EINVAL for
+ * an unknown ticket. */
+int gs_ticket_done(gs_ctx* ctx, gs_ticket ticket);
+/* Request preemption (pause): "preempting ... at step boundaries; its latent state is retained
+ * in device memory" (§1; §4.2; "a pause requested mid-step takes effect at
+ * the current step's completion").  If the request is in a run, the run stops after its current
+ * step; otherwise it is paused at once.  Thread-safe (any thread, while runs are in flight).
+ * GS_ESTATE for a DONE request.  steps_done_out (may be NULL) = steps completed so far. */
 int gs_preempt(gs_ctx* ctx, gs_req req, int* steps_done_out);
-/* Resume / reconfigure at a step boundary onto `ranks` (p' = nranks): re-shards the latent
- * (pure copy of contiguous token ranges, interval intersections of old and new shards). */
+/* Resume / reconfigure at a step boundary onto `ranks` (p' = nranks): "resume ... possibly at a
+ * different SP degree" (§4.2, §4.3 runtime SP degree switching; reconfigure
+ * when the request was not paused).  Re-shards the latent (pure copy of contiguous token
+ * ranges, interval intersections of old and new shards).  Collective over
+ * the processes owning old or new ranks.  GS_ESTATE if the request is RUNNING / DONE / QUEUED or a
+ * new rank belongs to an in-flight run (multi-process contexts: an old rank too, since the re-shard
+ * is collective over its process). */
 int gs_resume(gs_ctx* ctx, gs_req req, const int* ranks, int nranks);
 /* state in GS_REQ_*; ranks_out (host, >= 8 ints) may be NULL. */
 int gs_query(gs_ctx* ctx, gs_req req, int* steps_done, int* steps_total, int* nranks,
              int* ranks_out, int* state, int* n_tokens);
-/* Copy the latent [n, lat] fp32 to host: every shard owned by this process is written to
- * its token range (in emulated mode: the whole latent). */
+/* Copy the latent [n, lat] fp32 to host (nfloats must equal n*lat): every shard owned by this
+ * process is written to its token range (in emulated mode: the whole latent).  GS_ESTATE while the
+ * request is RUNNING or QUEUED. */
 int gs_read_latent(gs_ctx* ctx, gs_req req, float* host, size_t nfloats);
+/* Free a request's device state (GS_ESTATE while RUNNING). */
 int gs_release(gs_ctx* ctx, gs_req req);
+
+/* ------------------------------------------------------------------ VAE decode (NEXT-4)
+ * The pipeline stage after the DiT: "a VAE for latent encoding/decoding" (§2.1), decoupled
+ * from the DiT and always run on a single GPU (§4.3; Tab. stage_breakdown).
+ * Decoder shape: Wan2.1-VAE-like causal 3-D conv decoder (DESIGN.md §NEXT-4 readings V1-V8; the
+ * module walk of synth/vae.py): de-normalise + unpatchify the DiT latent, 1x1x1 conv, conv_in,
+ * residual blocks, temporal (x2, first-frame rule) and spatial (x2 nearest + conv) upsampling,
+ * RMS norm + SiLU + conv_out, clamp to [-1, 1].  Weights are generated on the device from the
+ * counter RNG (tensor id 200 + 4 * module + slot, seed weight_seed). */
+typedef struct {
+  int z_dim;          /* latent channels (16)                                            */
+  int dims[5];        /* decoder widths (384, 384, 384, 192, 96)                          */
+  int blocks;         /* residual blocks per up stage (3)                                 */
+  int mid_blocks;     /* residual blocks at the latent resolution (2)                     */
+  int temporal_up[3]; /* temporal x2 in up stages 0..2 (1, 1, 0)                          */
+  int out_ch;         /* output channels (3)                                              */
+  uint64_t weight_seed;
+} gs_vae_desc;
+int gs_vae_create(gs_ctx* ctx, const gs_vae_desc* desc, int* vae_id);
+/* Decode one latent on local rank `rank` (a single GPU): latent [F * Ht * Wt, 64] fp32 in DiT token
+ * layout (host, or device memory of the context's device when flags & 1), video
+ * [T_out][16 Ht][16 Wt][out_ch] fp32 (host, or device when flags & 2), T_out = F after the temporal
+ * stages (1 + 4 (F - 1) for the Wan shape).  Activation buffers are taken from and returned to the
+ * context's pool.  GS_EINVAL bad shape; GS_ENOMEM; GS_ECUDA. */
+int gs_vae_decode(gs_ctx* ctx, int vae_id, int rank, const float* latent, int F, int Ht, int Wt, float* video,
+                  int flags);
+/* Decode a request's latent (the stage after its last DiT step) on ONE of its GPUs: the latent is
+ * gathered from its shards onto ranks[0] of the request (emulated contexts; multi-process
+ * contexts need the whole request on this process).  video: host fp32 as gs_vae_decode. */
+int gs_vae_decode_request(gs_ctx* ctx, int vae_id, gs_req req, float* video);
+/* Parity entry point: one causal 3-D convolution (oracle/vae.py causal_conv3d) on device buffers,
+ * x bf16 [T][H][W][Cp], w bf16 [Coutp][kt][kh][kw][Cp], bias bf16 [Coutp], resid bf16
+ * [T][H][W][Coutp] or NULL, out per mode (0 bf16 [T][H][W][out_cs]; 1 temporal interleave;
+ * 2 fp32 clamp [T][H][W][out_real]). */
+int gs_debug_conv3d(gs_ctx* ctx, const void* x, const void* w, const void* bias, const void* resid, void* out,
+                    int T, int H, int W, int Cp, int kt, int kh, int kw, int Coutp, int out_cs, int mode,
+                    int out_real);
 
 /* ------------------------------------------------------------------ measurement */
 /* enable = 1: per-kernel-class and per-step CUDA-event timing inside gs_run_steps (events on the

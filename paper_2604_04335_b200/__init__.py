@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgs.so")
 
 GS_OK, GS_EINVAL, GS_ESTATE, GS_ENOMEM, GS_ECUDA, GS_ENCCL, GS_EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6
-REQ_PLACED, REQ_RUNNING, REQ_PAUSED, REQ_DONE = 0, 1, 2, 3
+REQ_PLACED, REQ_RUNNING, REQ_PAUSED, REQ_DONE, REQ_QUEUED = 0, 1, 2, 3, 4
 EPI_BF16, EPI_GELU_BF16, EPI_F32, EPI_RESID_F32, EPI_EULER_F32 = 0, 1, 2, 3, 4
 
 
@@ -29,6 +29,13 @@ class ModelDesc(ctypes.Structure):
                 ("rope_theta", ctypes.c_float), ("eps", ctypes.c_float),
                 ("flow_shift", ctypes.c_float), ("weight_seed", ctypes.c_uint64),
                 ("cross_attn", ctypes.c_int), ("text_len", ctypes.c_int), ("text_dim", ctypes.c_int)]
+
+
+class VaeDesc(ctypes.Structure):
+    """gs_vae_desc (include/gs.h): the VAE decoder shape (synth/vae.py VaeShape)."""
+    _fields_ = [("z_dim", ctypes.c_int), ("dims", ctypes.c_int * 5), ("blocks", ctypes.c_int),
+                ("mid_blocks", ctypes.c_int), ("temporal_up", ctypes.c_int * 3), ("out_ch", ctypes.c_int),
+                ("weight_seed", ctypes.c_uint64)]
 
 
 class Xfer(ctypes.Structure):
@@ -61,6 +68,10 @@ _SIG = {
     "gs_submit_text": [_P, _I, _I, _I, _I, _I, _U64, _U64, ctypes.c_float, _FP, _P, _IP, _I,
                        ctypes.POINTER(_U64)],
     "gs_run_steps": [_P, ctypes.POINTER(_U64), _I, _IP, _I, _I, _IP],
+    "gs_run_steps_async": [_P, ctypes.POINTER(_U64), _I, _IP, _I, _I, ctypes.POINTER(_U64)],
+    "gs_wait": [_P, _U64, _IP],
+    "gs_ticket_done": [_P, _U64],
+    "gs_place": [_P, _U64, _IP, _I],
     "gs_preempt": [_P, _U64, _IP],
     "gs_resume": [_P, _U64, _IP, _I],
     "gs_query": [_P, _U64, _IP, _IP, _IP, _IP, _IP, _IP],
@@ -81,6 +92,10 @@ _SIG = {
     "gs_plan_peer": [_I, _I, _I, _IP, _I, _I, ctypes.POINTER(ctypes.c_longlong), _IP,
                      ctypes.POINTER(ctypes.c_longlong)],
     "gs_set_option": [_P, ctypes.c_char_p, ctypes.c_longlong],
+    "gs_vae_create": [_P, ctypes.POINTER(VaeDesc), _IP],
+    "gs_vae_decode": [_P, _I, _I, _P, _I, _I, _I, _P, _I],
+    "gs_vae_decode_request": [_P, _I, _U64, _P],
+    "gs_debug_conv3d": [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I, _I],
 }
 _lib = None
 
@@ -237,33 +252,62 @@ class Context:
         return out
 
     # ---------------------------------------------------------------- requests
+    @staticmethod
+    def _n_tokens(width, height, frames):
+        return (1 + (frames - 1) // 4) * (height // 16) * (width // 16)
+
+    def _latent_arg(self, init_latent, width, height, frames, lat=64):
+        """The caller's initial latent as a float32 [n_tokens * lat] buffer (size checked here:
+        the C side reads exactly that many floats)."""
+        if init_latent is None:
+            return None, None
+        arr = np.ascontiguousarray(init_latent, dtype=np.float32)
+        n = self._n_tokens(width, height, frames)
+        if arr.size != n * lat:
+            raise ValueError(f"init_latent has {arr.size} floats, the request needs {n} x {lat}")
+        return arr, arr.ctypes.data_as(_FP)
+
+    def _ranks_arg(self, ranks):
+        """ranks=None submits a QUEUED request (placed later with place())."""
+        if ranks is None:
+            return None, 0
+        return _ints(ranks), len(ranks)
+
     def submit(self, model, width, height, frames, steps, noise_seed, ranks, init_latent=None):
         rid = ctypes.c_uint64()
-        lat = None
-        if init_latent is not None:
-            init_latent = np.ascontiguousarray(init_latent, dtype=np.float32)
-            lat = init_latent.ctypes.data_as(_FP)
+        keep, lat = self._latent_arg(init_latent, width, height, frames)
+        rk, nr = self._ranks_arg(ranks)
         self._ck(self._lib.gs_submit(self._h, model, width, height, frames, steps, noise_seed, lat,
-                                     _ints(ranks), len(ranks), ctypes.byref(rid)))
+                                     rk, nr, ctypes.byref(rid)))
+        del keep
         return rid.value
 
     def submit_text(self, model, width, height, frames, steps, noise_seed, ranks, prompt_seed=0,
-                    cfg_scale=0.0, prompt_embeds=None, init_latent=None):
+                    cfg_scale=0.0, prompt_embeds=None, init_latent=None, text_len=None, text_dim=None):
         """Cross-attention models: prompt_embeds = uint16 (bf16 bits) [nb, text_len, text_dim] or
-        None for the synthetic prompt of prompt_seed; cfg_scale > 0 enables CFG (nb = 2)."""
+        None for the synthetic prompt of prompt_seed; cfg_scale > 0 enables CFG (nb = 2).  The
+        prompt's shape is checked against nb (and text_len / text_dim when given)."""
         rid = ctypes.c_uint64()
-        lat = None
-        if init_latent is not None:
-            init_latent = np.ascontiguousarray(init_latent, dtype=np.float32)
-            lat = init_latent.ctypes.data_as(_FP)
+        keep, lat = self._latent_arg(init_latent, width, height, frames)
         pe = None
         if prompt_embeds is not None:
             prompt_embeds = np.ascontiguousarray(prompt_embeds, dtype=np.uint16)
+            nb = 2 if cfg_scale > 0 else 1
+            if prompt_embeds.ndim != 3 or prompt_embeds.shape[0] != nb:
+                raise ValueError(f"prompt_embeds must be [{nb}, text_len, text_dim] (cfg_scale={cfg_scale})")
+            if (text_len is not None and prompt_embeds.shape[1] != text_len) or \
+                    (text_dim is not None and prompt_embeds.shape[2] != text_dim):
+                raise ValueError(f"prompt_embeds shape {prompt_embeds.shape} != [{nb}, {text_len}, {text_dim}]")
             pe = prompt_embeds.ctypes.data_as(ctypes.c_void_p)
+        rk, nr = self._ranks_arg(ranks)
         self._ck(self._lib.gs_submit_text(self._h, model, width, height, frames, steps, noise_seed,
-                                          prompt_seed, cfg_scale, lat, pe, _ints(ranks), len(ranks),
-                                          ctypes.byref(rid)))
+                                          prompt_seed, cfg_scale, lat, pe, rk, nr, ctypes.byref(rid)))
+        del keep
         return rid.value
+
+    def place(self, req, ranks):
+        """First placement of a QUEUED request (include/gs.h gs_place)."""
+        self._ck(self._lib.gs_place(self._h, req, _ints(ranks), len(ranks)))
 
     def run_steps(self, reqs, ranks, k):
         ids = (ctypes.c_uint64 * len(reqs))(*reqs)
@@ -271,6 +315,26 @@ class Context:
         self._ck(self._lib.gs_run_steps(self._h, ids, len(reqs), _ints(ranks), len(ranks), k,
                                         ctypes.byref(done)))
         return done.value
+
+    def run_steps_async(self, reqs, ranks, k):
+        """Start k steps on a worker thread of the context; returns a ticket for wait()."""
+        ids = (ctypes.c_uint64 * len(reqs))(*reqs)
+        t = ctypes.c_uint64()
+        self._ck(self._lib.gs_run_steps_async(self._h, ids, len(reqs), _ints(ranks), len(ranks), k,
+                                              ctypes.byref(t)))
+        return t.value
+
+    def wait(self, ticket):
+        """Wait for an asynchronous run; returns the steps it ran (raises its error)."""
+        done = ctypes.c_int()
+        self._ck(self._lib.gs_wait(self._h, ticket, ctypes.byref(done)))
+        return done.value
+
+    def ticket_done(self, ticket):
+        rc = self._lib.gs_ticket_done(self._h, ticket)
+        if rc < 0:
+            self._ck(rc)
+        return bool(rc)
 
     def preempt(self, req):
         s = ctypes.c_int()
@@ -303,6 +367,62 @@ class Context:
 
     def release(self, req):
         self._ck(self._lib.gs_release(self._h, req))
+
+    # ---------------------------------------------------------------- VAE decode (NEXT-4)
+    def vae_create(self, z_dim=16, dims=(384, 384, 384, 192, 96), blocks=3, mid_blocks=2,
+                   temporal_up=(True, True, False), out_ch=3, weight_seed=4321):
+        d = VaeDesc(z_dim, (ctypes.c_int * 5)(*dims), blocks, mid_blocks,
+                    (ctypes.c_int * 3)(*[int(x) for x in temporal_up]), out_ch, weight_seed)
+        vid = ctypes.c_int()
+        self._ck(self._lib.gs_vae_create(self._h, ctypes.byref(d), ctypes.byref(vid)))
+        return vid.value
+
+    @staticmethod
+    def vae_out_shape(grid, temporal_up=(True, True, False), out_ch=3):
+        F, Ht, Wt = grid
+        t = F
+        for u in temporal_up:
+            if u:
+                t = 1 + 2 * (t - 1)
+        return (t, 16 * Ht, 16 * Wt, out_ch)
+
+    def vae_decode(self, vae, latent, grid, rank=0, out=None, temporal_up=(True, True, False), out_ch=3):
+        """latent: host fp32 [F*Ht*Wt, 64] (numpy) or a CUDA tensor; returns the video
+        [T_out, 16 Ht, 16 Wt, out_ch] fp32 (numpy, or `out` if given: numpy or CUDA tensor)."""
+        shape = self.vae_out_shape(grid, temporal_up, out_ch)
+        flags = 0
+        n = int(np.prod(grid)) * 64
+        if isinstance(latent, np.ndarray):
+            latent = np.ascontiguousarray(latent, dtype=np.float32)
+            if latent.size != n:
+                raise ValueError(f"latent has {latent.size} floats, grid {grid} needs {n}")
+            lp = latent.ctypes.data_as(ctypes.c_void_p)
+        else:
+            if latent.numel() != n:
+                raise ValueError(f"latent has {latent.numel()} floats, grid {grid} needs {n}")
+            lp, flags = latent.data_ptr(), 1
+        if out is None:
+            out = np.empty(shape, dtype=np.float32)
+        if isinstance(out, np.ndarray):
+            if out.size != int(np.prod(shape)) or out.dtype != np.float32 or not out.flags.c_contiguous:
+                raise ValueError(f"out must be a C-contiguous float32 array of shape {shape}")
+            op = out.ctypes.data_as(ctypes.c_void_p)
+        else:
+            op, flags = out.data_ptr(), flags | 2
+        self._ck(self._lib.gs_vae_decode(self._h, vae, rank, lp, *grid, op, flags))
+        return out
+
+    def vae_decode_request(self, vae, req, grid, temporal_up=(True, True, False), out_ch=3):
+        out = np.empty(self.vae_out_shape(grid, temporal_up, out_ch), dtype=np.float32)
+        self._ck(self._lib.gs_vae_decode_request(self._h, vae, req, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    def debug_conv3d(self, x, w, bias, out, T, H, W, Cp, k, Coutp, resid=None, out_cs=None, mode=0,
+                     out_real=0):
+        kt, kh, kw = k
+        self._ck(self._lib.gs_debug_conv3d(self._h, _ptr(x), _ptr(w), _ptr(bias), _ptr(resid), _ptr(out), T, H,
+                                           W, Cp, kt, kh, kw, Coutp, Coutp if out_cs is None else out_cs,
+                                           mode, out_real))
 
     # ---------------------------------------------------------------- measurement
     def profile(self, enable=True, reset=True):

@@ -29,26 +29,31 @@ def headers():
                   glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
-def up_to_date():
-    if not os.path.exists(LIB):
+def up_to_date(lib=LIB):
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
-        return LIB
+def build(force=False, verbose=False, defines=(), lib=LIB):
+    """Compile every source for sm_100a and link `lib`.  `defines` (e.g. "GS_ATTN_ALT=1") build a
+    development variant of the library for A/B runs (tools/kbench.py --lib); numerics-changing
+    choices are compile-time constants, never environment variables."""
+    if not force and up_to_date(lib):
+        return lib
     nd = nccl_dir()
+    tag = "_".join(d.replace("=", "") for d in defines)
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     objs = []
-    os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    bdir = os.path.join(HERE, "build" + ("_" + tag if tag else ""))
+    os.makedirs(bdir, exist_ok=True)
     procs = []
     for src in sources():
-        obj = os.path.join(HERE, "build", os.path.basename(src) + ".o")
+        obj = os.path.join(bdir, os.path.basename(src) + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC",
                "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-               "-c", src, "-o", obj]
+               *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -59,14 +64,16 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {src}:\n{out.decode()}")
         if verbose and out:
             sys.stderr.write(out.decode())
-    link = [nvcc, *ARCH, "-shared", "-o", LIB, *objs,
+    link = [nvcc, *ARCH, "-shared", "-o", lib, *objs,
             "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
             "-Xlinker", "-rpath," + os.path.join(nd, "lib")]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode())
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")), LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, lib=out))

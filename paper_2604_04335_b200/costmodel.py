@@ -46,3 +46,36 @@ def a2a_bytes_per_rank(n_tokens, dim, p):
     """Ulysses all-to-all bytes sent per rank per block: (Q,K,V fwd + O back) * (p-1)/p."""
     local = n_tokens / p
     return 4 * (p - 1) / p * local * dim * 2
+
+
+def vae_decode_flops(grid, dims=(384, 384, 384, 192, 96), blocks=3, mid_blocks=2,
+                     temporal_up=(True, True, False), z_dim=16, out_ch=3):
+    """Convolution FLOPs (2 per multiply-add) of the NEXT-4 VAE decoder for a DiT
+    latent grid (F, Ht, Wt): the algorithmic work of the unpadded channel counts, counted per
+    stage from the decoder's structure (tests/test_costmodel.py checks it against the oracle's
+    executed-conv count)."""
+    F, Ht, Wt = grid
+    T, H, W = F, 2 * Ht, 2 * Wt
+
+    def conv(t, h, w, cin, cout, taps):
+        return 2 * t * h * w * cin * cout * taps
+
+    tot = conv(T, H, W, z_dim, z_dim, 1) + conv(T, H, W, z_dim, dims[0], 27)
+    tot += mid_blocks * 2 * conv(T, H, W, dims[0], dims[0], 27)
+    cin = dims[0]
+    for i in range(4):
+        cout = dims[i + 1]
+        if i >= 1:
+            cin = dims[i] // 2
+        for _ in range(blocks):
+            tot += conv(T, H, W, cin, cout, 27) + conv(T, H, W, cout, cout, 27)
+            if cin != cout:
+                tot += conv(T, H, W, cin, cout, 1)
+            cin = cout
+        if i < 3:
+            if temporal_up[i]:
+                tot += conv(T - 1, H, W, cout, 2 * cout, 3)
+                T = 1 + 2 * (T - 1)
+            H, W = 2 * H, 2 * W
+            tot += conv(T, H, W, cout, cout // 2, 9)
+    return tot + conv(T, H, W, dims[4], out_ch, 27)

@@ -68,11 +68,7 @@ struct SeqTable {
 // half of every K tile (64 keys, the B operand's N half) and half of every V tile (64 of the d
 // columns), halving per-SM shared-memory B reads and L2 -> SM traffic (tools/micro: the UMMA smem
 // read path is 128 B/clk).
-// PS (round-2 experiment, GS_ATTN_PS=1): P goes to shared memory (PV as an SS MMA) so S_{j+1} can
-// be issued as soon as the softmax has loaded S_j, breaking the per-group chain S -> softmax -> P ->
-// PV -> S of v5 (profiles/r01_notes.md; tools/micro/attn_pv_smem_bench.cu: the SS-PV + P-store mix
-// runs at the MMA floor).  Costs 2 x 32 KB of P buffers, paid for with K / V rings of 3 / 2.
-template <int HD, bool PAIR, bool PS = false>
+template <int HD, bool PAIR>
 struct Cfg {
   static constexpr int BOXES = HD / 64;                  // 64-element (128 B) column boxes
   static constexpr int TILE_BYTES = 128 * HD * 2;        // one 128-row Q tile
@@ -80,13 +76,12 @@ struct Cfg {
   static constexpr int KBOX_BYTES = (PAIR ? 64 : 128) * 128;       // one [rows][64] K box
   static constexpr int VT_BYTES = 128 * (PAIR ? HD / 2 : HD) * 2;  // this CTA's part of a V tile
   // K ring deeper than V: a K slot frees after both S MMAs, a V slot only after both PV MMAs
-  static constexpr int KST = PS ? 3 : PAIR ? 4 : (HD == 128 ? 3 : 4);
-  static constexpr int VST = PS ? 2 : PAIR ? 4 : (HD == 128 ? 2 : 4);
+  static constexpr int KST = PAIR ? 4 : (HD == 128 ? 3 : 4);
+  static constexpr int VST = PAIR ? 4 : (HD == 128 ? 2 : 4);
   static constexpr int Q_OFF = 0;
   static constexpr int K_OFF = 2 * TILE_BYTES;
   static constexpr int V_OFF = K_OFF + KST * KT_BYTES;
-  static constexpr int P_OFF = V_OFF + VST * VT_BYTES;          // PS: P_w, 128 rows x 128 keys bf16
-  static constexpr int BAR_OFF = P_OFF + (PS ? 2 * 128 * 128 * 2 : 0);
+  static constexpr int BAR_OFF = V_OFF + VST * VT_BYTES;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
 };
 
@@ -104,7 +99,6 @@ __device__ __forceinline__ constexpr bool poly_pair(int k) {
 // P = exp2(S * scale - m) for the 128 columns of this thread's row, packed to bf16 pairs and
 // stored over the S columns [0, 64) in TMEM (P aliases S).  Returns the fp32 partial row sums.
 // FULL = false is the last (partial) KV tile of a request: masked columns get p = 0 exactly.
-// NCOL = 64: the v6 column half [col0, col0 + 64) of the row (v holds those 64 values).
 template <int POLY8, bool FULL, int NCOL = 128>
 __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], float2 sc2, float2 nm2,
                                                  int kv_valid, uint32_t tS, int col0 = 0) {
@@ -140,61 +134,15 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], floa
   return __fadd2_rn(acc0, acc1);
 }
 
-// PS: the same arithmetic, P stored to this thread's row of the shared-memory P tile in the UMMA
-// K-major 128B-swizzled layout (box b = keys [64 b, 64 b + 64) at b * 16384, row r at r * 128,
-// 16-byte chunk c at (c ^ (r & 7)) * 16), the layout TMA gives Q.
-template <int POLY8, bool FULL, int NCOL>
-__device__ __forceinline__ float2 exp_pack_regs(const uint32_t (&v)[NCOL], float2 sc2, float2 nm2, int kv_valid,
-                                               uint32_t (&pkall)[NCOL / 2]) {
-  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int c = 0; c < NCOL / 32; ++c) {
-    uint32_t* pk = pkall + 16 * c;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int col = c * 32 + 2 * i;
-      const float2 x =
-          __ffma2_rn(make_float2(__uint_as_float(v[col]), __uint_as_float(v[col + 1])), sc2, nm2);
-      float2 p;
-      if (poly_pair<POLY8>(i & 7)) {
-        p = exp2_poly2(x);
-      } else {
-        p.x = ex2_approx(x.x);
-        p.y = ex2_approx(x.y);
-      }
-      if (!FULL) {
-        p.x = col < kv_valid ? p.x : 0.f;
-        p.y = col + 1 < kv_valid ? p.y : 0.f;
-      }
-      if (i & 1)
-        acc1 = __fadd2_rn(acc1, p);
-      else
-        acc0 = __fadd2_rn(acc0, p);
-      pk[i] = pack_bf16x2(p.x, p.y);
-    }
-  }
-  return __fadd2_rn(acc0, acc1);
-}
-template <int NPK>
-__device__ __forceinline__ void store_p_smem(const uint32_t (&pk)[NPK], uint32_t prow, int rsw) {
-#pragma unroll
-  for (int ch = 0; ch < NPK / 4; ++ch) {  // keys [8 ch, 8 ch + 8)
-    const uint32_t a = prow + (ch >> 3) * 16384 + (((ch & 7) ^ rsw) << 4);
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(pk[4 * ch]), "r"(pk[4 * ch + 1]),
-                 "r"(pk[4 * ch + 2]), "r"(pk[4 * ch + 3])
-                 : "memory");
-  }
-}
-
 // SCATTER: the fused head->seq exchange epilogue (OScatter); a separate instantiation so the plain
 // kernel keeps its register allocation (the scatter lookup in the shared epilogue cost ~5%).
-template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false, bool PS = false>
+template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
                    const __grid_constant__ SeqTable tab, float scale_log2,
                    const __grid_constant__ OScatter osc) {
-  using C = Cfg<HD, PAIR, PS>;
+  using C = Cfg<HD, PAIR>;
   const unsigned cta_lin = blockIdx.y * gridDim.x + blockIdx.x;
   if (TRACE && threadIdx.x == 0 && cta_lin < 8192) {
     g_attn_ctatime[cta_lin * 4 + 0] = gtimer();
@@ -211,9 +159,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* sfull = vempty + C::VST;    // [2]
   uint64_t* pfull = sfull + 2;        // [2]
   uint64_t* ofull = pfull + 2;        // [2]
-  uint64_t* sfree = ofull + 2;        // [2] PS: the softmax group has loaded S_j (leader's, 4 x NC arrivals)
-  uint64_t* pfree = sfree + 2;        // [2] PS: PV_j done (P_w buffer and O_w free; multicast commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfree + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y;
@@ -250,8 +196,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&sfull[w], 1);
       mbar_init(&pfull[w], 4 * NC);
       mbar_init(&ofull[w], 1);
-      mbar_init(&sfree[w], 4 * NC);
-      mbar_init(&pfree[w], 1);
     }
     fence_barrier_init();
   }
@@ -341,7 +285,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint64_t qdesc0 = sdesc_sw128(sq, 16, 1024);
       const uint64_t kdesc0 = sdesc_sw128(sk0, 16, 1024);
       const uint64_t vdesc0 = sdesc_sw128(sv0, 16384, 1024);
-      const uint64_t pdesc0 = sdesc_sw128(smem_u32(smem + C::P_OFF), 16, 1024);  // PS only
       auto issue_s = [&](int w, int j) {  // S_w = Q_w K_j^T -> TMEM cols [128 w, 128 w + 128)
         TRACE_EV(0, w, j);
         const uint64_t qa = qdesc0 + ((w * C::TILE_BYTES) >> 4);
@@ -363,13 +306,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint64_t vb = vdesc0 + (((j % C::VST) * C::VT_BYTES) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          if (PS) {  // A = P_w from shared memory (K-major, the Q layout)
-            const uint32_t poff = ((w * 32768) + (kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-            if (PAIR)
-              mma_ss_2sm(tmem + 256 + w * 128, pdesc0 + poff, vb + ((kk * 2048) >> 4), idesc_o, (j > 0) || (kk > 0));
-            else
-              mma_ss(tmem + 256 + w * 128, pdesc0 + poff, vb + ((kk * 2048) >> 4), idesc_o, (j > 0) || (kk > 0));
-          } else if (PAIR)
+          if (PAIR)
             mma_ts_2sm(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, vb + ((kk * 2048) >> 4), idesc_o,
                        (j > 0) || (kk > 0));
           else
@@ -390,31 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       issue_s(0, 0);
       issue_s(1, 0);
       commit(&kempty[0]);
-      if (PS) {
-        // Per tile j and group w: S_w,j+1 as soon as the group has loaded S_w,j (sfree, early in its
-        // softmax), then PV_w,j as soon as P_w,j is in shared memory -- group 0 then group 1, so a
-        // group's PV never waits for the other group's softmax.  Waits suspend (try_wait).
-        for (int j = 0; j < nkv; ++j) {
-          const bool more = j + 1 < nkv;
-          if (more) mbar_wait(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
-          mbar_wait(&vfull[j % C::VST], (j / C::VST) & 1);
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            if (more) {
-              mbar_wait(&sfree[w], j & 1);
-              tc_fence_after();
-              issue_s(w, j + 1);
-              if (w == 1) commit(&kempty[(j + 1) % C::KST]);
-            }
-            mbar_wait(&pfull[w], j & 1);
-            tc_fence_after();
-            issue_pv(w, j);
-            commit(&pfree[w]);
-          }
-          commit(&vempty[j % C::VST]);
-        }
-      }
-      for (int j = 0; j < (PS ? 0 : nkv); ++j) {
+      for (int j = 0; j < nkv; ++j) {
         const bool more = j + 1 < nkv;
         // V_j and K_{j+1} landed long ago in steady state: check them before waiting on P (folding
         // these checks into P0's barrier via a helper warp was measured: no gain, see r01_notes.md)
@@ -458,16 +371,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       GS_TMEM_LD32(tS + 64, (*reinterpret_cast<uint32_t(*)[32]>(v + 64)));
       GS_TMEM_LD32(tS + 96, (*reinterpret_cast<uint32_t(*)[32]>(v + 96)));
       tmem_ld_wait();
-      if (PS) {  // S_w,j is in registers: its TMEM columns are free for S_w,j+1
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (PAIR)
-            mbar_arrive_cluster(mapa_shared(smem_u32(&sfree[w]), 0));
-          else
-            mbar_arrive(&sfree[w]);
-        }
-      }
       if (quarter == 0 && lane == 0) TRACE_EV(3, w, j);
       const bool full = kv_valid == 128;  // warp-uniform: only a request's last tile is partial
       if (!full) {
@@ -493,18 +396,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool need = m_tile > m_run + 8.0f;
       const float alpha = need ? ex2_approx(m_run - m_tile) : 1.0f;
       if (need) m_run = m_tile;
-      uint32_t pk_ps[64];  // PS only
-      float2 acc_ps = make_float2(0.f, 0.f);
-      if constexpr (PS) {  // exp first (registers), then wait for PV_w,j-1 before touching P_w buffer / O_w
-        if (full)
-          acc_ps = exp_pack_regs<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, pk_ps);
-        else
-          acc_ps = exp_pack_regs<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, pk_ps);
-        if (j > 0) {
-          mbar_wait(&pfree[w], (j - 1) & 1);
-          tc_fence_after();
-        }
-      }
       if (j > 0 && __any_sync(0xffffffffu, need)) {
 #pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
@@ -518,12 +409,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       l_run *= alpha;
       float2 acc;
-      if (PS) {
-        const int prow_i = quarter * 32 + lane;  // this thread's row of the 128-row tile w
-        store_p_smem(pk_ps, smem_u32(smem + C::P_OFF) + w * 32768 + prow_i * 128, prow_i & 7);
-        fence_proxy_async_smem();  // generic st.shared -> visible to the MMA (async proxy)
-        acc = acc_ps;
-      } else if (full)
+      if (full)
         acc = exp_pack_store<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
       else
         acc = exp_pack_store<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
@@ -590,25 +476,30 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (TRACE && threadIdx.x == 0 && cta_lin < 8192) g_attn_ctatime[cta_lin * 4 + 2] = gtimer();
 }
 
+#ifndef GS_ATTN_ALT
+#define GS_ATTN_ALT 0
+#endif
+#if GS_ATTN_ALT
 // ---------------------------------------------------------------------------------------------
-// v6 (d = 128): one 128-row Q tile per CTA (256 per CTA pair, M = 256 cta_group::2 MMAs), with S
-// and P double-buffered in TMEM:
-//   cols [0,128) O  |  [128,256) S0  |  [256,384) S1  |  [384,448) P0  |  [448,512) P1.
-// S_{j+2} is issued into S_j's buffer as soon as the softmax has loaded S_j (sfree), ahead of
-// PV_j, so the softmax of tile j+1 starts as soon as tile j's ends: the per-tile period is
-// max(softmax, PV + S on the tensor core) instead of the v3-v5 chain softmax + hand-off + PV + S
-// (profiles/r01_notes.md).  P_j goes to buffer j & 1, free once PV_{j-2} completed: S_j's
-// completion is committed after PV_{j-2} is issued, so waiting for S_j implies it.  The lazy O rescale waits for PV_{j-1} (rare: only when the running max grows
-// by more than 2^8).
-// Softmax: two warps per TMEM lane quarter (warps q and q + 4), each owning one 64-column half of
-// the 32 rows' S / P / O; the halves exchange their partial row maxima through shared memory
-// (named barrier per warp pair).  Two warps per SMSP hide the MUFU / F2FP latencies a single
-// warp exposes (tools/micro/xu_mix_bench.cu: 2 ex2 + F2FP + FADD2 per pair = 19.9 cycles with
-// one warp, 16.2 = the MUFU floor with two).
-//   warps 0-7: softmax, warp 8: TMA producer, warp 9: TMEM owner + MMA issuer (leader CTA).
-constexpr int THREADS1 = 320;
-constexpr int kProducerWarp1 = 8, kMmaWarp1 = 9;
-struct Cfg1 {
+// v7 (d = 128, CTA pairs): one 128-row Q tile per CTA (M = 256 cta_group::2 MMAs per pair), KV
+// tiles dealt alternately to two softmax warp sets (tile j -> set j & 1: warps 0-3 / 4-7, one
+// thread per query row, the whole 128-column S row in registers), S / P in three TMEM buffers:
+//   cols [0,128) O  |  [128 + 128 u, 256 + 128 u) S/P buffer u = j % 3  (P_j: bf16 pairs over
+//   the buffer's first 64 columns, as in v5).
+// The v5 chain (a Q tile's S_{j+1} waits for its own PV_j, which waits for its softmax) is gone:
+// S_{j+2} only follows PV_{j-1}, the OTHER set's tile, so each set's softmax of tile j+2 can start
+// as soon as its tile j is done, and the two sets keep the exp (MUFU) pipe and the tensor core
+// busy at once.  The sets share one O accumulator, so they share the running max: set j & 1
+// takes m_{j-1} from the other set (shared memory, one named barrier per warp pair), decides the
+// lazy rescale of tile j (O rescaled only when the max grows by more than 2^8, after PV_{j-1}
+// completed) and hands m_j on.  Each set keeps its partial row sum relative to the last max it
+// saw; the epilogue brings both to the final max with the same exp2 factors O received.
+//   warps 0-7: softmax, warp 8: TMA producer, warp 9: TMEM owner + MMA issuer (leader CTA), warps
+//   10, 11 idle (setmaxnreg acts on whole warpgroups).
+// Development variant (built with -DGS_ATTN_ALT=1; 12% slower than v5 at the c4 SP=8 shape in round 2).
+constexpr int THREADS7 = 384;
+constexpr int kProducerWarp7 = 8, kMmaWarp7 = 9;
+struct Cfg7 {
   static constexpr int HD = 128;
   static constexpr int TILE_BYTES = 128 * HD * 2;   // this CTA's Q tile
   static constexpr int KT_BYTES = 64 * HD * 2;      // 64 of the tile's 128 keys
@@ -619,26 +510,19 @@ struct Cfg1 {
   static constexpr int K_OFF = TILE_BYTES;
   static constexpr int V_OFF = K_OFF + KST * KT_BYTES;
   static constexpr int BAR_OFF = V_OFF + VST * VT_BYTES;
-  static constexpr int RED_OFF = BAR_OFF + 256;
-  static constexpr int SMEM = RED_OFF + 2 * 2 * 128 * 4 + 1024;
-  static constexpr uint32_t T_O = 0, T_S = 128, T_P = 384;
+  static constexpr int XCH_OFF = BAR_OFF + 256;              // float [2 sets][128 rows] running max
+  static constexpr int FIN_OFF = XCH_OFF + 2 * 128 * 4;      // float [2 sets][2 (l, m)][128 rows]
+  static constexpr int SMEM = FIN_OFF + 2 * 2 * 128 * 4 + 1024;
+  static constexpr uint32_t T_O = 0, T_S = 128;
 };
+static_assert(Cfg7::SMEM <= 232448, "v7 shared memory");
 
-template <int POLY8, bool TRACE>
-__global__ void __launch_bounds__(THREADS1, 1)
-    attn_db_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                   const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
-                   const __grid_constant__ SeqTable tab, float scale_log2, int flags) {
-  using C = Cfg1;
-  // flags (development A/B, GS_ATTN_FLAGS): bit 0 = softmax waits suspend (try_wait) instead of
-  // polling test_wait, bit 1 = same for the MMA issuer.  Polling loops are MIO-queue traffic that
-  // competes with MUFU (ncu: MUFU stalls on mio_throttle).
-  auto wait_sm = [&](uint64_t* bar, uint32_t par) {
-    if (flags & 1) mbar_wait(bar, par); else mbar_wait_spin(bar, par);
-  };
-  auto wait_mma = [&](uint64_t* bar, uint32_t par) {
-    if (flags & 2) mbar_wait(bar, par); else mbar_wait_spin(bar, par);
-  };
+template <int POLY8, bool SCATTER, bool TRACE = false>
+__global__ void __launch_bounds__(THREADS7, 1)
+    attn_alt_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, __nv_bfloat16* __restrict__ O, int o_rs,
+                    const __grid_constant__ SeqTable tab, float scale_log2, const __grid_constant__ OScatter osc) {
+  using C = Cfg7;
   constexpr int HD = C::HD;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -648,12 +532,12 @@ __global__ void __launch_bounds__(THREADS1, 1)
   uint64_t* kempty = kfull + C::KST;    // [KST]
   uint64_t* vfull = kempty + C::KST;    // [VST]
   uint64_t* vempty = vfull + C::VST;    // [VST]
-  uint64_t* sfull = vempty + C::VST;    // [2] S_j in buffer j & 1
-  uint64_t* pfull = sfull + 2;          // [2] P_j in buffer j & 1 (leader: 8 warp arrivals)
-  uint64_t* pvdone = pfull + 2;         // [2] PV_j (reads P buffer j & 1) completed
-  uint64_t* sfree = pvdone + 2;         // [2] softmax loaded S_j (leader: 16 warp arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
-  float* red = reinterpret_cast<float*>(smem + C::RED_OFF);  // [tile parity][half][128 rows]
+  uint64_t* sfull = vempty + C::VST;    // [3] S_j in buffer j % 3
+  uint64_t* pfull = sfull + 3;          // [3] P_j in buffer j % 3 (leader: 8 warp arrivals)
+  uint64_t* pvdone = pfull + 3;         // [3] PV_j completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pvdone + 3);
+  float* xch = reinterpret_cast<float*>(smem + C::XCH_OFF);
+  float* fin = reinterpret_cast<float*>(smem + C::FIN_OFF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int head = blockIdx.y;
@@ -664,8 +548,9 @@ __global__ void __launch_bounds__(THREADS1, 1)
   while (r + 1 < tab.nreq && blk >= tab.tile_start[r + 1]) ++r;
   const int pair = blk - tab.tile_start[r];
   const int kv_off = tab.kv_off[r], kv_len = tab.kv_len[r];
-  const int q_row0 = tab.q_off[r] + pair * 256 + rank * 128;
-  const int q_rows = min(128, tab.q_len[r] - pair * 256 - static_cast<int>(rank) * 128);  // may be <= 0
+  const int q_first = pair * 256 + static_cast<int>(rank) * 128;  // request-local first query row
+  const int q_row0 = tab.q_off[r] + q_first;
+  const int q_rows = min(128, tab.q_len[r] - q_first);  // may be <= 0
   const int nkv = (kv_len + 127) / 128;
 
   if (threadIdx.x == 0) {
@@ -678,26 +563,31 @@ __global__ void __launch_bounds__(THREADS1, 1)
       mbar_init(&vfull[s], 2);
       mbar_init(&vempty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sfull[b], 1);
-      mbar_init(&pfull[b], 16);
-      mbar_init(&pvdone[b], 1);
-      mbar_init(&sfree[b], 16);
+    for (int u = 0; u < 3; ++u) {
+      mbar_init(&sfull[u], 1);
+      mbar_init(&pfull[u], 8);
+      mbar_init(&pvdone[u], 1);
     }
     fence_barrier_init();
   }
-  if (warp == kProducerWarp1 && lane == 0) {
+  if (warp == kProducerWarp7 && lane == 0) {
     tma_prefetch(&tmQ);
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
   }
-  if (warp == kMmaWarp1) tmem_alloc_2sm(tmem_slot, 512);
+  if (warp == kMmaWarp7) tmem_alloc_2sm(tmem_slot, 512);
   tc_fence_before();
   cluster_sync();  // both CTAs' barriers initialised before any remote arrive / 2-SM TMA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the setup above overlaps the previous kernel's tail; global memory only from here
+  pdl_launch_dependents();
 
-  if (warp == kProducerWarp1) {
+  // register split: the CTA pool is 384 x 168 (launch allocation); warpgroup 2 (producer, MMA, two
+  // idle warps) shrinks to 56, freeing 4 x 32 x 112 = 14336 >= 8 x 32 x (208 - 168) = 10240.
+  if (warp >= 8) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+  if (warp == kProducerWarp7) {
     if (lane == 0) {
       auto arrive_tx = [&](uint64_t* bar, uint32_t bytes) {
         mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(bar), 0), bytes);
@@ -717,17 +607,19 @@ __global__ void __launch_bounds__(THREADS1, 1)
         tma_load_3d_2sm(&tmV, &vfull[vs], smem + C::V_OFF + vs * C::VT_BYTES, 64 * rank, head, kv_off + j * 128);
       }
     }
-  } else if (warp == kMmaWarp1) {
+  } else if (warp == kMmaWarp7) {
     if (rank == 0 && lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16(256, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16(256, HD, 0, 1);
       const uint64_t qdesc0 = sdesc_sw128(smem_u32(smem + C::Q_OFF), 16, 1024);
       const uint64_t kdesc0 = sdesc_sw128(smem_u32(smem + C::K_OFF), 16, 1024);
       const uint64_t vdesc0 = sdesc_sw128(smem_u32(smem + C::V_OFF), 16384, 1024);
-      auto issue_s = [&](int j) {  // S_j = Q K_j^T -> S buffer j & 1
+      auto issue_s = [&](int j) {  // S_j = Q K_j^T -> buffer j % 3; K slot and S_j signalled
+        mbar_wait_spin(&kfull[j % C::KST], (j / C::KST) & 1);
+        tc_fence_after();
         TRACE_EV(0, 0, j);
         const uint64_t kb = kdesc0 + (((j % C::KST) * C::KT_BYTES) >> 4);
-        const uint32_t d = tmem + C::T_S + (j & 1) * 128;
+        const uint32_t d = tmem + C::T_S + (j % 3) * 128;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t qoff = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
@@ -735,113 +627,111 @@ __global__ void __launch_bounds__(THREADS1, 1)
           mma_ss_2sm(d, qdesc0 + qoff, kb + koff, idesc_s, kk > 0);
         }
         mma_commit_2sm_mc(&kempty[j % C::KST], 0x3);
+        mma_commit_2sm_mc(&sfull[j % 3], 0x3);
       };
-      auto issue_pv = [&](int j) {  // O += P_j V_j, P_j read from TMEM buffer j & 1
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < 3 && j < nkv; ++j) issue_s(j);
+      for (int j = 0; j < nkv; ++j) {
+        const int u = j % 3;
+        mbar_wait_spin(&vfull[j % C::VST], (j / C::VST) & 1);
+        TRACE_EV(7, 0, j);
+        mbar_wait_spin(&pfull[u], (j / 3) & 1);
+        tc_fence_after();
         TRACE_EV(1, 0, j);
+        // O += P_j V_j, P_j read from TMEM (bf16 pairs over buffer u's first 64 columns)
         const uint64_t vb = vdesc0 + (((j % C::VST) * C::VT_BYTES) >> 4);
-        const uint32_t pa = tmem + C::T_P + (j & 1) * 64;
+        const uint32_t pa = tmem + C::T_S + u * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           mma_ts_2sm(tmem + C::T_O, pa + kk * 8, vb + ((kk * 2048) >> 4), idesc_o, (j > 0) || (kk > 0));
-        mma_commit_2sm_mc(&pvdone[j & 1], 0x3);
+        mma_commit_2sm_mc(&pvdone[u], 0x3);
         mma_commit_2sm_mc(&vempty[j % C::VST], 0x3);
-      };
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < 2 && j < nkv; ++j) {
-        wait_mma(&kfull[j % C::KST], (j / C::KST) & 1);
-        tc_fence_after();
-        issue_s(j);
-        mma_commit_2sm_mc(&sfull[j], 0x3);
-      }
-      const bool early_s = flags & 4;  // A/B: S_{j+2} issued before PV_j (after sfree) vs after it
-      if (nkv > 0) wait_mma(&vfull[0], 0);
-      for (int j = 0; j < nkv; ++j) {
-        const bool more = j + 2 < nkv;
-        if (more && early_s) {  // S_{j+2} into S_j's buffer as soon as the softmax has loaded S_j
-          wait_mma(&sfree[j & 1], (j >> 1) & 1);
-          wait_mma(&kfull[(j + 2) % C::KST], ((j + 2) / C::KST) & 1);
-          tc_fence_after();
-          issue_s(j + 2);
-        }
-        // V_j was checked at the end of the previous iteration: P_j is the only wait on the path
-        // from the softmax's hand-off to PV_j
-        if (flags & 8)
-          mbar_wait(&pfull[j & 1], (j >> 1) & 1);
-        else
-          mbar_wait_spin(&pfull[j & 1], (j >> 1) & 1);
-        TRACE_EV(10, 0, j);
-        tc_fence_after();
-        issue_pv(j);
-        if (more && !early_s) {  // S_j's buffer is free: P_j's arrival follows the softmax's load of S_j
-          wait_mma(&kfull[(j + 2) % C::KST], ((j + 2) / C::KST) & 1);
-          tc_fence_after();
-          issue_s(j + 2);
-        }
-        // S_{j+2}'s completion is signalled only after PV_j is issued: the commit tracks both, so
-        // the softmax's wait for S_{j+2} also guarantees P buffer j & 1 is free again.
-        if (more) mma_commit_2sm_mc(&sfull[j & 1], 0x3);
-        if (j + 1 < nkv) wait_mma(&vfull[(j + 1) % C::VST], ((j + 1) / C::VST) & 1);
+        // buffer u is free once PV_j has read P_j: the tensor core runs the MMAs in issue order
+        if (j + 3 < nkv) issue_s(j + 3);
       }
     }
-  } else if (warp < 8) {
-    const int quarter = warp & 3, half = warp >> 2;  // lane quarter, column half
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    const int set = warp >> 2, quarter = warp & 3;
     const int row_in = quarter * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t tO = tmem + lane_base + C::T_O + half * (HD / 2);
+    const uint32_t tO = tmem + lane_base + C::T_O;
     const float2 sc2 = make_float2(scale_log2, scale_log2);
     const uint32_t pfull_leader = mapa_shared(smem_u32(&pfull[0]), 0);
-    const uint32_t sfree_leader = mapa_shared(smem_u32(&sfree[0]), 0);
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1;
-      const uint32_t tS = tmem + lane_base + C::T_S + b * 128 + half * 64;
-      const uint32_t tP = tmem + lane_base + C::T_P + b * 64 + half * 32;
-      wait_sm(&sfull[b], (j >> 1) & 1);
+    // named barriers 1-4: set 0 -> set 1 hand-off of the running max (per lane quarter); 5-8: set 1 -> set 0;
+    // 9-12: the epilogue exchange of both sets' row sums
+    const int bar_put = 1 + quarter + 4 * set, bar_get = 1 + quarter + 4 * (set ^ 1);
+    float m_ref = -INFINITY, l_run = 0.f;  // this set's row sum, relative to exp2 max m_ref
+    for (int j = set; j < nkv; j += 2) {
+      const int u = j % 3;
+      const uint32_t tS = tmem + lane_base + C::T_S + u * 128;
+      mbar_wait(&sfull[u], (j / 3) & 1);
       tc_fence_after();
-      if (warp == 0 && lane == 0) TRACE_EV(2, 0, j);
+      if (quarter == 0 && lane == 0) TRACE_EV(2, 0, j);
+      __syncwarp();
       const int kv_valid = min(128, kv_len - j * 128);
-      uint32_t v[64];
+      uint32_t v[128];
       GS_TMEM_LD32(tS + 0, (*reinterpret_cast<uint32_t(*)[32]>(v + 0)));
       GS_TMEM_LD32(tS + 32, (*reinterpret_cast<uint32_t(*)[32]>(v + 32)));
+      GS_TMEM_LD32(tS + 64, (*reinterpret_cast<uint32_t(*)[32]>(v + 64)));
+      GS_TMEM_LD32(tS + 96, (*reinterpret_cast<uint32_t(*)[32]>(v + 96)));
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(sfree_leader + b * 8);  // S buffer b may be overwritten
-      if (warp == 0 && lane == 0) TRACE_EV(3, 0, j);
-      const bool full = kv_valid == 128;
+      if (quarter == 0 && lane == 0) TRACE_EV(3, 0, j);
+      const bool full = kv_valid == 128;  // warp-uniform: only a request's last tile is partial
       if (!full) {
 #pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (half * 64 + i >= kv_valid) v[i] = __float_as_uint(-INFINITY);
+        for (int i = 0; i < 128; ++i)
+          if (i >= kv_valid) v[i] = __float_as_uint(-INFINITY);
       }
-      // partial row max over this half: 4 independent FMNMX3 chains
-      float mx[4];
+      float mx[8];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) mx[c] = fmax3(__uint_as_float(v[16 * c]), __uint_as_float(v[16 * c + 1]),
+      for (int c = 0; c < 8; ++c) mx[c] = fmax3(__uint_as_float(v[16 * c]), __uint_as_float(v[16 * c + 1]),
                                                 __uint_as_float(v[16 * c + 2]));
 #pragma unroll
       for (int i = 3; i < 15; i += 2)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 8; ++c)
           mx[c] = fmax3(mx[c], __uint_as_float(v[16 * c + i]), __uint_as_float(v[16 * c + i + 1]));
 #pragma unroll
-      for (int c = 0; c < 4; ++c) mx[c] = fmaxf(mx[c], __uint_as_float(v[16 * c + 15]));
-      const float m_half = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-      if (warp == 0 && lane == 0) TRACE_EV(11, 0, j);
-      // exchange with the other half's warp (double-buffered by tile parity: the partner cannot
-      // reach tile j + 2's write before passing tile j + 1's barrier, i.e. after reading tile j)
-      red[(b * 2 + half) * 128 + row_in] = m_half;
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-      const float m_tile = fmaxf(m_half, red[(b * 2 + (half ^ 1)) * 128 + row_in]) * scale_log2;
-      if (warp == 0 && lane == 0) TRACE_EV(12, 0, j);
-      const bool need = m_tile > m_run + 8.0f;
-      const float alpha = need ? ex2_approx(m_run - m_tile) : 1.0f;
-      if (need) m_run = m_tile;
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        mbar_wait(&pvdone[(j - 1) & 1], ((j - 1) >> 1) & 1);  // O holds PV_0..PV_{j-1}
+      for (int c = 0; c < 8; ++c) mx[c] = fmaxf(mx[c], __uint_as_float(v[16 * c + 15]));
+      const float m_tile =
+          fmax3(fmax3(mx[0], mx[1], mx[2]), fmax3(mx[3], mx[4], mx[5]), fmaxf(mx[6], mx[7])) * scale_log2;
+      // running max after tile j - 1 (the other set's tile)
+      float m_prev = -INFINITY;
+      if (quarter == 0 && lane == 0) TRACE_EV(4, 0, j);
+      if (j > 0) {
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_get) : "memory");
+        m_prev = xch[(set ^ 1) * 128 + row_in];
+        if (m_prev != m_ref) {  // the other set moved the max at tile j - 1: same factor as O got
+          l_run *= ex2_approx(m_ref - m_prev);
+          m_ref = m_prev;
+        }
+      }
+      // lazy rescale: move the reference max only when it grows by more than 2^8
+      const bool need = m_tile > m_prev + 8.0f;
+      const float alpha = need ? ex2_approx(m_prev - m_tile) : 1.0f;
+      const float m_run = need ? m_tile : m_prev;
+      if (j + 1 < nkv) {
+        xch[set * 128 + row_in] = m_run;
+        asm volatile("bar.arrive %0, 64;" ::"r"(bar_put) : "memory");
+      }
+      l_run *= alpha;
+      m_ref = m_run;
+      if (quarter == 0 && lane == 0) TRACE_EV(5, 0, j);
+      __syncwarp();
+      float2 acc;
+      if (full)
+        acc = exp_pack_store<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
+      else
+        acc = exp_pack_store<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
+      l_run += acc.x + acc.y;
+      if (quarter == 0 && lane == 0) TRACE_EV(6, 0, j);
+      if (j > 0 && __any_sync(0xffffffffu, need)) {  // O holds PV_0..PV_{j-1}: rescale before PV_j
+        mbar_wait(&pvdone[(j - 1) % 3], ((j - 1) / 3) & 1);
         tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < HD / 64; ++c) {
+        for (int c = 0; c < HD / 32; ++c) {
           uint32_t o[32];
           GS_TMEM_LD32(tO + c * 32, o);
           tmem_ld_wait();
@@ -850,46 +740,55 @@ __global__ void __launch_bounds__(THREADS1, 1)
           GS_TMEM_ST32(tO + c * 32, o);
         }
       }
-      l_run *= alpha;
-      // P buffer b was last read by PV_{j-2}, which is complete: S_j's completion is committed
-      // after PV_{j-2} is issued and a commit tracks all of the issuing thread's earlier MMAs (an
-      // explicit wait on pv_done here measured ~290 cycles per tile under MUFU / MIO load).
-      if (warp == 0 && lane == 0) TRACE_EV(13, 0, j);
-      float2 acc;
-      if (full)
-        acc = exp_pack_store<POLY8, true, 64>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tP, half * 64);
-      else
-        acc = exp_pack_store<POLY8, false, 64>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tP, half * 64);
-      l_run += acc.x + acc.y;
-      if (warp == 0 && lane == 0) TRACE_EV(14, 0, j);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (TRACE && lane == 0 && half == 0 && blockIdx.x < 2 && blockIdx.y == 0 && j < 32)
-        g_attn_trace[blockIdx.x * 1024 + ((4 + quarter) * 32 + j) * 2] = clock64();
-      if (lane == 0) mbar_arrive_cluster(pfull_leader + b * 8);
+      if (lane == 0) mbar_arrive_cluster(pfull_leader + u * 8);
+      if (lane == 0) TRACE_EV(8 + quarter, 0, j);
+      __syncwarp();
     }
-    // row sum = both halves' partial sums (exchange slot of parity nkv & 1 is free: see above)
-    const int bf = nkv & 1;
-    red[(bf * 2 + half) * 128 + row_in] = l_run;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-    l_run += red[(bf * 2 + (half ^ 1)) * 128 + row_in];
-    // epilogue: O / l -> bf16 -> global, after the last PV (commits track all earlier MMAs)
-    if (nkv > 0) mbar_wait(&pvdone[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
+    // row sum: both sets' partial sums brought to the final max m_ref of the set that did the last tile
+    // The set of the last tile waits for the last PV before the exchange: its wait for S_{nkv-1}
+    // implied PV_{nkv-4} (same buffer) done, so the parity test cannot alias an older phase; the
+    // other set learns of the completion through the named barrier.
+    const int last = (nkv - 1) & 1;
+    fin[(set * 2 + 0) * 128 + row_in] = l_run;
+    fin[(set * 2 + 1) * 128 + row_in] = m_ref;
+    if (set == last) mbar_wait(&pvdone[(nkv - 1) % 3], ((nkv - 1) / 3) & 1);
+    asm volatile("bar.sync %0, 64;" ::"r"(9 + quarter) : "memory");
     tc_fence_after();
-    const float inv = 1.0f / l_run;
-    __nv_bfloat16* orow = O + static_cast<long long>(q_row0 + row_in) * o_rs + head * HD + half * (HD / 2);
+    const float m_fin = fin[(last * 2 + 1) * 128 + row_in];
+    float l_tot = 0.f;
 #pragma unroll
-    for (int c = 0; c < HD / 64; ++c) {
+    for (int s = 0; s < 2; ++s) {
+      const float ls = fin[(s * 2 + 0) * 128 + row_in], ms = fin[(s * 2 + 1) * 128 + row_in];
+      l_tot += ms == m_fin ? ls : ls * ex2_approx(ms - m_fin);
+    }
+    // epilogue: set s writes d columns [64 s, 64 s + 64)
+    const float inv = 1.0f / l_tot;
+    __nv_bfloat16* orow;
+    if (SCATTER) {  // fused head->seq exchange: straight into the token owner's O-proj input
+      const int t = q_first + row_in;
+      int i = 0;
+#pragma unroll
+      for (int k = 1; k < 8; ++k)
+        if (k < osc.nown && t >= osc.lo[r][k]) i = k;
+      orow = osc.base[r][i] + static_cast<long long>(t) * o_rs + head * HD;
+    } else {
+      orow = O + static_cast<long long>(q_row0 + row_in) * o_rs + head * HD;
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int col = set * 64 + c * 32;
       uint32_t v[32];
-      GS_TMEM_LD32(tO + c * 32, v);
+      GS_TMEM_LD32(tO + col, v);
       tmem_ld_wait();
       if (row_in < q_rows) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           pk[i] = pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+        uint4* dst = reinterpret_cast<uint4*>(orow + col);
 #pragma unroll
         for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
       }
@@ -898,36 +797,27 @@ __global__ void __launch_bounds__(THREADS1, 1)
   }
   __syncthreads();
   cluster_sync();  // the peer may still arrive on our barriers / read our TMEM until here
-  if (warp == kMmaWarp1) {
+  if (warp == kMmaWarp7) {
     __syncwarp();
     tc_fence_after();
     tmem_dealloc_2sm(tmem, 512);
   }
 }
 
-// Kernel version for d = 128: 5 (default, attn_tc_kernel) or 6 (attn_db_kernel, GS_ATTN_V=6).
-// v6 measured slower (1050-1130 vs 1360-1380 TFLOP/s at the c4 sp8 shape, profiles/r01_notes.md):
-// its two softmax warps per lane quarter run in lock-step, so the MUFU pipe idles through the
-// max / exchange / barrier phases that v5's two Q-tile groups overlap.
-int attn_version() {
-  static int v = [] {
-    const char* e = getenv("GS_ATTN_V");
-    return e ? atoi(e) : 5;
-  }();
-  return v;
-}
-
 template <int POLY8>
-cudaError_t launch_db(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs, int kv_rs, int o_rs,
-                      const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream) {
-  using C = Cfg1;
+cudaError_t launch_alt(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs, int kv_rs,
+                       int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream,
+                       const OScatter& osc) {
+  using C = Cfg7;
   CUtensorMap tq, tk, tv;
   if (!make_tma_3d_bf16(&tq, Q, 128, heads, q_rows, 256ull, q_rs * 2ull, 64, 1, 128) ||
       !make_tma_3d_bf16(&tk, K, 128, heads, kv_rows, 256ull, kv_rs * 2ull, 64, 1, 64) ||
       !make_tma_3d_bf16(&tv, V, 128, heads, kv_rows, 256ull, kv_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
   static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
-  auto kern = trace ? attn_db_kernel<POLY8, true> : attn_db_kernel<POLY8, false>;
+  auto kern = osc.nown > 0 ? attn_alt_kernel<POLY8, true>
+              : trace      ? attn_alt_kernel<POLY8, false, true>
+                           : attn_alt_kernel<POLY8, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
   const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(128.0));
@@ -935,30 +825,30 @@ cudaError_t launch_db(const void* Q, const void* K, const void* V, void* O, int 
   if (grid.x == 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(THREADS1);
+  cfg.blockDim = dim3(THREADS7);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = stream;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = 2;
-  attr.val.clusterDim.y = 1;
-  attr.val.clusterDim.z = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  static const int flags = [] {
-    const char* e = getenv("GS_ATTN_FLAGS");
-    return e ? atoi(e) : 0;
-  }();
-  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2, flags);
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2, osc);
 }
 
+#endif  // GS_ATTN_ALT
 template <int HD, int POLY8>
 cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
                    int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream,
                    const OScatter& osc) {
   constexpr bool PAIR = HD == 128;
-  if (HD == 128 && attn_version() >= 6 && osc.nown == 0)
-    return launch_db<POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream);
+#if GS_ATTN_ALT
+  if (HD == 128) return launch_alt<POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
+#endif
   using C = Cfg<HD, PAIR>;
   CUtensorMap tq, tk, tv;
   if (!make_tma_3d_bf16(&tq, Q, HD, heads, q_rows, HD * 2ull, q_rs * 2ull, 64, 1, 128) ||
@@ -966,17 +856,10 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
       !make_tma_3d_bf16(&tv, V, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
   static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
-  static const bool ps = [] {  // round-2 experiment: P in shared memory (Cfg PS), d = 128 only
-    const char* e = getenv("GS_ATTN_PS");
-    return e && e[0] == '1';
-  }();
-  const bool use_ps = ps && HD == 128 && osc.nown == 0;
-  auto kern = osc.nown > 0        ? attn_tc_kernel<HD, POLY8, false, PAIR, true>
-              : trace && use_ps ? attn_tc_kernel<HD, POLY8, true, PAIR, false, HD == 128>
-              : trace           ? attn_tc_kernel<HD, POLY8, true>
-              : use_ps          ? attn_tc_kernel<HD, POLY8, false, PAIR, false, HD == 128>
-                                : attn_tc_kernel<HD, POLY8, false>;
-  const int smem_bytes = use_ps ? Cfg<HD, PAIR, HD == 128>::SMEM : C::SMEM;
+  auto kern = osc.nown > 0 ? attn_tc_kernel<HD, POLY8, false, PAIR, true>
+              : trace      ? attn_tc_kernel<HD, POLY8, true>
+                           : attn_tc_kernel<HD, POLY8, false>;
+  const int smem_bytes = C::SMEM;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   if (e != cudaSuccess) return e;
   const float scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(HD)));
@@ -999,27 +882,19 @@ cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int h
   return cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, static_cast<__nv_bfloat16*>(O), o_rs, tab, scale_log2, osc);
 }
 
-// Fraction of exp2 pairs (in eighths) computed by the FMA-pipe polynomial.  Default from the
-// tuning sweep in profiles/; GS_ATTN_POLY8 overrides it (development aid).
-int poly8_setting() {
-  static int v = [] {
-    const char* e = getenv("GS_ATTN_POLY8");
-    int x = e ? atoi(e) : 0;
-    return (x == 0 || x == 2 || x == 3 || x == 4) ? x : 0;
-  }();
-  return v;
-}
+// Fraction of exp2 pairs (in eighths) computed by the FMA-pipe polynomial: a compile-time constant
+// (it changes output bits, so it must not differ between the processes of an SP group; the round-1
+// sweep in profiles/r01_notes.md found 0 fastest).  Other values build with -DGS_ATTN_POLY8=2|3|4.
+#ifndef GS_ATTN_POLY8
+#define GS_ATTN_POLY8 0
+#endif
+static_assert(GS_ATTN_POLY8 == 0 || GS_ATTN_POLY8 == 2 || GS_ATTN_POLY8 == 3 || GS_ATTN_POLY8 == 4, "POLY8");
 
 template <int HD>
 cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
                    int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream,
                    const OScatter& osc) {
-  switch (poly8_setting()) {
-    case 2: return launch_t<HD, 2>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
-    case 4: return launch_t<HD, 4>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
-    case 3: return launch_t<HD, 3>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
-    default: return launch_t<HD, 0>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
-  }
+  return launch_t<HD, GS_ATTN_POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
 }
 }  // namespace
 
@@ -1037,8 +912,8 @@ cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, v
   tab.nreq = nreq;
   int q_rows = 1, kv_rows = 1;
   tab.tile_start[0] = 0;
-  // a CTA pair (d = 128: 256 rows in v6, 512 in v3-v5) or a CTA (d = 64)
-  const int rows_per_block = d == 128 ? (attn_version() >= 6 ? 256 : 512) : 256;
+  // a CTA pair (d = 128: two 128-row Q tiles per CTA) or a CTA (d = 64)
+  const int rows_per_block = d == 128 ? (GS_ATTN_ALT ? 256 : 512) : 256;
   for (int r = 0; r < nreq; ++r) {
     if (q_len[r] < 0 || kv_len[r] < 1) return cudaErrorInvalidValue;
     tab.q_off[r] = q_off[r];

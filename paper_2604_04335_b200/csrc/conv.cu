@@ -1,0 +1,348 @@
+// tcgen05 implicit-GEMM causal 3-D convolution for the VAE decode stage (
+// oracle: oracle/vae.py causal_conv3d, reading V2):
+//   y[t, h, w, co] = b[co] + sum_{dt, dh, dw, ci} W[co, dt, dh, dw, ci] x[t + dt - (kt-1), h + dh - ph, w + dw - pw, ci]
+// with zero padding (kt - 1 frames before the sequence; ph = (kh-1)/2, pw = (kw-1)/2 on both sides).
+//
+// Design (B200-first; the GEMM of gemm.cu with a convolutional A operand):
+//   * activations channels-last bf16 [T][H][W][Cp] (Cp = channels padded to a multiple of 64);
+//     weights bf16 [Coutp][kt][kh][kw][Cp], i.e. the K index of the implicit GEMM is tap-major,
+//     channel-minor (K = kt kh kw Cp);
+//   * M tile of a CTA = 128 output voxels = a 4 (h) x 32 (w) patch of one frame; a CTA pair
+//     (cta_group::2, M = 256 MMAs) takes 8 x 32; one 4-D TMA box {64 ch, 32 w, 4 h, 1 t} per K block
+//     and tap loads the patch shifted by the tap with the conv's zero padding done by TMA's
+//     out-of-bounds fill (negative / past-the-end coordinates read zeros), already in the 128B-
+//     swizzled K-major layout the UMMA descriptor expects (128 rows x 128 B);
+//   * persistent CTA pairs, warp 0 TMA producer, warp 1 TMEM owner + MMA issuer (leader), warps 2-5
+//     epilogue from two TMEM accumulators (epilogue of tile i overlaps the MMAs of tile i + 1);
+//   * epilogue per output voxel (TMEM lane = voxel): + bias, + residual (bf16 or fp32, optional), then
+//     one of: bf16 store (64 B per thread per 32-channel chunk); fp32 store (the decoder's residual
+//     stream, 128 B per chunk); the temporal-upsample interleave (the
+//     two channel halves of frame t go to output frames 2t + 1, 2t + 2; reading V5); fp32 clamp to
+//     [-1, 1] of the first `out_real` channels (the decoder output, reading V7).
+// Each output depends only on its own inputs; no split-K, no atomics.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "kernels.h"
+#include "ptx.cuh"
+#include "tma.h"
+
+namespace gs {
+
+namespace {
+constexpr int CBM = 128;                 // voxels per CTA (pair: 256)
+constexpr int CBK = 64;                  // channels per K block
+constexpr int PATCH_W = 32, PATCH_H = 4;  // CTA patch (pair: 8 rows)
+constexpr int CA_BYTES = CBM * CBK * 2;  // 16 KB
+constexpr int CTHREADS = 192;
+
+template <int BN>
+struct CCfg {
+  static constexpr int B_BYTES = (BN / 2) * CBK * 2;
+  static constexpr int STAGE_BYTES = CA_BYTES + B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
+  static constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static_assert(SMEM_BYTES <= 232448, "shared memory");
+};
+
+__device__ __forceinline__ void tma_load_4d_2sm(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                                int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+struct TileGeom {
+  int num_hb, num_wb, num_m, num_n;
+  __device__ void coords(int tile, int& t, int& hb, int& wb, int& nb) const {
+    // n fastest (the A patch is reused from L2 by the pair's consecutive N tiles)
+    nb = tile % num_n;
+    const int m = tile / num_n;
+    wb = m % num_wb;
+    hb = (m / num_wb) % num_hb;
+    t = m / (num_wb * num_hb);
+  }
+};
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
+    conv3d_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ ConvParams cp) {
+  using C = CCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = bars;                     // [STAGES] leader's count both CTAs' bytes
+  uint64_t* empty = bars + C::STAGES;        // [STAGES] per CTA (multicast commit)
+  uint64_t* tfull = bars + 2 * C::STAGES;    // [2]
+  uint64_t* tempty = bars + 2 * C::STAGES + 2;  // [2] leader's: 4 epilogue warps x 2 CTAs
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  TileGeom g;
+  g.num_hb = (cp.H + 2 * PATCH_H - 1) / (2 * PATCH_H);
+  g.num_wb = (cp.W + PATCH_W - 1) / PATCH_W;
+  g.num_m = cp.T * g.num_hb * g.num_wb;
+  g.num_n = cp.Coutp / BN;
+  const int num_tiles = g.num_m * g.num_n;
+  const int cpb = cp.Cp / CBK;
+  const int num_k = cp.kt * cp.kh * cp.kw * cpb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+  }
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, C::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer (both CTAs): this CTA's voxel patch per tap and its weight half
+      int stage = 0;
+      uint32_t phase = 0;
+      const int ph = (cp.kh - 1) / 2, pw = (cp.kw - 1) / 2;
+      for (int tile = pair; tile < num_tiles; tile += npairs) {
+        int t, hb, wb, nb;
+        g.coords(tile, t, hb, wb, nb);
+        const int h0 = hb * 2 * PATCH_H + static_cast<int>(rank) * PATCH_H, w0 = wb * PATCH_W;
+        int cb = 0, dw = 0, dh = 0, dt = 0;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&full[stage]), 0), C::STAGE_BYTES);
+          tma_load_4d_2sm(&tmA, &full[stage], sa, cb * CBK, w0 + dw - pw, h0 + dh - ph, t + dt - (cp.kt - 1));
+          tma_load_2d_2sm(&tmB, &full[stage], sa + CA_BYTES, kb * CBK, nb * BN + static_cast<int>(rank) * (BN / 2));
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+          if (++cb == cpb) {  // K order: tap-major (dt, dh, dw), channel block minor
+            cb = 0;
+            if (++dw == cp.kw) {
+              dw = 0;
+              if (++dh == cp.kh) { dh = 0; ++dt; }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // MMA issuer (leader CTA)
+      constexpr uint32_t idesc = idesc_bf16(2 * CBM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
+        const int as = it & 1;
+        mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + CA_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < CBK / 16; ++kk)
+            mma_ss_2sm(d_tmem, sdesc_sw128(sa + kk * 32, 16, 1024), sdesc_sw128(sb + kk * 32, 16, 1024), idesc,
+                       (kb | kk) != 0);
+          mma_commit_2sm_mc(&empty[stage], 0x3);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_2sm_mc(&tfull[as], 0x3);
+      }
+    }
+  } else {
+    // epilogue: warp (2..5) % 4 = TMEM lane quarter = patch row; lane = patch column
+    const int quarter = warp & 3;
+    const uint32_t tempty_leader = mapa_shared(smem_u32(&tempty[0]), 0);
+    int it = 0;
+    for (int tile = pair; tile < num_tiles; tile += npairs, ++it) {
+      int t, hb, wb, nb;
+      g.coords(tile, t, hb, wb, nb);
+      const int as = it & 1;
+      mbar_wait(&tfull[as], (it >> 1) & 1);
+      tc_fence_after();
+      const int h = hb * 2 * PATCH_H + static_cast<int>(rank) * PATCH_H + quarter, w = wb * PATCH_W + lane;
+      const bool valid = h < cp.H && w < cp.W;
+      const long long vox = (static_cast<long long>(t) * cp.H + h) * cp.W + w;
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        GS_TMEM_LD32(tbase + c * 32, r);
+        tmem_ld_wait();
+        if (c + 1 == BN / 32) {  // accumulator fully in registers: hand it back to the MMA issuer
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(tempty_leader + as * 8);
+        }
+        if (!valid) continue;
+        const int ch0 = nb * BN + c * 32;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          const uint4 braw = __ldg(reinterpret_cast<const uint4*>(cp.bias + ch0 + i));
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 bf = __bfloat1622float2(b2[j]);
+            v[i + 2 * j] = __uint_as_float(r[i + 2 * j]) + bf.x;
+            v[i + 2 * j + 1] = __uint_as_float(r[i + 2 * j + 1]) + bf.y;
+          }
+        }
+        if (cp.resid != nullptr && cp.resid_f32) {
+          const float4* rp = reinterpret_cast<const float4*>(static_cast<const float*>(cp.resid) + vox * cp.Coutp + ch0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 r = __ldg(rp + q);
+            v[4 * q] += r.x;
+            v[4 * q + 1] += r.y;
+            v[4 * q + 2] += r.z;
+            v[4 * q + 3] += r.w;
+          }
+        } else if (cp.resid != nullptr) {
+          const uint4* rp =
+              reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(cp.resid) + vox * cp.Coutp + ch0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 raw = __ldg(rp + q);
+            const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 rf = __bfloat1622float2(r2[j]);
+              v[8 * q + 2 * j] += rf.x;
+              v[8 * q + 2 * j + 1] += rf.y;
+            }
+          }
+        }
+        if (cp.mode == CONV_OUT_F32_CLAMP) {
+          float* o = static_cast<float*>(cp.out) + vox * cp.out_real;
+          for (int i = 0; i < 32 && ch0 + i < cp.out_real; ++i) o[ch0 + i] = fminf(fmaxf(v[i], -1.0f), 1.0f);
+          continue;
+        }
+        if (cp.mode == CONV_OUT_F32) {
+          float4* o = reinterpret_cast<float4*>(static_cast<float*>(cp.out) + vox * cp.out_cs + ch0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          continue;
+        }
+        long long dst_vox = vox;
+        int dch = ch0;
+        if (cp.mode == CONV_OUT_TIME_INTERLEAVE) {  // output frames 2t + 1 (first half), 2t + 2 (second)
+          const int half = ch0 >= cp.out_real;
+          dch = ch0 - half * cp.out_real;
+          dst_vox = (static_cast<long long>(2 * t + 1 + half) * cp.H + h) * cp.W + w;
+        }
+        uint4* o = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(cp.out) + dst_vox * cp.out_cs + dch);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                            pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, C::TMEM_COLS);
+  }
+}
+
+bool make_tma_4d_act(CUtensorMap* m, const void* base, int Cp, int W, int H, int T) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(Cp), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
+                        static_cast<cuuint64_t>(T)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(Cp) * 2, static_cast<cuuint64_t>(W) * Cp * 2,
+                           static_cast<cuuint64_t>(H) * W * Cp * 2};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(CBK), PATCH_W, PATCH_H, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+cudaError_t launch_conv(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
+  using C = CCfg<BN>;
+  CUtensorMap ta, tb;
+  if (!make_tma_4d_act(&ta, x, cp.Cp, cp.W, cp.H, cp.T)) return cudaErrorInvalidValue;
+  const long long K = static_cast<long long>(cp.kt) * cp.kh * cp.kw * cp.Cp;
+  if (!make_tma_2d_bf16(&tb, w, K, cp.Coutp, K * 2, CBK, BN / 2)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const long long tiles = static_cast<long long>(cp.T) * ((cp.H + 7) / 8) * ((cp.W + 31) / 32) * (cp.Coutp / BN);
+  const int pairs = static_cast<int>(std::min<long long>(tiles, num_sms / 2));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(CTHREADS);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute at;
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, conv3d_tc_kernel<BN>, ta, tb, cp);
+}
+}  // namespace
+
+int conv_bn(int Coutp) {
+  if (Coutp % 256 == 0) return 256;
+  if (Coutp % 192 == 0) return 192;
+  if (Coutp % 128 == 0) return 128;
+  return 64;
+}
+
+cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
+  if (cp.T <= 0 || cp.H <= 0 || cp.W <= 0) return cudaSuccess;
+  if (cp.Cp % CBK || cp.Coutp % 64 || cp.kt < 1 || cp.kh < 1 || cp.kw < 1 || !cp.bias || !cp.out)
+    return cudaErrorInvalidValue;
+  if ((cp.mode == CONV_OUT_BF16 || cp.mode == CONV_OUT_F32) && (cp.out_cs % 8 || cp.out_cs < cp.Coutp))
+    return cudaErrorInvalidValue;
+  if (cp.mode == CONV_OUT_TIME_INTERLEAVE && (cp.out_real % 32 || 2 * cp.out_real > cp.Coutp || cp.out_cs % 8))
+    return cudaErrorInvalidValue;
+  switch (conv_bn(cp.Coutp)) {
+    case 256: return launch_conv<256>(x, w, cp, num_sms, stream);
+    case 192: return launch_conv<192>(x, w, cp, num_sms, stream);
+    case 128: return launch_conv<128>(x, w, cp, num_sms, stream);
+    default: return launch_conv<64>(x, w, cp, num_sms, stream);
+  }
+}
+
+}  // namespace gs

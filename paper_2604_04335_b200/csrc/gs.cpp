@@ -21,9 +21,17 @@
 
 using namespace gs;
 
+namespace gs {
+thread_local cudaStream_t tl_stream = nullptr;
+thread_local std::string* tl_err = nullptr;
+}  // namespace gs
+
 namespace {
 
 constexpr int MAX_BATCH = 8;
+
+// The stream this thread launches the context's work on (runtime.h tl_stream).
+inline cudaStream_t strm(gs_ctx* c) { return tl_stream ? tl_stream : c->stream; }
 
 int fail(gs_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
@@ -31,9 +39,30 @@ int fail(gs_ctx* c, int code, const char* fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(buf, sizeof buf, fmt, ap);
   va_end(ap);
-  if (c) c->err = buf;
+  if (tl_err) {
+    *tl_err = buf;
+  } else if (c) {
+    std::lock_guard<std::mutex> g(c->err_mu);
+    c->err = buf;
+  }
   return code;
 }
+
+int no_runs_in_flight(gs_ctx* c, const char* what);
+
+// GS_DEBUG=1: progress lines on stderr (diagnosis of hangs on the GPU box)
+bool dbg_on() {
+  static const bool on = getenv("GS_DEBUG") != nullptr;
+  return on;
+}
+#define DBG(...)                            \
+  do {                                      \
+    if (dbg_on()) {                         \
+      fprintf(stderr, "[gs] " __VA_ARGS__); \
+      fprintf(stderr, "\n");                \
+      fflush(stderr);                       \
+    }                                       \
+  } while (0)
 
 #define CK(call)                                                                          \
   do {                                                                                    \
@@ -58,7 +87,7 @@ int fail(gs_ctx* c, int code, const char* fmt, ...) {
 int ensure(gs_ctx* c, DevBuf& b, size_t bytes) {
   if (bytes <= b.cap) return GS_OK;
   if (b.p) {
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(strm(c)));
     CK(cudaFree(b.p));
     b.p = nullptr;
     b.cap = 0;
@@ -79,6 +108,7 @@ constexpr size_t kPoolGrain = size_t(2) << 20;  // 2 MiB blocks
 size_t pool_round(size_t bytes) { return (std::max<size_t>(bytes, 1) + kPoolGrain - 1) / kPoolGrain * kPoolGrain; }
 
 void* pool_alloc(gs_ctx* c, size_t bytes) {
+  std::lock_guard<std::mutex> g(c->pool_mu);
   const size_t sz = pool_round(bytes);
   auto it = c->pool.find(sz);
   if (it != c->pool.end()) {
@@ -89,7 +119,7 @@ void* pool_alloc(gs_ctx* c, size_t bytes) {
   void* p = nullptr;
   if (cudaMalloc(&p, sz) == cudaSuccess) return p;
   cudaGetLastError();
-  cudaStreamSynchronize(c->stream);  // out of memory: return the cached blocks and retry
+  cudaStreamSynchronize(strm(c));  // out of memory: return the cached blocks and retry
   for (auto& kv : c->pool) cudaFree(kv.second);
   c->pool.clear();
   if (cudaMalloc(&p, sz) == cudaSuccess) return p;
@@ -97,12 +127,15 @@ void* pool_alloc(gs_ctx* c, size_t bytes) {
   return nullptr;
 }
 
+// Callers free a block only after its last user completed (the owning request is not running and
+// the freeing path synchronised its stream), so a block may be reused on any lane.
 void pool_free(gs_ctx* c, void* p, size_t bytes) {
+  std::lock_guard<std::mutex> g(c->pool_mu);
   if (p) c->pool.emplace(pool_round(bytes), p);
 }
 
 // ------------------------------------------------------------------ profiling scopes
-cudaEvent_t get_event(gs_ctx* c) {
+cudaEvent_t get_event(gs_ctx* c) {  // caller holds prof_mu
   if (!c->event_pool.empty()) {
     cudaEvent_t e = c->event_pool.back();
     c->event_pool.pop_back();
@@ -120,20 +153,23 @@ struct Scope {
   Scope(gs_ctx* c_, const char* n, int launches) : c(c_), name(n) {
     c->launches += launches;
     if (c->prof) {
+      std::lock_guard<std::mutex> g(c->prof_mu);
       a = get_event(c);
       b = get_event(c);
-      cudaEventRecord(a, c->stream);
+      cudaEventRecord(a, strm(c));
     }
   }
   ~Scope() {
     if (c->prof) {
-      cudaEventRecord(b, c->stream);
+      std::lock_guard<std::mutex> g(c->prof_mu);
+      cudaEventRecord(b, strm(c));
       c->prof_pending.push_back({name, {a, b}});
     }
   }
 };
 
 void prof_flush(gs_ctx* c) {
+  std::lock_guard<std::mutex> g(c->prof_mu);
   // "_gaps": device time between consecutive scopes (launch latency, kernel ramp / drain outside
   // any kernel, host-side stalls), = span(first start .. last end) - sum of the scopes.
   if (c->prof_pending.size() > 1) {
@@ -202,7 +238,7 @@ int gen(gs_ctx* c, Model& m, void** dst, const WSpec& s, uint64_t seed) {
   }
   m.allocs.push_back(p);
   const float scale = s.fan_in > 0 ? static_cast<float>(std::sqrt(3.0 / s.fan_in)) : s.scale;
-  CK(rng_fill(p, n, seed, s.tid, s.kind, scale, c->stream));
+  CK(rng_fill(p, n, seed, s.tid, s.kind, scale, strm(c)));
   *dst = p;
   return GS_OK;
 }
@@ -409,11 +445,11 @@ int prepare_rank(gs_ctx* c, const Plan& P, int i, RankArena& A) {
   for (size_t r = 0; r < P.ureqs.size(); ++r)
     for (int a = 0; a < 3; ++a) grid[3 * r + a] = P.ureqs[r]->grid[a];
   if (P.rows[i] > 0) {
-    CK(cudaMemcpyAsync(A.row_req.p, rr.data(), rr.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(A.row_tok.p, rt.data(), rt.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(A.row_req.p, rr.data(), rr.size() * 4, cudaMemcpyHostToDevice, strm(c)));
+    CK(cudaMemcpyAsync(A.row_tok.p, rt.data(), rt.size() * 4, cudaMemcpyHostToDevice, strm(c)));
   }
-  CK(cudaMemcpyAsync(A.req_grid.p, grid.data(), grid.size() * 4, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaStreamSynchronize(c->stream));  // host vectors go out of scope
+  CK(cudaMemcpyAsync(A.req_grid.p, grid.data(), grid.size() * 4, cudaMemcpyHostToDevice, strm(c)));
+  CK(cudaStreamSynchronize(strm(c)));  // host vectors go out of scope
   return GS_OK;
 }
 
@@ -426,9 +462,9 @@ int move_latent(gs_ctx* c, const Plan& P, int i, RankArena& A, int dir) {
     float* packed = A.zpack.as<float>() + static_cast<size_t>(P.loff[i][r]) * lat;
     float* shard = P.reqs[r]->shards[i].z;
     if (dir == 0)
-      CK(cudaMemcpyAsync(packed, shard, cnt, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(packed, shard, cnt, cudaMemcpyDeviceToDevice, strm(c)));
     else
-      CK(cudaMemcpyAsync(shard, packed, cnt, cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(shard, packed, cnt, cudaMemcpyDeviceToDevice, strm(c)));
   }
   return GS_OK;
 }
@@ -446,10 +482,10 @@ int my_position(gs_ctx* c, const Plan& P) {
 
 int copy_block(gs_ctx* c, void* dst, const void* src, const gs_xfer& x, size_t esz) {
   if (x.rows == 1 || (x.src_pitch == x.width && x.dst_pitch == x.width))
-    CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(x.rows * x.width) * esz, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(x.rows * x.width) * esz, cudaMemcpyDeviceToDevice, strm(c)));
   else
     CK(cudaMemcpy2DAsync(dst, x.dst_pitch * esz, src, x.src_pitch * esz, x.width * esz, x.rows,
-                         cudaMemcpyDeviceToDevice, c->stream));
+                         cudaMemcpyDeviceToDevice, strm(c)));
   return GS_OK;
 }
 
@@ -470,7 +506,7 @@ int run_emulated(gs_ctx* c, const std::vector<std::vector<gs_xfer>>& plans, BufF
         if (snd[k]->width != rcv[k]->width) return fail(c, GS_ESTATE, "exchange size mismatch %d -> %d", i, j);
         char* dst = static_cast<char*>(bufs(j, rcv[k]->dst_buf)) + rcv[k]->dst_off * esz;
         const char* src = static_cast<const char*>(bufs(i, snd[k]->src_buf)) + snd[k]->src_off * esz;
-        CK(cudaMemcpyAsync(dst, src, snd[k]->width * esz, cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaMemcpyAsync(dst, src, snd[k]->width * esz, cudaMemcpyDeviceToDevice, strm(c)));
       }
     }
   for (int i = 0; i < p; ++i)
@@ -513,9 +549,9 @@ int exchange_qkv(gs_ctx* c, const Plan& P) {
   for (int t = 0; t < 3; ++t)
     for (const gs_xfer& x : plans[t ? 1 : 0]) {
       if (x.op == GS_XFER_SEND)
-        NK(ncclSend(snd[t] + x.src_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, c->stream));
+        NK(ncclSend(snd[t] + x.src_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, strm(c)));
       else if (x.op == GS_XFER_RECV)
-        NK(ncclRecv(rcv[t] + x.dst_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, c->stream));
+        NK(ncclRecv(rcv[t] + x.dst_off, x.width * 2, ncclUint8, P.ranks[x.peer], c->comm, strm(c)));
     }
   NK(ncclGroupEnd());
   for (int t = 0; t < 3; ++t)
@@ -545,10 +581,10 @@ int exchange_o(gs_ctx* c, const Plan& P) {
   for (const gs_xfer& x : plan) {
     if (x.op == GS_XFER_SEND)
       NK(ncclSend(static_cast<bf16*>(arena_buf(A, x.src_buf)) + x.src_off, x.width * 2, ncclUint8, P.ranks[x.peer],
-                  c->comm, c->stream));
+                  c->comm, strm(c)));
     else if (x.op == GS_XFER_RECV)
       NK(ncclRecv(static_cast<bf16*>(arena_buf(A, x.dst_buf)) + x.dst_off, x.width * 2, ncclUint8, P.ranks[x.peer],
-                  c->comm, c->stream));
+                  c->comm, strm(c)));
   }
   NK(ncclGroupEnd());
   for (const gs_xfer& x : plan)
@@ -572,7 +608,7 @@ struct IpcExport {
   int ok;
 };
 
-int peer_setup(gs_ctx* c, Plan& P) {
+int peer_setup(gs_ctx* c, Plan& P, const unsigned* gens = nullptr) {
   P.peer = false;
   if (c->a2a_mode != 1 || P.p == 1 || P.R != 0 || P.B > OSC_MAX_REQ || c->world > 8) return GS_OK;
   P.qr_of.assign(P.p, nullptr);
@@ -580,12 +616,6 @@ int peer_setup(gs_ctx* c, Plan& P) {
   P.vr_of.assign(P.p, nullptr);
   P.orecv_of.assign(P.p, nullptr);
   P.flags_of.assign(P.p, nullptr);
-  if (!c->flags) {
-    // words [0, 8): barrier counters per source rank, [8, 16): mapping-probe counters
-    const size_t words = static_cast<size_t>(c->emulated ? c->world : 1) * 16;
-    CK(cudaMalloc(&c->flags, words * 8));
-    CK(cudaMemset(c->flags, 0, words * 8));
-  }
   if (c->emulated) {
     for (int j = 0; j < P.p; ++j) {
       RankArena& A = c->local[P.ranks[j]];
@@ -602,24 +632,53 @@ int peer_setup(gs_ctx* c, Plan& P) {
   // peers (re-opened only when a peer re-allocated), then agree that every position mapped all
   // of them before any kernel stores into peer memory.
   const int me = my_position(c, P);
+  if (me < 0) return fail(c, GS_ESTATE, "peer_setup: this process is not in the SP group");
   RankArena& A = c->local[0];
   IpcExport mine{};
   void* bases[5] = {A.qr.p, A.kr.p, A.vr.p, A.orecv.p, c->flags};
+  // the arena generation moves whenever an exported buffer was re-allocated since the last run
+  if (memcmp(bases, c->exported, sizeof bases) != 0) {
+    memcpy(c->exported, bases, sizeof bases);
+    ++c->arena_gen;
+  }
+  auto use_mappings = [&] {
+    for (int j = 0; j < P.p; ++j) {
+      void* const* p = j == me ? bases : c->peers[P.ranks[j]].p;
+      P.qr_of[j] = static_cast<bf16*>(p[0]);
+      P.kr_of[j] = static_cast<bf16*>(p[1]);
+      P.vr_of[j] = static_cast<bf16*>(p[2]);
+      P.orecv_of[j] = static_cast<bf16*>(p[3]);
+      P.flags_of[j] = static_cast<unsigned long long*>(p[4]);
+    }
+    P.peer = true;
+  };
+  // cache hit: the same SP group verified its mappings before, and every position (this one
+  // included, gens from the step-0 agreement) still has the generation those mappings belong to
+  if (gens && c->cached_ok && c->cached_group == P.ranks) {
+    bool same = gens[me] == c->peer_gen[c->my_rank];
+    for (int j = 0; j < P.p && same; ++j)
+      if (j != me) same = gens[j] == c->peer_gen[P.ranks[j]];
+    if (same) {
+      use_mappings();
+      return GS_OK;
+    }
+  }
+  ++c->ipc_exchanges;
   for (int b = 0; b < 5; ++b) CK(cudaIpcGetMemHandle(&mine.h[b], bases[b]));
   mine.ok = 1;
   if (!c->ipc_dev) CK(cudaMalloc(&c->ipc_dev, 9 * sizeof(IpcExport)));
   IpcExport* dev = static_cast<IpcExport*>(c->ipc_dev);
   auto exchange = [&](IpcExport* host_all) -> int {
-    CK(cudaMemcpyAsync(dev + me, host_all + me, sizeof(IpcExport), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dev + me, host_all + me, sizeof(IpcExport), cudaMemcpyHostToDevice, strm(c)));
     NK(ncclGroupStart());
     for (int j = 0; j < P.p; ++j) {
       if (j == me) continue;
-      NK(ncclSend(dev + me, sizeof(IpcExport), ncclUint8, P.ranks[j], c->comm, c->stream));
-      NK(ncclRecv(dev + j, sizeof(IpcExport), ncclUint8, P.ranks[j], c->comm, c->stream));
+      NK(ncclSend(dev + me, sizeof(IpcExport), ncclUint8, P.ranks[j], c->comm, strm(c)));
+      NK(ncclRecv(dev + j, sizeof(IpcExport), ncclUint8, P.ranks[j], c->comm, strm(c)));
     }
     NK(ncclGroupEnd());
-    CK(cudaMemcpyAsync(host_all, dev, P.p * sizeof(IpcExport), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(host_all, dev, P.p * sizeof(IpcExport), cudaMemcpyDeviceToHost, strm(c)));
+    CK(cudaStreamSynchronize(strm(c)));
     return GS_OK;
   };
   std::vector<IpcExport> all(P.p);
@@ -655,10 +714,10 @@ int peer_setup(gs_ctx* c, Plan& P) {
       wt.slot[wt.n] = c->flags + 8 + gj;
       wt.val[wt.n++] = c->probe_seen[gj] + 1;
     }
-    CK(peer_signal(sig, c->stream));
-    CK(peer_wait_probe(wt, 2000, c->d_flag + 12, c->stream));
-    CK(cudaMemcpyAsync(c->h_flag + 12, c->d_flag + 12, 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(peer_signal(sig, strm(c)));
+    CK(peer_wait_probe(wt, 2000, c->d_flag + 12, strm(c)));
+    CK(cudaMemcpyAsync(c->h_flag + 12, c->d_flag + 12, 4, cudaMemcpyDeviceToHost, strm(c)));
+    CK(cudaStreamSynchronize(strm(c)));
     ok = c->h_flag[12];
     if (ok)
       for (int j = 0; j < P.p; ++j)
@@ -668,16 +727,14 @@ int peer_setup(gs_ctx* c, Plan& P) {
   agree[me].ok = ok;
   RET(exchange(agree.data()));
   for (int j = 0; j < P.p; ++j) ok &= agree[j].ok;
+  c->cached_ok = false;
   if (!ok) return GS_OK;
-  for (int j = 0; j < P.p; ++j) {
-    void* const* p = j == me ? bases : c->peers[P.ranks[j]].p;
-    P.qr_of[j] = static_cast<bf16*>(p[0]);
-    P.kr_of[j] = static_cast<bf16*>(p[1]);
-    P.vr_of[j] = static_cast<bf16*>(p[2]);
-    P.orecv_of[j] = static_cast<bf16*>(p[3]);
-    P.flags_of[j] = static_cast<unsigned long long*>(p[4]);
+  use_mappings();
+  if (gens) {  // remember the verified group and the generations its mappings belong to
+    c->cached_group = P.ranks;
+    for (int j = 0; j < P.p; ++j) c->peer_gen[P.ranks[j]] = gens[j];
+    c->cached_ok = true;
   }
-  P.peer = true;
   return GS_OK;
 }
 
@@ -695,7 +752,7 @@ int peer_barrier(gs_ctx* c, const Plan& P, const std::vector<int>& mine) {
       f.val[f.n] = ++c->sig_sent[P.ranks[i]][P.ranks[j]];
       ++f.n;
     }
-    CK(peer_signal(f, c->stream));
+    CK(peer_signal(f, strm(c)));
   }
   for (int j : mine) {
     PeerFlags f{};
@@ -705,7 +762,7 @@ int peer_barrier(gs_ctx* c, const Plan& P, const std::vector<int>& mine) {
       f.val[f.n] = ++c->sig_seen[P.ranks[i]][P.ranks[j]];
       ++f.n;
     }
-    CK(peer_wait(f, c->stream));
+    CK(peer_wait(f, strm(c)));
   }
   ++c->a2a_peer;
   return GS_OK;
@@ -716,7 +773,7 @@ int gemm(gs_ctx* c, const char* name, int epi, int M, int N, int K, const void* 
          const EpiParams& ep) {
   if (M == 0) return GS_OK;
   Scope sc(c, name, 1);
-  CK(gemm_bf16_tc(epi, M, N, K, A, K, W, K, ep, c->num_sms, c->stream));
+  CK(gemm_bf16_tc(epi, M, N, K, A, K, W, K, ep, c->num_sms, strm(c)));
   return GS_OK;
 }
 
@@ -736,7 +793,7 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
   {
     Scope sc(c, "ln_mod", 1);
     if (M) CK(ln_modulate(A.x.as<float>(), M, D, w.mod + 0 * D, A.e.as<float>() + 0 * D, w.mod + 1 * D,
-                          A.e.as<float>() + 1 * D, 6 * D, A.row_req.as<int>(), eps, A.a.as<bf16>(), c->stream));
+                          A.e.as<float>() + 1 * D, 6 * D, A.row_req.as<int>(), eps, A.a.as<bf16>(), strm(c)));
   }
   RET(gemm(c, "gemm_qkv", EPI_BF16, M, 3 * D, D, A.a.p, w.w_qkv, epi(A.qkv.p, 3 * D, w.b_qkv)));
   {
@@ -765,7 +822,7 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
       }
     }
     if (M) CK(qk_norm_rope_pack(A.qkv.as<bf16>(), M, D, P.H, w.g_q, w.g_k, eps, rp, pk, A.qs.as<bf16>(),
-                                A.ks.as<bf16>(), A.vs.as<bf16>(), c->stream));
+                                A.ks.as<bf16>(), A.vs.as<bf16>(), strm(c)));
   }
   return GS_OK;
 }
@@ -780,7 +837,7 @@ int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
   if (P.p == 1) {
     const int rs = P.H * P.hd;
     CK(attention_tc(A.qs.p, A.ks.p, A.vs.p, A.o.p, P.H, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
-                    c->stream));
+                    strm(c)));
     return GS_OK;
   }
   if (P.peer) {  // fused head->seq exchange: output rows straight into their owners' ORECV
@@ -796,14 +853,14 @@ int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
       }
     const int rs = P.Hf * P.hd;
     CK(attention_tc(A.qr.p, A.kr.p, A.vr.p, nullptr, P.Hf, P.hd, rs, rs, P.D, so.data(), sl.data(), P.B,
-                    c->num_sms, c->stream, &osc));
+                    c->num_sms, strm(c), &osc));
     return GS_OK;
   }
   // full heads of this position
   if (P.Hf) {
     const int rs = P.Hf * P.hd;
     CK(attention_tc(A.qr.p, A.kr.p, A.vr.p, A.o.p, P.Hf, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
-                    c->stream));
+                    strm(c)));
   }
   // partial-head units: the unit's query chunk of every request against the head's full K / V
   for (size_t t = 0; t < P.units_of[j].size(); ++t) {
@@ -818,7 +875,7 @@ int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
     const bf16* v = A.vr.as<bf16>() + P.unit_kv_off(j, static_cast<int>(t));
     bf16* o = A.o.as<bf16>() + P.unit_q_off(j, static_cast<int>(t));
     CK(attention_tc_segments(q, k, v, o, 1, P.hd, P.hd, P.hd, P.hd, qo.data(), ql.data(), so.data(), sl.data(), P.B,
-                             c->stream));
+                             strm(c)));
   }
   return GS_OK;
 }
@@ -834,12 +891,12 @@ int block_cross(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
   {
     Scope sc(c, "ln_mod", 1);
     CK(ln_modulate(A.x.as<float>(), M, D, w.ln3_shift, P.m->zeros, w.ln3_scale_m1, P.m->zeros, 0,
-                   A.row_req.as<int>(), eps, A.a.as<bf16>(), c->stream));
+                   A.row_req.as<int>(), eps, A.a.as<bf16>(), strm(c)));
   }
   RET(gemm(c, "gemm_cross_q", EPI_BF16, M, D, D, A.a.p, w.w_cq, epi(A.qc.p, D, w.b_cq)));
   {
     Scope sc(c, "rmsnorm", 1);
-    CK(rmsnorm_rows(A.qc.as<bf16>(), D, M, D, w.g_cq, eps, A.qc.as<bf16>(), c->stream));
+    CK(rmsnorm_rows(A.qc.as<bf16>(), D, M, D, w.g_cq, eps, A.qc.as<bf16>(), strm(c)));
   }
   const int li = local_index(c, P.ranks[i]);
   for (int v = 0; v < P.B; ++v) {
@@ -851,7 +908,7 @@ int block_cross(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
     bf16* q = A.qc.as<bf16>() + static_cast<size_t>(P.loff[i][v]) * D;
     const int zero = 0;
     // in place: each CTA reads its Q tiles before it writes the same rows / head columns of O
-    CK(attention_tc_segments(q, kv, kv + per, q, P.H, P.hd, D, D, D, &zero, &cnt, &zero, &Lt, 1, c->stream));
+    CK(attention_tc_segments(q, kv, kv + per, q, P.H, P.hd, D, D, D, &zero, &cnt, &zero, &Lt, 1, strm(c)));
   }
   RET(gemm(c, "gemm_cross_o", EPI_ADD_F32, M, D, D, A.qc.p, w.w_co, epi(A.x.p, D, w.b_co)));
   return GS_OK;
@@ -872,7 +929,7 @@ int block_post(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
     Scope sc(c, "ln_mod", 1);
     if (M) CK(ln_modulate(A.x.as<float>(), M, D, w.mod + 3 * D, A.e.as<float>() + 3 * D, w.mod + 4 * D,
                           A.e.as<float>() + 4 * D, 6 * D, A.row_req.as<int>(), P.m->desc.eps, A.a.as<bf16>(),
-                          c->stream));
+                          strm(c)));
   }
   RET(gemm(c, "gemm_mlp_up", EPI_GELU_BF16, M, F, D, A.a.p, w.w_1, epi(A.h.p, F, w.b_1)));
   EpiParams e2 = epi(A.x.p, D, w.b_2);
@@ -891,11 +948,11 @@ int step_prologue(gs_ctx* c, const Plan& P, int i, RankArena& A, const float* t)
     Scope sc(c, "time_embed", 4);
     TimeEmbedW tw{m->w_t1, m->b_t1, m->w_t2, m->b_t2, m->w_tp, m->b_tp, D, m->desc.freq_dim};
     CK(time_embed(tw, static_cast<int>(P.ureqs.size()), t, A.temb.as<float>(), A.e0.as<float>(),
-                  A.e.as<float>(), c->stream));
+                  A.e.as<float>(), strm(c)));
   }
   {
     Scope sc(c, "patch_embed", 1);
-    if (M) CK(f32_to_bf16(A.zpack.as<float>(), A.zb.as<bf16>(), static_cast<long long>(M) * m->desc.lat, c->stream));
+    if (M) CK(f32_to_bf16(A.zpack.as<float>(), A.zb.as<bf16>(), static_cast<long long>(M) * m->desc.lat, strm(c)));
   }
   RET(gemm(c, "patch_embed", EPI_F32, M, D, m->desc.lat, A.zb.p, m->w_pe, epi(A.x.p, D, m->b_pe)));
   return GS_OK;
@@ -907,7 +964,7 @@ int step_epilogue(gs_ctx* c, const Plan& P, int i, RankArena& A, const float* ds
   {
     Scope sc(c, "head", 1);
     if (M) CK(ln_modulate(A.x.as<float>(), M, D, m->mod_head, A.e0.as<float>(), m->mod_head + D, A.e0.as<float>(), D,
-                          A.row_req.as<int>(), m->desc.eps, A.a.as<bf16>(), c->stream));
+                          A.row_req.as<int>(), m->desc.eps, A.a.as<bf16>(), strm(c)));
   }
   if (!P.text) {
     EpiParams eh = epi(A.zpack.p, m->desc.lat, m->b_head);
@@ -933,7 +990,7 @@ int step_epilogue(gs_ctx* c, const Plan& P, int i, RankArena& A, const float* ds
     Scope sc(c, "cfg_euler", 1);
     const size_t off = static_cast<size_t>(P.loff[i][v]) * lat;
     CK(cfg_euler(A.zpack.as<float>() + off, zu, A.vbuf.as<float>() + off, vu, cnt, dsig[P.real[v]], P.reqs[v]->cfg,
-                 c->stream));
+                 strm(c)));
   }
   return GS_OK;
 }
@@ -967,29 +1024,35 @@ int run_one_step(gs_ctx* c, const Plan& P, const std::vector<int>& mine) {
   return GS_OK;
 }
 
-// Agree on "stop at this boundary" across the SP group (NCCL mode): OR of local flags.
-int agree_stop(gs_ctx* c, const Plan& P, int local_flag, int* stop) {
+// Agree on "stop at this boundary" across the SP group (NCCL mode): OR of local flags.  The same
+// exchange carries each position's arena generation (gens[j] for SP position j; may be null), which
+// lets the first step of a run re-use cached IPC mappings (peer_setup).
+int agree_stop(gs_ctx* c, const Plan& P, int local_flag, int* stop, unsigned* gens = nullptr) {
   if (c->emulated || P.p == 1) {
     *stop = local_flag;
     return GS_OK;
   }
-  int me = 0;
-  for (int i = 0; i < P.p; ++i)
-    if (P.ranks[i] == c->my_rank) me = i;
+  const int me = my_position(c, P);
+  if (me < 0) return fail(c, GS_ESTATE, "agree_stop: this process is not in the SP group");
   c->h_flag[0] = local_flag;
-  CK(cudaMemcpyAsync(c->d_flag, c->h_flag, 4, cudaMemcpyHostToDevice, c->stream));
+  c->h_flag[1] = static_cast<int>(c->arena_gen);
+  CK(cudaMemcpyAsync(c->d_flag, c->h_flag, 8, cudaMemcpyHostToDevice, strm(c)));
   NK(ncclGroupStart());
   for (int j = 0; j < P.p; ++j) {
     if (j == me) continue;
-    NK(ncclSend(c->d_flag, 1, ncclInt32, P.ranks[j], c->comm, c->stream));
-    NK(ncclRecv(c->d_flag + 1 + j, 1, ncclInt32, P.ranks[j], c->comm, c->stream));
+    NK(ncclSend(c->d_flag, 2, ncclInt32, P.ranks[j], c->comm, strm(c)));
+    NK(ncclRecv(c->d_flag + 2 + 2 * j, 2, ncclInt32, P.ranks[j], c->comm, strm(c)));
   }
   NK(ncclGroupEnd());
-  CK(cudaMemcpyAsync(c->h_flag + 1, c->d_flag + 1, 8 * 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpyAsync(c->h_flag + 2, c->d_flag + 2, 16 * 4, cudaMemcpyDeviceToHost, strm(c)));
+  CK(cudaStreamSynchronize(strm(c)));
   int s = local_flag;
-  for (int j = 0; j < P.p; ++j)
-    if (j != me) s |= c->h_flag[1 + j];
+  for (int j = 0; j < P.p; ++j) {
+    if (j == me) continue;
+    s |= c->h_flag[2 + 2 * j];
+    if (gens) gens[j] = static_cast<unsigned>(c->h_flag[3 + 2 * j]);
+  }
+  if (gens) gens[me] = c->arena_gen;
   *stop = s;
   return GS_OK;
 }
@@ -1021,7 +1084,7 @@ int ensure_text_cache(gs_ctx* c, Model* m, Request* q, int li) {
   if (!buf.p) return fail(c, GS_ENOMEM, "text cache alloc failed");
   DevBuf emb, h1, cx, kv;
   auto cleanup = [&] {
-    cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(strm(c));
     for (DevBuf* b : {&emb, &h1, &cx, &kv})
       if (b->p) cudaFree(b->p);
   };
@@ -1034,11 +1097,11 @@ int ensure_text_cache(gs_ctx* c, Model* m, Request* q, int li) {
     if ((rc = ensure(c, kv, rows * 2 * D * 2)) != GS_OK) break;
     cudaError_t e = cudaSuccess;
     if (!q->prompt_host.empty())
-      e = cudaMemcpyAsync(emb.p, q->prompt_host.data(), rows * T * 2, cudaMemcpyHostToDevice, c->stream);
+      e = cudaMemcpyAsync(emb.p, q->prompt_host.data(), rows * T * 2, cudaMemcpyHostToDevice, strm(c));
     else
       for (int b = 0; b < nb && e == cudaSuccess; ++b)
         e = rng_normal_bf16(emb.as<bf16>() + static_cast<size_t>(b) * Lt * T, static_cast<long long>(Lt) * T,
-                            q->prompt_seed, 50 + b, c->stream);
+                            q->prompt_seed, 50 + b, strm(c));
     if (e != cudaSuccess) {
       rc = fail(c, GS_ECUDA, "prompt upload: %s", cudaGetErrorString(e));
       break;
@@ -1051,9 +1114,9 @@ int ensure_text_cache(gs_ctx* c, Model* m, Request* q, int li) {
       for (int b = 0; b < nb && rc == GS_OK; ++b) {
         bf16* dst = buf.as<bf16>() + (static_cast<size_t>(b) * NL + l) * 2 * per;
         const bf16* src = kv.as<bf16>() + static_cast<size_t>(b) * Lt * 2 * D;
-        e = rmsnorm_rows(src, 2 * D, Lt, D, w.g_ck, m->desc.eps, dst, c->stream);
+        e = rmsnorm_rows(src, 2 * D, Lt, D, w.g_ck, m->desc.eps, dst, strm(c));
         if (e == cudaSuccess)
-          e = cudaMemcpy2DAsync(dst + per, D * 2, src + D, 2 * D * 2, D * 2, Lt, cudaMemcpyDeviceToDevice, c->stream);
+          e = cudaMemcpy2DAsync(dst + per, D * 2, src + D, 2 * D * 2, D * 2, Lt, cudaMemcpyDeviceToDevice, strm(c));
         if (e != cudaSuccess) rc = fail(c, GS_ECUDA, "text cache: %s", cudaGetErrorString(e));
       }
     }
@@ -1092,12 +1155,31 @@ int gs_nccl_unique_id(void* out128) {
   return GS_OK;
 }
 
-static int init_common(gs_ctx* c, int device) {
+// nlanes: one stream per local rank (lane 0 = the caller thread's stream); per global rank an idle
+// busy slot; the peer-store barrier words (fused all-to-alls, p > 1 only).
+static int init_common(gs_ctx* c, int device, int nlanes) {
+  DBG("init: device %d lanes %d", device, nlanes);
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  CK(cudaMallocHost(&c->h_flag, 16 * 4));
-  CK(cudaMalloc(&c->d_flag, 16 * 4));
+  c->lanes.push_back(c->stream);
+  for (int i = 1; i < nlanes; ++i) {
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    c->lanes.push_back(s);
+  }
+  c->busy.assign(c->world, 0);
+  CK(cudaMallocHost(&c->h_flag, 64 * 4));
+  CK(cudaMalloc(&c->d_flag, 64 * 4));
+  CK(cudaMallocHost(&c->h_id, 4 * 8));
+  CK(cudaMalloc(&c->d_id, 4 * 8));
+  if (c->world > 1) {
+    // words [0, 8): barrier counters per source rank, [8, 16): mapping-probe counters
+    const size_t words = static_cast<size_t>(c->emulated ? c->world : 1) * 16;
+    CK(cudaMalloc(&c->flags, words * 8));
+    CK(cudaMemset(c->flags, 0, words * 8));
+  }
+  DBG("init: done");
   return GS_OK;
 }
 
@@ -1107,7 +1189,7 @@ int gs_init(int device, int world_size, int rank, const void* nccl_uid, gs_ctx**
   c->device = device;
   c->world = world_size;
   c->my_rank = rank;
-  int rc = init_common(c, device);
+  int rc = init_common(c, device, 1);
   if (rc != GS_OK) {
     *out = c;
     return rc;
@@ -1122,16 +1204,17 @@ int gs_init(int device, int world_size, int rank, const void* nccl_uid, gs_ctx**
     ncclUniqueId id;
     memcpy(&id, nccl_uid, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->comm, world_size, id, rank);
+    if (r == ncclSuccess) r = ncclCommSplit(c->comm, 0, rank, &c->ctrl, nullptr);
     if (r != ncclSuccess) {
       *out = c;
-      return fail(c, GS_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+      return fail(c, GS_ENCCL, "ncclCommInitRank / ncclCommSplit: %s", ncclGetErrorString(r));
     }
-    // Our kernels release their dependents early (griddepcontrol.launch_dependents); a collective
-    // launched right after one must not start before it completes.  NCCL's own kernels are not
-    // known to wait on griddepcontrol, so multi-process contexts run in plain stream order unless
-    // GS_PDL=1 asks otherwise (this path has not been measured on two physical GPUs).
-    const char* e = getenv("GS_PDL");
-    if (!(e && e[0] == '1')) g_pdl.store(0);
+    // Programmatic dependent launch stays on: only OUR kernels carry the PDL launch attribute, so
+    // (a) an NCCL kernel enqueued after one of ours is a plain launch and waits for its completion,
+    // and (b) one of ours enqueued after an NCCL kernel may only start early if that kernel triggers
+    // griddepcontrol.launch_dependents, which NCCL's kernels do not -- the trigger is then implicit at
+    // their completion.  The fused peer-store exchange has no NCCL kernels on the data path at all.
+    // (Unmeasured on two physical GPUs: gpurun gives one; tests/test_gpu_multiproc.py covers it.)
   }
   *out = c;
   return GS_OK;
@@ -1143,7 +1226,7 @@ int gs_init_emulated(int device, int world_size, gs_ctx** out) {
   c->device = device;
   c->world = world_size;
   c->emulated = true;
-  int rc = init_common(c, device);
+  int rc = init_common(c, device, world_size);
   c->local.resize(world_size);
   for (int r = 0; r < world_size; ++r) c->local[r].rank = r;
   *out = c;
@@ -1152,7 +1235,16 @@ int gs_init_emulated(int device, int world_size, gs_ctx** out) {
 
 void gs_destroy(gs_ctx* c) {
   if (!c) return;
+  {
+    std::vector<gs_ticket> open;
+    {
+      std::lock_guard<std::mutex> g(c->table_mu);
+      for (auto& kv : c->tickets) open.push_back(kv.first);
+    }
+    for (gs_ticket t : open) gs_wait(c, t, nullptr);
+  }
   cudaSetDevice(c->device);
+  for (size_t i = 1; i < c->lanes.size(); ++i) cudaStreamSynchronize(c->lanes[i]);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& kv : c->reqs) {
     free_shards(c, kv.second->shards);
@@ -1162,6 +1254,11 @@ void gs_destroy(gs_ctx* c) {
   c->pool.clear();
   for (auto& m : c->models)
     for (void* p : m->allocs) cudaFree(p);
+  for (auto& v : c->vaes) {
+    for (void* p : v->allocs) cudaFree(p);
+    for (DevBuf* b : {&v->act[0], &v->act[1], &v->act[2], &v->act[3], &v->lat_stage, &v->vid_stage})
+      if (b->p) cudaFree(b->p);
+  }
   for (auto& A : c->local) {
     DevBuf* bufs[] = {&A.x, &A.a, &A.qkv, &A.qs, &A.ks, &A.vs, &A.qr, &A.kr, &A.vr, &A.o, &A.orecv,
                       &A.ostage, &A.h, &A.zpack, &A.zb, &A.e0, &A.e, &A.temb, &A.row_req, &A.row_tok,
@@ -1176,9 +1273,13 @@ void gs_destroy(gs_ctx* c) {
   if (c->ipc_dev) cudaFree(c->ipc_dev);
   for (auto e : c->event_pool) cudaEventDestroy(e);
   if (c->ev_order) cudaEventDestroy(c->ev_order);
+  if (c->ctrl) ncclCommDestroy(c->ctrl);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   if (c->d_flag) cudaFree(c->d_flag);
+  if (c->h_id) cudaFreeHost(c->h_id);
+  if (c->d_id) cudaFree(c->d_id);
+  for (size_t i = 1; i < c->lanes.size(); ++i) cudaStreamDestroy(c->lanes[i]);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1215,8 +1316,13 @@ int gs_info(gs_ctx* c, int* num_sms, int* world_size, int* nlocal) {
 
 int gs_model_create(gs_ctx* c, const gs_model_desc* d, int* model_id) {
   if (!c || !d || !model_id) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->run_mu);
+  DBG("model_create: enter");
+  std::lock_guard<std::mutex> g(c->api_mu);
+  DBG("model_create: api_mu");
+  RET(no_runs_in_flight(c, "gs_model_create"));
+  DBG("model_create: idle checked");
   CK(cudaSetDevice(c->device));
+  DBG("model_create: device set, stream %p", (void*)strm(c));
   if (d->dim <= 0 || d->heads <= 0 || d->dim % d->heads || d->dim % 64 || d->dim > 8192 || d->ffn % 256 ||
       d->layers < 1 || d->lat != 64 || d->freq_dim % 2 || d->freq_dim % 64)
     return fail(c, GS_EINVAL, "unsupported model shape (dim %d heads %d ffn %d lat %d)", d->dim, d->heads, d->ffn, d->lat);
@@ -1230,6 +1336,7 @@ int gs_model_create(gs_ctx* c, const gs_model_desc* d, int* model_id) {
   m->blocks.resize(d->layers);
   for (int l = 0; l < d->layers; ++l)
     for (const WSpec& s : all_block_specs(*d)) RET(gen(c, *m, block_slot(m->blocks[l], s.name), s, d->weight_seed + l));
+  DBG("model_create: block weights launched");
   for (const WSpec& s : all_global_specs(*d)) RET(gen(c, *m, global_slot(*m, s.name), s, d->weight_seed + 1000000ull));
   if (d->cross_attn) {
     // norm3 affine as ln_modulate tables: LN(x) * (1 + (w - 1)) + b, w - 1 exact in fp32
@@ -1241,7 +1348,7 @@ int gs_model_create(gs_ctx* c, const gs_model_desc* d, int* model_id) {
     m->allocs.push_back(pz);
     CK(cudaMemcpy(pz, zeros.data(), D * 4, cudaMemcpyHostToDevice));
     m->zeros = static_cast<float*>(pz);
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(strm(c)));
     for (int l = 0; l < d->layers; ++l) {
       BlockW& b = m->blocks[l];
       CK(cudaMemcpy(wv.data(), b.ln3_w, D * 2, cudaMemcpyDeviceToHost));
@@ -1287,7 +1394,9 @@ int gs_model_create(gs_ctx* c, const gs_model_desc* d, int* model_id) {
   CK(cudaMemcpy(pa, axis.data(), axis.size() * 4, cudaMemcpyHostToDevice));
   m->cs_tab = static_cast<float2*>(pt);
   m->slot_axis = static_cast<int*>(pa);
-  CK(cudaStreamSynchronize(c->stream));
+  DBG("model_create: syncing");
+  CK(cudaStreamSynchronize(strm(c)));
+  DBG("model_create: synced");
   c->models.push_back(std::move(m));
   *model_id = static_cast<int>(c->models.size()) - 1;
   return GS_OK;
@@ -1305,23 +1414,110 @@ int gs_get_weight(gs_ctx* c, int model, int layer, const char* name, void* host,
     if (bytes != want) return fail(c, GS_EINVAL, "%s is %zu bytes, got %zu", name, want, bytes);
     void** slot = layer < 0 ? global_slot(m, name) : block_slot(m.blocks[layer], name);
     CK(cudaSetDevice(c->device));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(strm(c)));
     CK(cudaMemcpy(host, *slot, bytes, cudaMemcpyDeviceToHost));
     return GS_OK;
   }
   return fail(c, GS_EINVAL, "unknown tensor %s", name);
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------------ requests and runs
+namespace {
+
+// Sets this thread's launch stream to the lane of `rank` for the guard's lifetime (emulated mode:
+// one lane per virtual rank, so disjoint SP groups run on different streams; NCCL mode: lane 0).
+struct LaneGuard {
+  cudaStream_t saved;
+  LaneGuard(gs_ctx* c, int rank) : saved(tl_stream) {
+    const int li = local_index(c, rank);
+    tl_stream = c->lanes[li >= 0 && li < static_cast<int>(c->lanes.size()) ? li : 0];
+  }
+  ~LaneGuard() { tl_stream = saved; }
+};
+
+// GS_ESTATE if a rank of `ranks` belongs to an in-flight run (caller holds table_mu).
+int check_idle(gs_ctx* c, const int* ranks, int n, const char* what) {
+  for (int i = 0; i < n; ++i)
+    if (c->busy[ranks[i]])
+      return fail(c, GS_ESTATE, "%s: rank %d belongs to in-flight run %llu (GPU sets of concurrent runs must be "
+                  "disjoint)", what, ranks[i], (unsigned long long)c->busy[ranks[i]]);
+  return GS_OK;
+}
+
+int no_runs_in_flight(gs_ctx* c, const char* what) {
+  std::lock_guard<std::mutex> g(c->table_mu);
+  if (!c->tickets.empty()) return fail(c, GS_ESTATE, "%s needs every run waited for (%zu in flight)", what, c->tickets.size());
+  return GS_OK;
+}
+
+// Allocate and initialise the latent shards of q on `ranks` (z_T from its seed or host copy).
+int place_shards(gs_ctx* c, Request* q, const int* ranks, int nranks) {
+  const int lat = c->models[q->model]->desc.lat;
+  LaneGuard lane(c, ranks[0]);
+  std::vector<Shard> sh(nranks);
+  int rc = GS_OK;
+  for (int i = 0; i < nranks && rc == GS_OK; ++i) {
+    Shard& s = sh[i];
+    s.rank = ranks[i];
+    shard_bounds(q->n, nranks, i, &s.lo, &s.hi);
+    if (local_index(c, s.rank) < 0) continue;
+    if ((rc = alloc_shard(c, s, lat)) != GS_OK) break;
+    cudaError_t e;
+    if (!q->init_host.empty())
+      e = cudaMemcpyAsync(s.z, q->init_host.data() + static_cast<size_t>(s.lo) * lat,
+                          static_cast<size_t>(s.hi - s.lo) * lat * 4, cudaMemcpyHostToDevice, strm(c));
+    else
+      e = rng_noise(s.z, s.lo, s.hi - s.lo, lat, q->noise_seed, strm(c));
+    if (e != cudaSuccess) rc = fail(c, GS_ECUDA, "initial latent: %s", cudaGetErrorString(e));
+  }
+  cudaError_t e = cudaStreamSynchronize(strm(c));
+  if (rc == GS_OK && e != cudaSuccess) rc = fail(c, GS_ECUDA, "initial latent: %s", cudaGetErrorString(e));
+  if (rc != GS_OK) {
+    free_shards(c, sh);
+    return rc;
+  }
+  q->init_host.clear();
+  q->init_host.shrink_to_fit();
+  q->shards = std::move(sh);
+  q->ranks.assign(ranks, ranks + nranks);
+  return GS_OK;
+}
+
+// NCCL mode: every process of the job submits every request (gs.h), so the id sequence agrees; a
+// min/max all-reduce of the new id over the world detects a process that skipped a submit.
+int check_job_wide_id(gs_ctx* c, gs_req id) {
+  if (c->emulated || c->world == 1) return GS_OK;
+  long long* h = c->h_id;
+  long long* d = c->d_id;
+  h[0] = static_cast<long long>(id);
+  h[1] = -static_cast<long long>(id);
+  CK(cudaMemcpyAsync(d, h, 16, cudaMemcpyHostToDevice, strm(c)));
+  NK(ncclAllReduce(d, d + 2, 2, ncclInt64, ncclMax, c->ctrl, strm(c)));
+  CK(cudaMemcpyAsync(h + 2, d + 2, 16, cudaMemcpyDeviceToHost, strm(c)));
+  CK(cudaStreamSynchronize(strm(c)));
+  if (h[2] != static_cast<long long>(id) || -h[3] != static_cast<long long>(id))
+    return fail(c, GS_ESTATE, "request id %llu differs across processes (ids %lld..%lld): every process must submit "
+                "every request", (unsigned long long)id, -h[3], h[2]);
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 static int submit_impl(gs_ctx* c, int model, int width, int height, int frames, int steps, uint64_t noise_seed,
                        const float* init_latent, const int* ranks, int nranks, bool text, uint64_t prompt_seed,
                        float cfg_scale, const void* prompt_embeds, gs_req* out) {
   if (!c || !out) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->run_mu);
+  std::lock_guard<std::mutex> g(c->api_mu);
   CK(cudaSetDevice(c->device));
   if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
   if (width <= 0 || height <= 0 || width % 16 || height % 16 || frames < 1 || (frames - 1) % 4 || steps < 1)
     return fail(c, GS_EINVAL, "bad request shape %dx%d frames %d steps %d", width, height, frames, steps);
-  RET(check_ranks(c, ranks, nranks));
+  const bool queued = ranks == nullptr && nranks == 0;
+  if (!queued) RET(check_ranks(c, ranks, nranks));
   Model& m = *c->models[model];
   if (text != (m.desc.cross_attn != 0))
     return fail(c, GS_EINVAL, text ? "gs_submit_text needs a cross-attention model"
@@ -1335,6 +1531,8 @@ static int submit_impl(gs_ctx* c, int model, int width, int height, int frames, 
     return fail(c, GS_EINVAL, "token grid exceeds RoPE table (%d)", m.p_max);
   q->n = q->grid[0] * q->grid[1] * q->grid[2];
   q->steps = steps;
+  q->noise_seed = noise_seed;
+  if (init_latent) q->init_host.assign(init_latent, init_latent + static_cast<size_t>(q->n) * m.desc.lat);
   if (text) {
     q->nb = cfg_scale > 0.f ? 2 : 1;
     q->cfg = cfg_scale > 0.f ? cfg_scale : 0.f;
@@ -1344,23 +1542,17 @@ static int submit_impl(gs_ctx* c, int model, int width, int height, int frames, 
       q->prompt_host.assign(static_cast<const uint16_t*>(prompt_embeds), static_cast<const uint16_t*>(prompt_embeds) + n);
     }
   }
-  q->ranks.assign(ranks, ranks + nranks);
-  q->shards.resize(nranks);
-  for (int i = 0; i < nranks; ++i) {
-    Shard& s = q->shards[i];
-    s.rank = ranks[i];
-    shard_bounds(q->n, nranks, i, &s.lo, &s.hi);
-    if (local_index(c, s.rank) < 0) continue;
-    RET(alloc_shard(c, s, m.desc.lat));
-    if (init_latent)
-      CK(cudaMemcpyAsync(s.z, init_latent + static_cast<size_t>(s.lo) * m.desc.lat,
-                         static_cast<size_t>(s.hi - s.lo) * m.desc.lat * 4, cudaMemcpyHostToDevice, c->stream));
-    else
-      CK(rng_noise(s.z, s.lo, s.hi - s.lo, m.desc.lat, noise_seed, c->stream));
+  {
+    std::lock_guard<std::mutex> g2(c->table_mu);
+    if (!queued) RET(check_idle(c, ranks, nranks, "gs_submit"));
+    q->id = c->next_req++;
   }
-  CK(cudaStreamSynchronize(c->stream));
+  RET(check_job_wide_id(c, q->id));
+  if (queued)
+    q->state = GS_REQ_QUEUED;
+  else
+    RET(place_shards(c, q.get(), ranks, nranks));
   std::lock_guard<std::mutex> g2(c->table_mu);
-  q->id = c->next_req++;
   *out = q->id;
   c->reqs[q->id] = std::move(q);
   return GS_OK;
@@ -1379,58 +1571,82 @@ int gs_submit_text(gs_ctx* c, int model, int width, int height, int frames, int 
                      prompt_seed, cfg_scale, prompt_embeds, out);
 }
 
-int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int nranks, int k, int* steps_run) {
-  if (!c || !ids) return GS_EINVAL;
-  if (steps_run) *steps_run = 0;
-  std::lock_guard<std::mutex> g(c->run_mu);
+int gs_place(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
+  if (!c) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->api_mu);
   CK(cudaSetDevice(c->device));
-  if (nreq < 1 || nreq > MAX_BATCH) return fail(c, GS_EINVAL, "batch of %d requests (1..%d)", nreq, MAX_BATCH);
   RET(check_ranks(c, ranks, nranks));
-  std::vector<Request*> reqs;
-  for (int r = 0; r < nreq; ++r) {
-    Request* q = find_req(c, ids[r]);
-    if (!q) return fail(c, GS_EINVAL, "unknown request %llu", (unsigned long long)ids[r]);
-    for (Request* o : reqs)
-      if (o == q) return fail(c, GS_EINVAL, "request listed twice");
-    if (q->state != GS_REQ_PLACED) return fail(c, GS_ESTATE, "request %llu is not runnable (state %d)", (unsigned long long)q->id, q->state);
-    if (!reqs.empty() && q->model != reqs[0]->model) return fail(c, GS_ESTATE, "batch mixes models");
-    if (static_cast<int>(q->ranks.size()) != nranks || !std::equal(q->ranks.begin(), q->ranks.end(), ranks))
-      return fail(c, GS_ESTATE, "request %llu is not placed on the given ranks", (unsigned long long)q->id);
-    if (k < 0 || q->step_idx + k > q->steps) return fail(c, GS_EINVAL, "k=%d exceeds remaining steps", k);
-    reqs.push_back(q);
+  Request* q = nullptr;
+  {
+    std::lock_guard<std::mutex> g2(c->table_mu);
+    auto it = c->reqs.find(id);
+    if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request");
+    q = it->second.get();
+    if (q->state != GS_REQ_QUEUED) return fail(c, GS_ESTATE, "gs_place needs a queued request (state %d)", q->state.load());
+    RET(check_idle(c, ranks, nranks, "gs_place"));
   }
+  RET(place_shards(c, q, ranks, nranks));
+  std::lock_guard<std::mutex> g2(c->table_mu);
+  q->state = GS_REQ_PLACED;
+  return GS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// The body of a run (worker thread of ticket t): rows of the batch on each local position, k steps
+// with the preemption check at every step boundary, latent back to the shards, states updated.
+void run_body(gs_ctx* c, Ticket* t, std::vector<Request*> reqs, int k) {
+  cudaSetDevice(c->device);
+  tl_err = &t->err;
+  const int* ranks = t->ranks.data();
+  const int nranks = static_cast<int>(t->ranks.size());
+  LaneGuard lane(c, ranks[0]);
   Model* m = c->models[reqs[0]->model].get();
   Plan P;
   make_plan(P, m, reqs, ranks, nranks);
   const std::vector<int> mine = local_positions(c, P);
+  int done = 0, rc = GS_OK;
   for (int i : mine) {
     RankArena& A = c->local[local_index(c, P.ranks[i])];
-    for (Request* q : reqs) RET(ensure_text_cache(c, m, q, local_index(c, P.ranks[i])));
-    RET(prepare_rank(c, P, i, A));
-    RET(move_latent(c, P, i, A, 0));
+    for (Request* q : reqs)
+      if (rc == GS_OK) rc = ensure_text_cache(c, m, q, local_index(c, P.ranks[i]));
+    if (rc == GS_OK) rc = prepare_rank(c, P, i, A);
+    if (rc == GS_OK) rc = move_latent(c, P, i, A, 0);
   }
-  RET(peer_setup(c, P));
-  for (Request* q : reqs) q->state = GS_REQ_RUNNING;
-  int done = 0, rc = GS_OK;
-  for (int s = 0; s < k; ++s) {
+  for (int s = 0; s < k && rc == GS_OK; ++s) {
     int flag = 0;
     for (Request* q : reqs) flag |= q->preempt.load();
     int stop = 0;
-    rc = agree_stop(c, P, flag, &stop);
+    unsigned gens[8] = {};
+    // the first step's agreement also carries the arena generations, so peer_setup can re-use the
+    // IPC mappings of an unchanged SP group without exchanging handles (arenas are sized above)
+    if (s == 0 && !c->emulated && P.p > 1 && c->a2a_mode == 1) {
+      void* bases[5] = {c->local[0].qr.p, c->local[0].kr.p, c->local[0].vr.p, c->local[0].orecv.p, c->flags};
+      if (memcmp(bases, c->exported, sizeof bases) != 0) {
+        memcpy(c->exported, bases, sizeof bases);
+        ++c->arena_gen;
+      }
+    }
+    rc = agree_stop(c, P, flag, &stop, s == 0 ? gens : nullptr);
+    if (rc == GS_OK && s == 0) rc = peer_setup(c, P, c->emulated || P.p == 1 ? nullptr : gens);
     if (rc != GS_OK || stop) break;
     cudaEvent_t s0 = nullptr, s1 = nullptr;
     if (c->prof_steps) {
+      std::lock_guard<std::mutex> g(c->prof_mu);
       s0 = get_event(c);
       s1 = get_event(c);
-      cudaEventRecord(s0, c->stream);
+      cudaEventRecord(s0, strm(c));
     }
     rc = run_one_step(c, P, mine);
-    if (c->prof_steps) cudaEventRecord(s1, c->stream);
+    if (c->prof_steps) cudaEventRecord(s1, strm(c));
     if (rc != GS_OK) break;
-    cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaError_t e = cudaStreamSynchronize(strm(c));
     if (c->prof_steps) {  // whole-step device time (gs_stats "step_ms"): the step-time CV of §8(d)
       float ms = 0;
       cudaEventElapsedTime(&ms, s0, s1);
+      std::lock_guard<std::mutex> g(c->prof_mu);
       c->step_ms.push_back(ms);
       c->event_pool.push_back(s0);
       c->event_pool.push_back(s1);
@@ -1447,18 +1663,109 @@ int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int n
     int r2 = move_latent(c, P, i, c->local[local_index(c, P.ranks[i])], 1);
     if (rc == GS_OK) rc = r2;
   }
-  cudaError_t e = cudaStreamSynchronize(c->stream);
+  cudaError_t e = cudaStreamSynchronize(strm(c));
   if (rc == GS_OK && e != cudaSuccess) rc = fail(c, GS_ECUDA, "%s", cudaGetErrorString(e));
+  std::lock_guard<std::mutex> g(c->table_mu);
   for (Request* q : reqs) {
-    if (q->preempt.load()) {
+    if (q->preempt.exchange(0))
       q->state = GS_REQ_PAUSED;
-      q->preempt.store(0);
-    } else {
+    else
       q->state = q->step_idx >= q->steps ? GS_REQ_DONE : GS_REQ_PLACED;
-    }
   }
-  if (steps_run) *steps_run = done;
-  return rc;
+  t->rc = rc;
+  t->steps_run = done;
+  t->finished.store(1);
+  tl_err = nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gs_run_steps_async(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int nranks, int k,
+                       gs_ticket* ticket) {
+  if (!c || !ids || !ticket) return GS_EINVAL;
+  *ticket = 0;
+  std::lock_guard<std::mutex> g(c->api_mu);
+  CK(cudaSetDevice(c->device));
+  if (nreq < 1 || nreq > MAX_BATCH) return fail(c, GS_EINVAL, "batch of %d requests (1..%d)", nreq, MAX_BATCH);
+  RET(check_ranks(c, ranks, nranks));
+  if (!c->emulated) {
+    bool member = false;
+    for (int i = 0; i < nranks; ++i) member |= ranks[i] == c->my_rank;
+    if (!member) return fail(c, GS_ESTATE, "this process (rank %d) owns none of the run's ranks", c->my_rank);
+  }
+  auto t = std::make_unique<Ticket>();
+  t->ranks.assign(ranks, ranks + nranks);
+  std::vector<Request*> reqs;
+  gs_ticket id;
+  {
+    // validation and the PLACED -> RUNNING transition are one critical section with gs_preempt
+    std::lock_guard<std::mutex> g2(c->table_mu);
+    for (int r = 0; r < nreq; ++r) {
+      auto it = c->reqs.find(ids[r]);
+      if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request %llu", (unsigned long long)ids[r]);
+      Request* q = it->second.get();
+      for (Request* o : reqs)
+        if (o == q) return fail(c, GS_EINVAL, "request listed twice");
+      if (q->state != GS_REQ_PLACED)
+        return fail(c, GS_ESTATE, "request %llu is not runnable (state %d)", (unsigned long long)q->id, q->state.load());
+      if (!reqs.empty() && q->model != reqs[0]->model) return fail(c, GS_ESTATE, "batch mixes models");
+      if (static_cast<int>(q->ranks.size()) != nranks || !std::equal(q->ranks.begin(), q->ranks.end(), ranks))
+        return fail(c, GS_ESTATE, "request %llu is not placed on the given ranks", (unsigned long long)q->id);
+      if (k < 0 || q->step_idx + k > q->steps) return fail(c, GS_EINVAL, "k=%d exceeds remaining steps", k);
+      reqs.push_back(q);
+    }
+    RET(check_idle(c, ranks, nranks, "gs_run_steps"));
+    id = c->next_ticket++;
+    for (int i = 0; i < nranks; ++i) c->busy[ranks[i]] = id;
+    for (Request* q : reqs) q->state = GS_REQ_RUNNING;
+  }
+  Ticket* tp = t.get();
+  {
+    std::lock_guard<std::mutex> g2(c->table_mu);
+    c->tickets[id] = std::move(t);
+  }
+  tp->th = std::thread(run_body, c, tp, reqs, k);
+  *ticket = id;
+  return GS_OK;
+}
+
+int gs_wait(gs_ctx* c, gs_ticket id, int* steps_run) {
+  if (!c) return GS_EINVAL;
+  if (steps_run) *steps_run = 0;
+  std::unique_ptr<Ticket> t;
+  {
+    std::lock_guard<std::mutex> g(c->table_mu);
+    auto it = c->tickets.find(id);
+    if (it == c->tickets.end()) return fail(c, GS_EINVAL, "unknown ticket %llu", (unsigned long long)id);
+    t = std::move(it->second);
+    c->tickets.erase(it);
+  }
+  if (t->th.joinable()) t->th.join();
+  {
+    std::lock_guard<std::mutex> g(c->table_mu);
+    for (int r : t->ranks)
+      if (c->busy[r] == id) c->busy[r] = 0;
+  }
+  if (steps_run) *steps_run = t->steps_run;
+  if (t->rc != GS_OK) return fail(c, t->rc, "%s", t->err.c_str());
+  return GS_OK;
+}
+
+int gs_ticket_done(gs_ctx* c, gs_ticket id) {
+  if (!c) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->table_mu);
+  auto it = c->tickets.find(id);
+  if (it == c->tickets.end()) return fail(c, GS_EINVAL, "unknown ticket %llu", (unsigned long long)id);
+  return it->second->finished.load() ? 1 : 0;
+}
+
+int gs_run_steps(gs_ctx* c, const gs_req* ids, int nreq, const int* ranks, int nranks, int k, int* steps_run) {
+  if (steps_run) *steps_run = 0;
+  gs_ticket t = 0;
+  RET(gs_run_steps_async(c, ids, nreq, ranks, nranks, k, &t));
+  return gs_wait(c, t, steps_run);
 }
 
 int gs_preempt(gs_ctx* c, gs_req id, int* steps_done_out) {
@@ -1468,9 +1775,11 @@ int gs_preempt(gs_ctx* c, gs_req id, int* steps_done_out) {
   if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request");
   Request* q = it->second.get();
   if (q->state == GS_REQ_DONE) return fail(c, GS_ESTATE, "request already finished");
+  // a run moves PLACED -> RUNNING and back under table_mu: the flag set here is seen by its next
+  // step-boundary check, or the request is paused before any run can claim it
   if (q->state == GS_REQ_RUNNING)
     q->preempt.store(1);
-  else
+  else if (q->state == GS_REQ_PLACED)
     q->state = GS_REQ_PAUSED;
   if (steps_done_out) *steps_done_out = q->step_idx;
   return GS_OK;
@@ -1478,19 +1787,36 @@ int gs_preempt(gs_ctx* c, gs_req id, int* steps_done_out) {
 
 int gs_resume(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
   if (!c) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->run_mu);
+  std::lock_guard<std::mutex> g(c->api_mu);
   CK(cudaSetDevice(c->device));
-  Request* q = find_req(c, id);
-  if (!q) return fail(c, GS_EINVAL, "unknown request");
-  if (q->state != GS_REQ_PAUSED && q->state != GS_REQ_PLACED)
-    return fail(c, GS_ESTATE, "resume needs a paused or placed request (state %d)", q->state);
   RET(check_ranks(c, ranks, nranks));
+  Request* q = nullptr;
+  {
+    std::lock_guard<std::mutex> g2(c->table_mu);
+    auto it = c->reqs.find(id);
+    if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request");
+    q = it->second.get();
+    if (q->state != GS_REQ_PAUSED && q->state != GS_REQ_PLACED)
+      return fail(c, GS_ESTATE, "resume needs a paused or placed request (state %d)", q->state.load());
+    RET(check_idle(c, ranks, nranks, "gs_resume (new ranks)"));
+    // NCCL mode: the re-shard is collective over the old ranks' processes too, and a process must not
+    // drive the communicator from two threads -> their ranks must be idle.  Emulated mode: reading
+    // the old shards is a device copy that does not disturb another run on those ranks.
+    if (!c->emulated) RET(check_idle(c, q->ranks.data(), static_cast<int>(q->ranks.size()), "gs_resume (old ranks)"));
+  }
+  LaneGuard lane(c, ranks[0]);
   const int lat = c->models[q->model]->desc.lat;
   std::vector<Shard> ns(nranks);
   for (int i = 0; i < nranks; ++i) {
     ns[i].rank = ranks[i];
     shard_bounds(q->n, nranks, i, &ns[i].lo, &ns[i].hi);
-    if (local_index(c, ns[i].rank) >= 0) RET(alloc_shard(c, ns[i], lat));
+    if (local_index(c, ns[i].rank) >= 0) {
+      int rc = alloc_shard(c, ns[i], lat);
+      if (rc != GS_OK) {
+        free_shards(c, ns);
+        return rc;
+      }
+    }
   }
   // interval intersections old x new: pure copies, planned on the host
   std::vector<int> old_ranks(q->ranks);
@@ -1507,7 +1833,12 @@ int gs_resume(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
     auto bufs = [&](int rank, int id) -> void* {
       return id == GS_BUF_OLD ? shard_of(q->shards, rank) : shard_of(ns, rank);
     };
-    RET(run_emulated(c, plans, bufs, 4));
+    const int rc = run_emulated(c, plans, bufs, 4);
+    if (rc != GS_OK) {
+      cudaStreamSynchronize(strm(c));
+      free_shards(c, ns);
+      return rc;
+    }
   } else {
     std::vector<gs_xfer> plan;
     plan_reshard(q->n, lat, old_ranks.data(), static_cast<int>(old_ranks.size()), ranks, nranks, c->my_rank, plan);
@@ -1519,18 +1850,19 @@ int gs_resume(gs_ctx* c, gs_req id, const int* ranks, int nranks) {
       NK(ncclGroupStart());
       for (const gs_xfer& x : plan) {
         if (x.op == GS_XFER_SEND)
-          NK(ncclSend(zo + x.src_off, x.width * 4, ncclUint8, x.peer, c->comm, c->stream));
+          NK(ncclSend(zo + x.src_off, x.width * 4, ncclUint8, x.peer, c->comm, strm(c)));
         else if (x.op == GS_XFER_RECV)
-          NK(ncclRecv(zn + x.dst_off, x.width * 4, ncclUint8, x.peer, c->comm, c->stream));
+          NK(ncclRecv(zn + x.dst_off, x.width * 4, ncclUint8, x.peer, c->comm, strm(c)));
       }
       NK(ncclGroupEnd());
     }
     for (const gs_xfer& x : plan)
       if (x.op == GS_XFER_COPY) RET(copy_block(c, zn + x.dst_off, zo + x.src_off, x, 4));
   }
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(strm(c)));
   free_shards(c, q->shards);
   free_text_cache(c, q);  // rebuilt on the new ranks at their first step
+  std::lock_guard<std::mutex> g2(c->table_mu);
   q->shards = ns;
   q->ranks.assign(ranks, ranks + nranks);
   q->state = q->step_idx >= q->steps ? GS_REQ_DONE : GS_REQ_PLACED;
@@ -1556,13 +1888,16 @@ int gs_query(gs_ctx* c, gs_req id, int* steps_done, int* steps_total, int* nrank
 
 int gs_read_latent(gs_ctx* c, gs_req id, float* host, size_t nfloats) {
   if (!c || !host) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->api_mu);
   Request* q = find_req(c, id);
   if (!q) return fail(c, GS_EINVAL, "unknown request");
   if (q->state == GS_REQ_RUNNING) return fail(c, GS_ESTATE, "request is running");
+  if (q->state == GS_REQ_QUEUED) return fail(c, GS_ESTATE, "request is queued (not placed)");
   const int lat = c->models[q->model]->desc.lat;
   if (nfloats != static_cast<size_t>(q->n) * lat) return fail(c, GS_EINVAL, "latent has %d x %d floats", q->n, lat);
   CK(cudaSetDevice(c->device));
-  CK(cudaStreamSynchronize(c->stream));
+  LaneGuard lane(c, q->ranks[0]);
+  CK(cudaStreamSynchronize(strm(c)));
   for (const Shard& s : q->shards)
     if (s.z && s.hi > s.lo)
       CK(cudaMemcpy(host + static_cast<size_t>(s.lo) * lat, s.z, static_cast<size_t>(s.hi - s.lo) * lat * 4,
@@ -1572,15 +1907,19 @@ int gs_read_latent(gs_ctx* c, gs_req id, float* host, size_t nfloats) {
 
 int gs_release(gs_ctx* c, gs_req id) {
   if (!c) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->table_mu);
-  auto it = c->reqs.find(id);
-  if (it == c->reqs.end()) return fail(c, GS_EINVAL, "unknown request");
-  if (it->second->state == GS_REQ_RUNNING) return fail(c, GS_ESTATE, "request is running");
+  std::lock_guard<std::mutex> g(c->api_mu);  // no run can claim the request meanwhile
+  Request* q = find_req(c, id);
+  if (!q) return fail(c, GS_EINVAL, "unknown request");
+  if (q->state == GS_REQ_RUNNING) return fail(c, GS_ESTATE, "request is running");
   cudaSetDevice(c->device);
-  cudaStreamSynchronize(c->stream);
-  free_shards(c, it->second->shards);
-  free_text_cache(c, it->second.get());
-  c->reqs.erase(it);
+  if (!q->ranks.empty()) {
+    LaneGuard lane(c, q->ranks[0]);
+    cudaStreamSynchronize(strm(c));
+  }
+  free_shards(c, q->shards);
+  free_text_cache(c, q);
+  std::lock_guard<std::mutex> g2(c->table_mu);
+  c->reqs.erase(id);
   return GS_OK;
 }
 
@@ -1588,6 +1927,7 @@ int gs_profile(gs_ctx* c, int enable, int reset) {
   if (!c) return GS_EINVAL;
   c->prof = enable == 1;
   c->prof_steps = enable == 1 || enable == 2;
+  std::lock_guard<std::mutex> g(c->prof_mu);
   if (reset) {
     c->prof_tab.clear();
     c->step_ms.clear();
@@ -1598,6 +1938,7 @@ int gs_profile(gs_ctx* c, int enable, int reset) {
 
 int gs_stats(gs_ctx* c, char* json, size_t len) {
   if (!c || !json || len == 0) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->prof_mu);
   std::string s = "{";
   for (auto& kv : c->prof_tab) {
     char buf[160];
@@ -1612,8 +1953,8 @@ int gs_stats(gs_ctx* c, char* json, size_t len) {
   }
   s += "], ";
   char buf[160];
-  snprintf(buf, sizeof buf, "\"a2a_peer\": %lld, \"a2a_plan\": %lld, \"launches\": %lld}", c->a2a_peer,
-           c->a2a_plan, c->launches);
+  snprintf(buf, sizeof buf, "\"a2a_peer\": %lld, \"a2a_plan\": %lld, \"launches\": %lld, \"ipc_exchanges\": %lld}",
+           c->a2a_peer.load(), c->a2a_plan.load(), c->launches.load(), c->ipc_exchanges);
   s += buf;
   if (s.size() + 1 > len) return fail(c, GS_EINVAL, "stats buffer too small (%zu)", s.size() + 1);
   memcpy(json, s.c_str(), s.size() + 1);
@@ -1623,7 +1964,7 @@ int gs_stats(gs_ctx* c, char* json, size_t len) {
 int gs_stream(gs_ctx* c, int rank, void** stream_out) {
   if (!c || !stream_out) return GS_EINVAL;
   if (local_index(c, rank) < 0) return fail(c, GS_EINVAL, "rank %d not owned by this process", rank);
-  *stream_out = c->stream;
+  *stream_out = c->lanes[local_index(c, rank)];
   return GS_OK;
 }
 
@@ -1634,7 +1975,7 @@ namespace {
 int order_after_legacy(gs_ctx* c) {
   if (!c->ev_order) CK(cudaEventCreateWithFlags(&c->ev_order, cudaEventDisableTiming));
   CK(cudaEventRecord(c->ev_order, cudaStreamLegacy));
-  CK(cudaStreamWaitEvent(c->stream, c->ev_order, 0));
+  CK(cudaStreamWaitEvent(strm(c), c->ev_order, 0));
   return GS_OK;
 }
 }  // namespace
@@ -1643,7 +1984,8 @@ int gs_debug_gemm(gs_ctx* c, int e, int M, int N, int K, const void* A, const vo
                   const float* gate_a, const float* gate_b, int gate_b_stride, const int* row_req,
                   const float* dsig_host) {
   if (!c) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->run_mu);
+  std::lock_guard<std::mutex> g(c->api_mu);
+  RET(no_runs_in_flight(c, "gs_debug_gemm"));
   CK(cudaSetDevice(c->device));
   RET(order_after_legacy(c));
   EpiParams ep{};
@@ -1656,27 +1998,29 @@ int gs_debug_gemm(gs_ctx* c, int e, int M, int N, int K, const void* A, const vo
   ep.row_req = row_req;
   if (dsig_host)
     for (int i = 0; i < 8; ++i) ep.dsig[i] = dsig_host[i];
-  cudaError_t err = gemm_bf16_tc(e, M, N, K, A, K, W, K, ep, c->num_sms, c->stream);
+  cudaError_t err = gemm_bf16_tc(e, M, N, K, A, K, W, K, ep, c->num_sms, strm(c));
   if (err != cudaSuccess) return fail(c, err == cudaErrorInvalidValue ? GS_EINVAL : GS_ECUDA, "gemm: %s", cudaGetErrorString(err));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(strm(c)));
   return GS_OK;
 }
 
 int gs_debug_attention(gs_ctx* c, const void* q, const void* k, const void* v, void* o, int heads, int d, int q_rs,
                        int kv_rs, int o_rs, const int* seq_off, const int* seq_len, int nreq) {
   if (!c || !seq_off || !seq_len) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->run_mu);
+  std::lock_guard<std::mutex> g(c->api_mu);
+  RET(no_runs_in_flight(c, "gs_debug_attention"));
   CK(cudaSetDevice(c->device));
   RET(order_after_legacy(c));
-  cudaError_t err = attention_tc(q, k, v, o, heads, d, q_rs, kv_rs, o_rs, seq_off, seq_len, nreq, c->num_sms, c->stream);
+  cudaError_t err = attention_tc(q, k, v, o, heads, d, q_rs, kv_rs, o_rs, seq_off, seq_len, nreq, c->num_sms, strm(c));
   if (err != cudaSuccess) return fail(c, err == cudaErrorInvalidValue ? GS_EINVAL : GS_ECUDA, "attention: %s", cudaGetErrorString(err));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(strm(c)));
   return GS_OK;
 }
 
 int gs_debug_time_embed(gs_ctx* c, int model, int nreq, const float* t, float* e0, float* e) {
   if (!c || !t || !e0 || !e) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->run_mu);
+  std::lock_guard<std::mutex> g(c->api_mu);
+  RET(no_runs_in_flight(c, "gs_debug_time_embed"));
   CK(cudaSetDevice(c->device));
   if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
   if (nreq < 1 || nreq > MAX_BATCH) return fail(c, GS_EINVAL, "nreq");
@@ -1687,17 +2031,18 @@ int gs_debug_time_embed(gs_ctx* c, int model, int nreq, const float* t, float* e
   RET(ensure(c, A.e, MAX_BATCH * 6 * D * 4));
   RET(ensure(c, A.temb, (MAX_BATCH * m->desc.freq_dim + 2 * MAX_BATCH * D) * 4));
   TimeEmbedW tw{m->w_t1, m->b_t1, m->w_t2, m->b_t2, m->w_tp, m->b_tp, D, m->desc.freq_dim};
-  CK(time_embed(tw, nreq, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), c->stream));
-  CK(cudaMemcpyAsync(e0, A.e0.p, static_cast<size_t>(nreq) * D * 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaMemcpyAsync(e, A.e.p, static_cast<size_t>(nreq) * 6 * D * 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(time_embed(tw, nreq, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), strm(c)));
+  CK(cudaMemcpyAsync(e0, A.e0.p, static_cast<size_t>(nreq) * D * 4, cudaMemcpyDeviceToHost, strm(c)));
+  CK(cudaMemcpyAsync(e, A.e.p, static_cast<size_t>(nreq) * 6 * D * 4, cudaMemcpyDeviceToHost, strm(c)));
+  CK(cudaStreamSynchronize(strm(c)));
   return GS_OK;
 }
 
 int gs_debug_block(gs_ctx* c, int model, int layer, float* x, int nreq, const int* grids, const int* tok_lo,
                    const int* n_rows, const float* t, const void* prompts) {
   if (!c || !x || !grids || !tok_lo || !n_rows || !t) return GS_EINVAL;
-  std::lock_guard<std::mutex> g(c->run_mu);
+  std::lock_guard<std::mutex> g(c->api_mu);
+  RET(no_runs_in_flight(c, "gs_debug_block"));
   CK(cudaSetDevice(c->device));
   if (model < 0 || model >= static_cast<int>(c->models.size())) return fail(c, GS_EINVAL, "bad model id");
   Model* m = c->models[model].get();
@@ -1731,19 +2076,19 @@ int gs_debug_block(gs_ctx* c, int model, int layer, float* x, int nreq, const in
     std::vector<int> rt(P.rows[0]);
     for (int r = 0; r < nreq; ++r)
       for (int i = 0; i < n_rows[r]; ++i) rt[P.loff[0][r] + i] = tok_lo[r] + i;
-    CK(cudaMemcpyAsync(A.row_tok.p, rt.data(), rt.size() * 4, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaMemcpyAsync(A.row_tok.p, rt.data(), rt.size() * 4, cudaMemcpyHostToDevice, strm(c)));
+    CK(cudaStreamSynchronize(strm(c)));
   }
   const int D = m->desc.dim;
   TimeEmbedW tw{m->w_t1, m->b_t1, m->w_t2, m->b_t2, m->w_tp, m->b_tp, D, m->desc.freq_dim};
-  CK(time_embed(tw, nreq, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), c->stream));
+  CK(time_embed(tw, nreq, t, A.temb.as<float>(), A.e0.as<float>(), A.e.as<float>(), strm(c)));
   const size_t xbytes = static_cast<size_t>(P.rows[0]) * D * 4;
-  CK(cudaMemcpyAsync(A.x.p, x, xbytes, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(A.x.p, x, xbytes, cudaMemcpyHostToDevice, strm(c)));
   RET(block_pre(c, P, 0, A, layer));
   RET(block_attn(c, P, 0, A));
   RET(block_post(c, P, 0, A, layer));
-  CK(cudaMemcpyAsync(x, A.x.p, xbytes, cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpyAsync(x, A.x.p, xbytes, cudaMemcpyDeviceToHost, strm(c)));
+  CK(cudaStreamSynchronize(strm(c)));
   for (auto& q : own) free_text_cache(c, q.get());
   prof_flush(c);
   return GS_OK;

@@ -141,6 +141,43 @@ cudaError_t peer_wait(const PeerFlags& f, cudaStream_t stream);
 // before any data-path kernel stores into peer memory.
 cudaError_t peer_wait_probe(const PeerFlags& f, int timeout_ms, int* ok, cudaStream_t stream);
 
+// ----------------------------------------------------------------- VAE decode (conv.cu, vae_kernels.cu)
+// Implicit-GEMM causal 3-D convolution (oracle/vae.py causal_conv3d): x bf16 [T][H][W][Cp]
+// channels-last, w bf16 [Coutp][kt][kh][kw][Cp], bias bf16 [Coutp], optional residual bf16
+// [T][H][W][Coutp] added in fp32.  Cp, Coutp multiples of 64.  Output modes:
+enum ConvOut : int {
+  CONV_OUT_BF16 = 0,             // out bf16 [T][H][W][out_cs], channels [0, Coutp)
+  CONV_OUT_TIME_INTERLEAVE = 1,  // temporal upsample: channels [0, out_real) -> frame 2t+1,
+                                 // [out_real, 2 out_real) -> frame 2t+2 (out bf16 [.][H][W][out_cs])
+  CONV_OUT_F32_CLAMP = 2,        // out fp32 [T][H][W][out_real] = clamp(acc + b, -1, 1), channels < out_real
+  CONV_OUT_F32 = 3,              // out fp32 [T][H][W][out_cs] (the decoder's fp32 residual stream)
+};
+struct ConvParams {
+  int T, H, W, Cp, kt, kh, kw, Coutp;
+  const __nv_bfloat16* bias;
+  const void* resid;   // bf16 or (resid_f32) fp32 [T][H][W][Coutp], or null
+  void* out;
+  int out_cs, mode, out_real;
+  int resid_f32;
+};
+cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream);
+// DiT latent [F*Ht*Wt, 64] fp32 (features (c, pt, ph, pw)) -> z bf16 [F][2Ht][2Wt][64]:
+// z = lat * std[c] + mean[c] for the 16 channels, channels 16..63 = 0 (reading V6).
+cudaError_t vae_unpatchify(const float* lat, int F, int Ht, int Wt, const float* mean, const float* stdv,
+                           __nv_bfloat16* z, cudaStream_t stream);
+// y = SiLU(x sqrt(C) / max(||x||, 1e-12) gamma) per voxel over the C real channels of Cp (pad -> 0);
+// x fp32 (the residual stream) or bf16 (x_bf16 != null).
+cudaError_t vae_rmsnorm_silu(const float* x, const __nv_bfloat16* x_bf16, long long nvox, int C, int Cp,
+                             const __nv_bfloat16* gamma, __nv_bfloat16* y, cudaStream_t stream);
+// Nearest x2 in H and W: y bf16 [T][2H][2W][Cp] from x fp32 (RNE) or x_bf16 [T][H][W][Cp].
+cudaError_t vae_upsample2(const float* x, const __nv_bfloat16* x_bf16, int T, int H, int W, int Cp,
+                          __nv_bfloat16* y, cudaStream_t stream);
+// y bf16 = RNE(x fp32), n elements (n % 4 == 0).
+cudaError_t vae_cast_bf16(const float* x, long long n, __nv_bfloat16* y, cudaStream_t stream);
+// Dense [Cout][taps][Cin] bf16 -> padded [Coutp][taps][Cp] (zeros elsewhere).
+cudaError_t vae_pad_weight(const __nv_bfloat16* src, int Cout, int taps, int Cin, int Coutp, int Cp,
+                           __nv_bfloat16* dst, cudaStream_t stream);
+
 // ----------------------------------------------------------------- RNG (rng.cu)
 // Counter RNG of DESIGN.md "Input recipe" (independent re-implementation of synth/rng.py).
 enum RngKind : int { RNG_BF16_SCALED = 0, RNG_BF16_GAIN = 1, RNG_F32_SCALED = 2 };

@@ -9,6 +9,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gs.h"
@@ -48,6 +49,35 @@ struct Model {
   std::vector<void*> allocs;
 };
 
+// VAE decoder (NEXT-4, csrc/vae.cpp): modules in the walk order of synth/vae.py (independently
+// re-built there); convolution weights padded to [Coutp][kt kh kw][Cp] bf16.
+struct VaeConv {
+  int cin = 0, cout = 0, kt = 1, kh = 1, kw = 1, cp = 0, coutp = 0;
+  __nv_bfloat16* w = nullptr;
+  __nv_bfloat16* b = nullptr;
+};
+struct VaeNorm {
+  int c = 0;
+  __nv_bfloat16* gamma = nullptr;
+};
+struct VaeRes {
+  VaeNorm n1, n2;
+  VaeConv c1, c2, skip;  // skip.cout == 0: identity shortcut
+};
+struct Vae {
+  gs_vae_desc desc{};
+  float* mean = nullptr;  // [z_dim] fp32
+  float* stdv = nullptr;
+  VaeConv post, conv_in, conv_out;
+  std::vector<VaeRes> mid;
+  std::vector<std::vector<VaeRes>> up;  // per stage
+  std::vector<VaeConv> tconv, sconv;    // per stage (tconv.cout == 0: no temporal upsample)
+  VaeNorm norm_out;
+  std::vector<void*> allocs;
+  DevBuf act[4];        // activation buffers (roles X, N, H, S), grow-only across decodes
+  DevBuf lat_stage, vid_stage;
+};
+
 struct Shard {
   int rank = -1;
   int lo = 0, hi = 0;  // token range
@@ -61,8 +91,13 @@ struct Request {
   int grid[3] = {1, 1, 1};
   int n = 0;
   int steps = 0;
-  int step_idx = 0;
-  int state = GS_REQ_PLACED;
+  // written by a run's worker thread, read by gs_query / gs_preempt on the caller's thread
+  std::atomic<int> step_idx{0};
+  std::atomic<int> state{GS_REQ_PLACED};
+  // a request submitted without placement (GS_REQ_QUEUED) keeps the recipe of its initial latent
+  // until gs_place: the noise seed, or the caller's latent copied at submit
+  uint64_t noise_seed = 0;
+  std::vector<float> init_host;
   std::vector<int> ranks;
   std::vector<Shard> shards;  // one per SP position
   std::atomic<int> preempt{0};
@@ -87,6 +122,22 @@ struct Prof {
   long long n = 0;
 };
 
+// An asynchronous run (gs_run_steps_async): its worker thread, result and GPU set.
+struct Ticket {
+  std::thread th;
+  int rc = GS_OK;
+  int steps_run = 0;
+  std::string err;
+  std::vector<int> ranks;
+  std::atomic<int> finished{0};
+};
+
+// The stream a thread launches the context's work on: a run's worker thread sets its lane (the
+// stream of the run's first rank); API calls use the lane of the ranks they act on, or lane 0.
+extern thread_local cudaStream_t tl_stream;
+// Error message sink of a worker thread (its ticket); nullptr = the context's message.
+extern thread_local std::string* tl_err;
+
 }  // namespace gs
 
 struct gs_ctx {
@@ -95,15 +146,25 @@ struct gs_ctx {
   int my_rank = 0;   // real mode
   bool emulated = false;
   int num_sms = 148;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;     // lane 0 (the caller thread's default)
+  std::vector<cudaStream_t> lanes;   // per local rank index: stream of runs led by that rank
   ncclComm_t comm = nullptr;
   std::vector<gs::RankArena> local;  // emulated: world entries; real: 1 entry
   std::vector<std::unique_ptr<gs::Model>> models;
+  std::vector<std::unique_ptr<gs::Vae>> vaes;
   std::map<gs_req, std::unique_ptr<gs::Request>> reqs;
   gs_req next_req = 1;
   std::string err;
-  std::mutex table_mu;  // guards reqs
-  std::mutex run_mu;    // one run / resume at a time
+  std::mutex api_mu;    // serialises the API calls that allocate or launch (not the runs' workers)
+  std::mutex table_mu;  // guards reqs, request states, tickets, busy
+  std::mutex err_mu;    // err
+  std::mutex pool_mu;   // pool
+  std::mutex prof_mu;   // prof_tab, prof_pending, event_pool, step_ms
+  // asynchronous runs: in-flight tickets and, per global rank, the ticket using it (0 = idle);
+  // runs on overlapping GPU sets are refused (Eq. capacity; Alg.1 "no GPU overlap")
+  std::map<gs_ticket, std::unique_ptr<gs::Ticket>> tickets;
+  gs_ticket next_ticket = 1;
+  std::vector<gs_ticket> busy;
   // measurement
   bool prof = false;        // per-kernel-class events (gs_profile enable = 1)
   bool prof_steps = false;  // per-step events (enable = 1 or 2)
@@ -111,15 +172,20 @@ struct gs_ctx {
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
   std::vector<cudaEvent_t> event_pool;
   std::vector<float> step_ms;       // device time of each profiled step (gs_stats "step_ms")
-  long long launches = 0;
+  std::atomic<long long> launches{0};
   cudaEvent_t ev_order = nullptr;   // debug entry points: order after the legacy stream
   // caching allocator for per-request state (latent shards, text caches): released blocks are
   // kept for reuse -- submit / release in a serving loop never reach cudaMalloc / cudaFree, whose
   // cost after an idle period was measured at 250-650 ms.  All users are ordered on `stream`.
   std::multimap<size_t, void*> pool;
   // pinned scratch for preemption agreement
-  int* h_flag = nullptr;
+  int* h_flag = nullptr;   // [64]: per-step agreement (flag, arena generation) and probe results
   int* d_flag = nullptr;
+  // NCCL mode: control-plane communicator (ncclCommSplit of comm) for the job-wide request-id check,
+  // so a gs_submit on the caller's thread never drives the communicator a run's worker uses
+  ncclComm_t ctrl = nullptr;
+  long long* h_id = nullptr;  // [4] scratch of the id check
+  long long* d_id = nullptr;
   // fused (peer-store) all-to-alls: mode 1 = peer stores wherever p divides the
   // heads (default), 0 = transfer plans (NCCL send / recv, emulated device copies)
   int a2a_mode = 1;
@@ -131,6 +197,16 @@ struct gs_ctx {
     void* p[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   };
   PeerMap peers[8];
+  // IPC mapping cache (NCCL mode): the exported buffers' generation (bumped whenever one of them is
+  // re-allocated), and per peer the generation its cached mappings belong to; a run whose SP group
+  // reports unchanged generations in the step-0 agreement re-uses the mappings without exchanging
+  // handles or probing
+  unsigned arena_gen = 1;
+  void* exported[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  unsigned peer_gen[8] = {};
+  std::vector<int> cached_group;  // ranks of the last verified peer-store group
+  bool cached_ok = false;
+  long long ipc_exchanges = 0;    // full handle exchanges (gs_stats)
   void* ipc_dev = nullptr;                                // device staging of the handle exchange
-  long long a2a_peer = 0, a2a_plan = 0;                   // exchanges run each way (gs_stats)
+  std::atomic<long long> a2a_peer{0}, a2a_plan{0};       // exchanges run each way (gs_stats)
 };

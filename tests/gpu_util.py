@@ -43,3 +43,54 @@ def to_dev(x, dtype):
 def randn_bf16(gen, shape, scale=1.0):
     """bf16 bit patterns of N(0, scale^2) samples."""
     return bf16_bits(gen.standard_normal(shape) * scale)
+
+
+class LazyBlocks:
+    """The L blocks' fp64 parameters generated one layer at a time while the oracle iterates them
+    (a 30-layer Wan-1.3B list is ~9 GB in fp64)."""
+
+    def __init__(self, shape):
+        self.shape = shape
+
+    def __len__(self):
+        return self.shape.layers
+
+    def __iter__(self):
+        from synth import models as sm
+        for layer in range(self.shape.layers):
+            yield sm.as_f64(sm.block_params(self.shape, layer))
+
+
+def _oracle_one_request(args):
+    from oracle import dit
+    from synth import models as sm
+    shape, z0, grid, step_idx, n_steps, k = args
+    glob = sm.as_f64(sm.global_params(shape))
+    return dit.dit_steps([z0], [grid], [step_idx], n_steps, k, glob, LazyBlocks(shape), shape.heads)[0]
+
+
+def oracle_steps_per_request(shape, z0s, grids, step_idx, n_steps, k):
+    """oracle dit_steps of a batch, one request per worker process.  Packing is an exact
+    re-arrangement of the method (tests/test_oracle_pins.py: the packed oracle equals each request
+    alone up to fp64 rounding, <= 1e-12 relative, at block and at step level), so this is the
+    batch's oracle result; the workers split the host's cores (numpy's element-wise softmax work
+    is single-threaded, BLAS is not)."""
+    import multiprocessing as mp
+    import os
+    n = len(z0s)
+    ncpu = len(os.sched_getaffinity(0))
+    per = str(max(1, ncpu // n))
+    saved = {v: os.environ.get(v) for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    for v in saved:
+        os.environ[v] = per
+    try:
+        with mp.get_context("spawn").Pool(n) as pool:
+            return pool.map(_oracle_one_request,
+                            [(shape, np.asarray(z, np.float64), g, i, n_steps, k)
+                             for z, g, i in zip(z0s, grids, step_idx)])
+    finally:
+        for v, val in saved.items():
+            if val is None:
+                os.environ.pop(v, None)
+            else:
+                os.environ[v] = val

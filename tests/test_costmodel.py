@@ -32,3 +32,17 @@ def test_block_split_matches_step_model():
     assert L * costmodel.flops_per_block([N], D, F) == costmodel.paper_flops_per_step(L, N, D, F)
     # varlen: attention term is sum n^2 (block diagonal), GEMM term is linear in N
     assert costmodel.attn_flops_per_block([3, 4], 8) == 4 * 8 * (9 + 16)
+
+
+def test_vae_decode_flops_matches_oracle_walk():
+    """bench.py's VAE work count (costmodel, product side) equals the oracle's count of the convs
+    it executes (oracle/vae.py decode_flops, pinned in tests/test_vae_pins.py) -- two independent
+    walks of the decoder."""
+    from oracle import vae as ov
+    from paper_2604_04335_b200 import costmodel
+    from synth import vae as sv
+    for shape in (sv.WAN_VAE, sv.TINY_VAE):
+        for grid in [(21, 45, 80), (1, 64, 64), (3, 2, 3)]:
+            assert costmodel.vae_decode_flops(grid, shape.dims, shape.blocks, shape.mid_blocks,
+                                              shape.temporal_up, shape.z_dim, shape.out_ch) == \
+                ov.decode_flops(grid, shape, sv.vae_modules)

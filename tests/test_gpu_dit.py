@@ -10,7 +10,7 @@ import pytest
 from oracle import dit
 from synth import models as sm
 from synth import rng
-from tests.gpu_util import max_row_rel_l2, rel_l2
+from tests.gpu_util import max_row_rel_l2, oracle_steps_per_request, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -139,11 +139,8 @@ def test_step_config2_wan13b_full_depth(gs):
     assert ctx.run_steps(reqs, [0], 1) == 1
     z1 = [ctx.read_latent(r) for r in reqs]
     ctx.close()
-    glob = sm.as_f64(sm.global_params(shape))
-    blocks = [sm.as_f64(sm.block_params(shape, l)) for l in range(shape.layers)]
     grids = [sm.token_grid(1024, 1024)] * 4
-    ref = dit.dit_steps([z.astype(np.float64) for z in z0], grids, [0, 2, 0, 7], 50, 1, glob, blocks,
-                        shape.heads)
+    ref = oracle_steps_per_request(shape, z0, grids, [0, 2, 0, 7], 50, 1)
     for i, (a, b, r) in enumerate(zip(z0, z1, ref)):
         err = rel_l2(b.astype(np.float64) - a, r - a)
         worst = max_row_rel_l2(b.astype(np.float64) - a, r - a)
@@ -244,6 +241,90 @@ def test_preempt_from_another_thread_stops_at_step_boundary(gs):
     zr = ctx.read_latent(ref)
     ctx.close()
     assert np.array_equal(z.view(np.uint32), zr.view(np.uint32))
+
+
+def test_async_runs_on_disjoint_sets_concurrent_and_bit_exact(gs):
+    """gs_run_steps_async: two SP groups ({0,1} and {2,3,4,5}) in flight together from one thread
+    give the same bytes as serial runs; a run on a set overlapping an in-flight run is refused
+    (GS_ESTATE: Eq. capacity, Alg.1 "no GPU overlap" P:498)."""
+    shape = sm.WAN_1_3B.with_layers(2)
+    w, h, f = 416, 240, 5
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    mid = _mk(ctx, shape)
+    a = ctx.submit(mid, w, h, f, 50, 1000, [0, 1])
+    b = ctx.submit(mid, w, h, f, 50, 1001, [2, 3, 4, 5])
+    c = ctx.submit(mid, 256, 256, 1, 50, 1002, [1])
+    ta = ctx.run_steps_async([a], [0, 1], 3)
+    tb = ctx.run_steps_async([b], [2, 3, 4, 5], 3)
+    with pytest.raises(gs.GsError) as ei:
+        ctx.run_steps_async([c], [1], 1)             # rank 1 belongs to ticket ta
+    assert ei.value.code == gs.GS_ESTATE
+    with pytest.raises(gs.GsError):
+        ctx.resume(c, [5])                            # new rank 5 belongs to ticket tb
+    assert ctx.wait(tb) == 3 and ctx.wait(ta) == 3
+    with pytest.raises(gs.GsError):
+        ctx.wait(ta)                                  # a ticket is waited for once
+    za, zb = ctx.read_latent(a), ctx.read_latent(b)
+    refs = []
+    for seed in (1000, 1001):
+        r = ctx.submit(mid, w, h, f, 50, seed, [0])
+        assert ctx.run_steps([r], [0], 3) == 3
+        refs.append(ctx.read_latent(r))
+    ctx.close()
+    assert np.array_equal(za.view(np.uint32), refs[0].view(np.uint32))
+    assert np.array_equal(zb.view(np.uint32), refs[1].view(np.uint32))
+
+
+def test_queued_submit_then_place(gs):
+    """A request submitted without placement holds no GPU (state QUEUED, |X_r| = 0) until
+    gs_place; placed on GPU 3 it steps exactly like a request submitted straight onto GPU 0."""
+    shape = sm.TINY.with_layers(2)
+    ctx = gs.Context(device=0, world_size=4, emulated=True)
+    mid = _mk(ctx, shape)
+    g = np.random.default_rng(4)
+    z0 = g.standard_normal((256, 64)).astype(np.float32)
+    q = ctx.submit(mid, 256, 256, 1, 50, 1000, None, init_latent=z0)
+    assert ctx.query(q)["state"] == gs.REQ_QUEUED and ctx.query(q)["ranks"] == []
+    with pytest.raises(gs.GsError):
+        ctx.read_latent(q)
+    with pytest.raises(gs.GsError):
+        ctx.run_steps([q], [3], 1)
+    ctx.place(q, [3])
+    with pytest.raises(gs.GsError):
+        ctx.place(q, [2])                             # already placed
+    np.testing.assert_array_equal(ctx.read_latent(q), z0)
+    assert ctx.run_steps([q], [3], 2) == 2
+    d = ctx.submit(mid, 256, 256, 1, 50, 1000, [0], init_latent=z0)
+    assert ctx.run_steps([d], [0], 2) == 2
+    zq, zd = ctx.read_latent(q), ctx.read_latent(d)
+    # noise-seeded queued request == noise-seeded direct request
+    s1 = ctx.submit(mid, 256, 256, 1, 50, 77, None)
+    ctx.place(s1, [2])
+    s2 = ctx.submit(mid, 256, 256, 1, 50, 77, [1])
+    n1, n2 = ctx.read_latent(s1), ctx.read_latent(s2)
+    ctx.close()
+    assert np.array_equal(zq.view(np.uint32), zd.view(np.uint32))
+    assert np.array_equal(n1.view(np.uint32), n2.view(np.uint32))
+    with pytest.raises(ValueError):
+        gs.Context.__new__(gs.Context)._latent_arg(np.zeros(10), 256, 256, 1)
+
+
+def test_preempt_async_run_from_same_thread(gs):
+    """Preempting a request whose run is in flight (started with gs_run_steps_async) takes effect
+    at the next step boundary; the steps run are reported by gs_wait and progress is kept."""
+    shape = sm.TINY.with_layers(12)
+    ctx = gs.Context(device=0)
+    mid = _mk(ctx, shape)
+    req = ctx.submit(mid, 512, 512, 1, 1000, 1000, [0])
+    t = ctx.run_steps_async([req], [0], 900)
+    import time
+    time.sleep(0.3)
+    assert not ctx.ticket_done(t)
+    ctx.preempt(req)
+    n = ctx.wait(t)
+    q = ctx.query(req)
+    ctx.close()
+    assert 0 < n < 900 and q["steps_done"] == n and q["state"] == gs.REQ_PAUSED
 
 
 def test_contract_errors(gs):

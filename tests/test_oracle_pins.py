@@ -277,6 +277,20 @@ def test_block_varlen_packing_equals_alone():
         np.testing.assert_allclose(packed[off:off + n], alone, atol=1e-13)
 
 
+def test_steps_varlen_packing_equals_alone():
+    """A batch's step == each request stepped alone (different step indices; the basis of
+    tests/gpu_util.oracle_steps_per_request)."""
+    shape = sm.TINY.with_layers(2)
+    glob = sm.as_f64(sm.global_params(shape))
+    blocks = [sm.as_f64(sm.block_params(shape, l)) for l in range(shape.layers)]
+    grids = [(1, 2, 3), (2, 2, 2)]
+    zs = [RNG.standard_normal((int(np.prod(g)), shape.lat)) for g in grids]
+    packed = dit.dit_steps(zs, grids, [0, 7], 50, 2, glob, blocks, shape.heads)
+    for z, g, i, p in zip(zs, grids, [0, 7], packed):
+        alone = dit.dit_steps([z], [g], [i], 50, 2, glob, blocks, shape.heads)[0]
+        np.testing.assert_allclose(p, alone, rtol=0, atol=1e-12 * np.abs(alone).max())
+
+
 def test_block_rows_sampled_equals_full():
     shape, blk = _tiny_block()
     grid = (2, 3, 5)

@@ -13,7 +13,10 @@ KEYS = ['gpu__time_duration.sum', 'sm__cycles_elapsed.avg.per_second', 'dram__by
         'sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active',
         'sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active',
         'smsp__issue_active.avg.pct_of_peak_sustained_active', 'smsp__inst_executed.sum',
-        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']
+        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed',
+        'lts__throughput.avg.pct_of_peak_sustained_elapsed', 'lts__t_bytes.sum',
+        'l1tex__throughput.avg.pct_of_peak_sustained_active',
+        'sm__memory_throughput.avg.pct_of_peak_sustained_elapsed']
 STALL = 'smsp__average_warps_issue_stalled_'
 
 
