@@ -433,12 +433,18 @@ def run_gpu(args, rank, world, local_rank):
 
     dist = None
     if world > 1:
+        # NCCL's INIT lines (stderr) show each rank's communicator and nranks for the driver's log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         uid = [gs.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         ctx = gs.Context(device=local_rank, world_size=world, rank=rank, nccl_uid=uid[0])
+        inf = ctx.info()
+        print(f"[bench] rank {rank}/{world}: gs context on cuda:{local_rank}, NCCL world {inf['world_size']}, "
+              f"{inf['num_sms']} SMs", file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(local_rank)
         ctx = gs.Context(device=local_rank)

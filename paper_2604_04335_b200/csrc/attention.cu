@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 //   10, 11 idle (setmaxnreg acts on whole warpgroups).
 // Development variant (built with -DGS_ATTN_ALT=1; 12% slower than v5 at the c4 SP=8 shape in round 2).
 constexpr int THREADS7 = 384;
-constexpr int kProducerWarp7 = 8, kMmaWarp7 = 9;
+constexpr int kProducerWarp7 = 8, kMmaWarp7 = 9, kSIssueWarp7 = 10;
 struct Cfg7 {
   static constexpr int HD = 128;
   static constexpr int TILE_BYTES = 128 * HD * 2;   // this CTA's Q tile
@@ -510,7 +510,7 @@ struct Cfg7 {
   static constexpr int K_OFF = TILE_BYTES;
   static constexpr int V_OFF = K_OFF + KST * KT_BYTES;
   static constexpr int BAR_OFF = V_OFF + VST * VT_BYTES;
-  static constexpr int XCH_OFF = BAR_OFF + 256;              // float [2 sets][128 rows] running max
+  static constexpr int XCH_OFF = BAR_OFF + 512;              // float [2 sets][128 rows] running max
   static constexpr int FIN_OFF = XCH_OFF + 2 * 128 * 4;      // float [2 sets][2 (l, m)][128 rows]
   static constexpr int SMEM = FIN_OFF + 2 * 2 * 128 * 4 + 1024;
   static constexpr uint32_t T_O = 0, T_S = 128;
@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(THREADS7, 1)
   uint64_t* sfull = vempty + C::VST;    // [3] S_j in buffer j % 3
   uint64_t* pfull = sfull + 3;          // [3] P_j in buffer j % 3 (leader: 8 warp arrivals)
   uint64_t* pvdone = pfull + 3;         // [3] PV_j completed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pvdone + 3);
+  uint64_t* pvis = pvdone + 3;          // [3] PV_j issued (PV issuer -> S issuer, leader CTA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pvis + 3);
   float* xch = reinterpret_cast<float*>(smem + C::XCH_OFF);
   float* fin = reinterpret_cast<float*>(smem + C::FIN_OFF);
 
@@ -567,6 +568,7 @@ __global__ void __launch_bounds__(THREADS7, 1)
       mbar_init(&sfull[u], 1);
       mbar_init(&pfull[u], 8);
       mbar_init(&pvdone[u], 1);
+      mbar_init(&pvis[u], 1);
     }
     fence_barrier_init();
   }
@@ -607,13 +609,17 @@ __global__ void __launch_bounds__(THREADS7, 1)
         tma_load_3d_2sm(&tmV, &vfull[vs], smem + C::V_OFF + vs * C::VT_BYTES, 64 * rank, head, kv_off + j * 128);
       }
     }
-  } else if (warp == kMmaWarp7) {
-    if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16(256, 128, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16(256, HD, 0, 1);
-      const uint64_t qdesc0 = sdesc_sw128(smem_u32(smem + C::Q_OFF), 16, 1024);
-      const uint64_t kdesc0 = sdesc_sw128(smem_u32(smem + C::K_OFF), 16, 1024);
-      const uint64_t vdesc0 = sdesc_sw128(smem_u32(smem + C::V_OFF), 16384, 1024);
+  } else if ((warp == kMmaWarp7 || warp == kSIssueWarp7) && rank == 0 && lane == 0) {
+    // Two issuers in the leader CTA, on different SMSPs: warp 9 issues the PV MMAs, warp 10 the S MMAs,
+    // so neither's barrier polls (~200 cycles each under MUFU load) leave the tensor core idle.  S_{j+3}
+    // overwrites the buffer PV_j reads: the S issuer waits for "PV_j issued" (pvis, with the tcgen05
+    // thread-sync fences), after which the in-order tensor core runs PV_j before S_{j+3}.
+    constexpr uint32_t idesc_s = idesc_bf16(256, 128, 0, 0);
+    constexpr uint32_t idesc_o = idesc_bf16(256, HD, 0, 1);
+    const uint64_t qdesc0 = sdesc_sw128(smem_u32(smem + C::Q_OFF), 16, 1024);
+    const uint64_t kdesc0 = sdesc_sw128(smem_u32(smem + C::K_OFF), 16, 1024);
+    const uint64_t vdesc0 = sdesc_sw128(smem_u32(smem + C::V_OFF), 16384, 1024);
+    if (warp == kSIssueWarp7) {
       auto issue_s = [&](int j) {  // S_j = Q K_j^T -> buffer j % 3; K slot and S_j signalled
         mbar_wait_spin(&kfull[j % C::KST], (j / C::KST) & 1);
         tc_fence_after();
@@ -631,6 +637,12 @@ __global__ void __launch_bounds__(THREADS7, 1)
       };
       mbar_wait(q_full, 0);
       for (int j = 0; j < 3 && j < nkv; ++j) issue_s(j);
+      for (int j = 0; j + 3 < nkv; ++j) {
+        mbar_wait_spin(&pvis[j % 3], (j / 3) & 1);  // PV_j is in the tensor core's queue
+        tc_fence_after();
+        issue_s(j + 3);
+      }
+    } else {
       for (int j = 0; j < nkv; ++j) {
         const int u = j % 3;
         mbar_wait_spin(&vfull[j % C::VST], (j / C::VST) & 1);
@@ -646,8 +658,8 @@ __global__ void __launch_bounds__(THREADS7, 1)
           mma_ts_2sm(tmem + C::T_O, pa + kk * 8, vb + ((kk * 2048) >> 4), idesc_o, (j > 0) || (kk > 0));
         mma_commit_2sm_mc(&pvdone[u], 0x3);
         mma_commit_2sm_mc(&vempty[j % C::VST], 0x3);
-        // buffer u is free once PV_j has read P_j: the tensor core runs the MMAs in issue order
-        if (j + 3 < nkv) issue_s(j + 3);
+        tc_fence_before();
+        mbar_arrive(&pvis[u]);
       }
     }
   }

@@ -62,6 +62,39 @@ __device__ __forceinline__ float row_sum(float v, float* red) {
   }
   return block_sum<TPR / 32>(v, red);
 }
+// Two row sums at once (q and k of the qk kernel): the same per-value order as two row_sum calls
+// (identical bits), one exchange instead of two -- the kernel is bound by these latency chains.
+template <int TPR>
+__device__ __forceinline__ float2 row_sum2(float a, float b, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (TPR == 32) return make_float2(a, b);
+  const int w = threadIdx.x >> 5;
+  if (TPR == 64) {
+    const int slot = w >> 1;
+    named_bar_sync(1 + slot, 64);  // the partner has read the previous exchange
+    if ((threadIdx.x & 31) == 0) {
+      red[4 * slot + (w & 1)] = a;
+      red[4 * slot + 2 + (w & 1)] = b;
+    }
+    named_bar_sync(1 + slot, 64);
+    return make_float2(red[4 * slot] + red[4 * slot + 1], red[4 * slot + 2] + red[4 * slot + 3]);
+  }
+  constexpr int NW = TPR / 32;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) {
+    red[w] = a;
+    red[NW + w] = b;
+  }
+  __syncthreads();
+  if (NW == 4)
+    return make_float2((red[0] + red[1]) + (red[2] + red[3]), (red[4] + red[5]) + (red[6] + red[7]));
+  return make_float2(((red[0] + red[1]) + (red[2] + red[3])) + ((red[4] + red[5]) + (red[6] + red[7])),
+                     ((red[8] + red[9]) + (red[10] + red[11])) + ((red[12] + red[13]) + (red[14] + red[15])));
+}
 constexpr int kWarpRowMaxD = 2048;
 constexpr int kWarpRowsPerCta = 8;
 
@@ -254,8 +287,9 @@ __device__ __forceinline__ void qk_finish(const QkTables& tb, const uint4* src, 
                                           __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out,
                                           float* red) {
   const int nv = D >> 3;
-  const float rq = rsqrtf(row_sum<TPR>(sq, red) / D + eps);
-  const float rk = rsqrtf(row_sum<TPR>(sk, red) / D + eps);
+  const float2 ssum = row_sum2<TPR>(sq, sk, red);
+  const float rq = rsqrtf(ssum.x / D + eps);
+  const float rk = rsqrtf(ssum.y / D + eps);
 
   const int r = rp.row_req[row];
   const int tok = rp.row_tok[row];
@@ -321,7 +355,7 @@ __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
                              float eps, const RopeParams rp, const PackParams pk,
                              __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
                              __nv_bfloat16* __restrict__ v_out) {
-  __shared__ float red[16];
+  __shared__ float red[32];  // row_sum2: 4 per row slot (TPR = 64, 8 slots) or 2 x 8 warps
   __shared__ QkTables tb;
   pdl_wait();
   pdl_launch_dependents();

@@ -128,3 +128,38 @@ def test_vae_decode_request_equals_decode_of_latent(gs):
     ctx.close()
     assert a.shape == (9, 48, 64, 3)
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.slow
+def test_vae_decode_fullsize_720p_sampled_windows(gs, ctx):
+    """Config 4's latent at full size (DiT grid 21 x 45 x 80 -> 81 x 720 x 1280 x 3, the bench's
+    launch configuration) against the oracle on sampled windows.  The decoder is causal in time and
+    its spatial receptive field is ~17 latent pixels (conv taps summed over the walk), so the oracle
+    decode of a crop -- latent frames 0..1, +-10 tokens around a sample token, clipped at the true
+    borders (where the crop's zero padding IS the conv padding) -- equals the full decode on the sample
+    token's 16 x 16 output pixels of output frames 0..4 (translation equivariance, pinned in
+    tests/test_vae_pins.py)."""
+    import torch
+    shape = sv.WAN_VAE
+    grid = (21, 45, 80)
+    vid = ctx.vae_create(shape.z_dim, shape.dims, shape.blocks, shape.mid_blocks, shape.temporal_up,
+                         shape.out_ch, shape.weight_seed)
+    g = np.random.default_rng(8)
+    lat = g.standard_normal((int(np.prod(grid)), 64)).astype(np.float32)
+    out = torch.empty(ctx.vae_out_shape(grid), device="cuda", dtype=torch.float32)
+    ctx.vae_decode(vid, torch.from_numpy(lat).cuda(), grid, out=out)
+    video = out[:5].cpu().numpy().astype(np.float64)            # output frames of latent frames 0, 1
+    params = sv.vae_params(shape)
+    lat4 = lat.reshape(grid[0], grid[1], grid[2], 64)
+    R = 10
+    for th, tw in [(22, 40), (0, 0), (44, 79), (3, 77)]:
+        h0, h1 = max(0, th - R), min(grid[1], th + R + 1)
+        w0, w1 = max(0, tw - R), min(grid[2], tw + R + 1)
+        crop = lat4[:2, h0:h1, w0:w1].reshape(-1, 64).astype(np.float64)
+        ref = ov.decode(crop, (2, h1 - h0, w1 - w0), params, shape)   # [5, 16 (h1-h0), 16 (w1-w0), 3]
+        oh, ow = 16 * (th - h0), 16 * (tw - w0)
+        got = video[:, 16 * th:16 * th + 16, 16 * tw:16 * tw + 16]
+        want = ref[:, oh:oh + 16, ow:ow + 16]
+        err = rel_l2(got, want)
+        print(f"720p window at token ({th}, {tw}): rel-L2 {err:.3e}")
+        assert err < TOL, (th, tw, err)
