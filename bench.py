@@ -644,6 +644,8 @@ def run_gpu(args, rank, world, local_rank):
         "kernels": kernels,
         "step_ms_each": [round(x, 3) for x in step_ms],
         "step_cv": round(float(np.std(step_ms) / np.mean(step_ms)), 5) if len(step_ms) > 1 else None,
+        "step_cv_context": "paper Tab. 1 (P:170-173, SURVEY §8(c) P7): per-step latency CV <= 0.04% on its GPUs; "
+                           "ours includes the power-capped clock wander of this box (clocks.reasons)",
         "gpu_launches": int(launches),
         "e2e": {"value": round(e2e_v, 3), "unit": "ms", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": lat_bytes, "steps": e2e_steps,

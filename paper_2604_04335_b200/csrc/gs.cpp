@@ -715,10 +715,11 @@ int peer_setup(gs_ctx* c, Plan& P, const unsigned* gens = nullptr) {
       wt.val[wt.n++] = c->probe_seen[gj] + 1;
     }
     CK(peer_signal(sig, strm(c)));
-    CK(peer_wait_probe(wt, 2000, c->d_flag + 12, strm(c)));
-    CK(cudaMemcpyAsync(c->h_flag + 12, c->d_flag + 12, 4, cudaMemcpyDeviceToHost, strm(c)));
+    // probe result in word 40 (words 0-17 carry the per-step agreement)
+    CK(peer_wait_probe(wt, 2000, c->d_flag + 40, strm(c)));
+    CK(cudaMemcpyAsync(c->h_flag + 40, c->d_flag + 40, 4, cudaMemcpyDeviceToHost, strm(c)));
     CK(cudaStreamSynchronize(strm(c)));
-    ok = c->h_flag[12];
+    ok = c->h_flag[40];
     if (ok)
       for (int j = 0; j < P.p; ++j)
         if (j != me) ++c->probe_seen[P.ranks[j]];
