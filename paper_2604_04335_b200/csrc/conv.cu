@@ -34,20 +34,37 @@ namespace gs {
 
 namespace {
 constexpr int CBM = 128;                 // voxels per CTA (pair: 256)
-constexpr int CBK = 64;                  // channels per K block
 constexpr int PATCH_W = 32, PATCH_H = 4;  // CTA patch (pair: 8 rows)
-constexpr int CA_BYTES = CBM * CBK * 2;  // 16 KB
 constexpr int CTHREADS = 192;
 
-template <int BN>
+// KB = channels per K block: 64 (rows of 128 B, 128-byte swizzle) or 32 (rows of 64 B, 64-byte
+// swizzle) for channel counts = 32 mod 64 (the 96-channel last stage runs unpadded).
+template <int BN, int KB>
 struct CCfg {
-  static constexpr int B_BYTES = (BN / 2) * CBK * 2;
-  static constexpr int STAGE_BYTES = CA_BYTES + B_BYTES;
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 8 ? 8 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int A_BYTES = CBM * KB * 2;
+  static constexpr int B_BYTES = (BN / 2) * KB * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int MAXST = KB == 64 ? 8 : 16;
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > MAXST ? MAXST : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
-  static constexpr uint32_t TMEM_COLS = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                      : 2 * BN <= 256 ? 256 : 512;
   static_assert(SMEM_BYTES <= 232448, "shared memory");
+  static_assert(A_BYTES % 1024 == 0 && STAGE_BYTES % 1024 == 0, "swizzle atoms stay 1024-aligned");
 };
+
+// Shared-memory descriptor of a K-major operand with KB-channel rows (128B or 64B swizzle).
+template <int KB>
+__device__ __forceinline__ uint64_t sdesc_kb(uint32_t saddr) {
+  if (KB == 64) return sdesc_sw128(saddr, 16, 1024);
+  uint64_t d = 0;  // 64-byte swizzle (layout type 4): 8-row core groups of 512 B
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(512 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;
+  return d;
+}
 
 __device__ __forceinline__ void tma_load_4d_2sm(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
                                                 int c2, int c3) {
@@ -70,11 +87,12 @@ struct TileGeom {
   }
 };
 
-template <int BN>
+template <int BN, int KB>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
     conv3d_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ ConvParams cp) {
-  using C = CCfg<BN>;
+  using C = CCfg<BN, KB>;
+  constexpr int CA_BYTES = C::A_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
@@ -93,7 +111,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
   g.num_m = cp.T * g.num_hb * g.num_wb;
   g.num_n = cp.Coutp / BN;
   const int num_tiles = g.num_m * g.num_n;
-  const int cpb = cp.Cp / CBK;
+  const int cpb = cp.Cp / KB;
   const int num_k = cp.kt * cp.kh * cp.kw * cpb;
 
   if (threadIdx.x == 0) {
@@ -133,8 +151,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&full[stage]), 0), C::STAGE_BYTES);
-          tma_load_4d_2sm(&tmA, &full[stage], sa, cb * CBK, w0 + dw - pw, h0 + dh - ph, t + dt - (cp.kt - 1));
-          tma_load_2d_2sm(&tmB, &full[stage], sa + CA_BYTES, kb * CBK, nb * BN + static_cast<int>(rank) * (BN / 2));
+          tma_load_4d_2sm(&tmA, &full[stage], sa, cb * KB, w0 + dw - pw, h0 + dh - ph, t + dt - (cp.kt - 1));
+          tma_load_2d_2sm(&tmB, &full[stage], sa + CA_BYTES, kb * KB, nb * BN + static_cast<int>(rank) * (BN / 2));
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           if (++cb == cpb) {  // K order: tap-major (dt, dh, dw), channel block minor
             cb = 0;
@@ -163,8 +181,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + CA_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < CBK / 16; ++kk)
-            mma_ss_2sm(d_tmem, sdesc_sw128(sa + kk * 32, 16, 1024), sdesc_sw128(sb + kk * 32, 16, 1024), idesc,
+          for (int kk = 0; kk < KB / 16; ++kk)
+            mma_ss_2sm(d_tmem, sdesc_kb<KB>(sa + kk * 32), sdesc_kb<KB>(sb + kk * 32), idesc,
                        (kb | kk) != 0);
           mma_commit_2sm_mc(&empty[stage], 0x3);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -271,7 +289,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
   }
 }
 
-bool make_tma_4d_act(CUtensorMap* m, const void* base, int Cp, int W, int H, int T) {
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -280,28 +298,47 @@ bool make_tma_4d_act(CUtensorMap* m, const void* base, int Cp, int W, int H, int
       return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
+  return enc;
+}
+
+bool make_tma_4d_act(CUtensorMap* m, const void* base, int Cp, int W, int H, int T, int kb) {
+  auto enc = tma_encoder();
   if (!enc) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(Cp), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                         static_cast<cuuint64_t>(T)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(Cp) * 2, static_cast<cuuint64_t>(W) * Cp * 2,
                            static_cast<cuuint64_t>(H) * W * Cp * 2};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(CBK), PATCH_W, PATCH_H, 1};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(kb), PATCH_W, PATCH_H, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Weights [Coutp][K] bf16 with box {kb, rows}; 128B swizzle for kb = 64, 64B for kb = 32.
+bool make_tma_w(CUtensorMap* m, const void* base, long long K, int Coutp, int kb, int rows) {
+  if (kb == 64) return make_tma_2d_bf16(m, base, K, Coutp, K * 2, 64, rows);
+  auto enc = tma_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(Coutp)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(rows)};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int KB>
 cudaError_t launch_conv(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
-  using C = CCfg<BN>;
+  using C = CCfg<BN, KB>;
   CUtensorMap ta, tb;
-  if (!make_tma_4d_act(&ta, x, cp.Cp, cp.W, cp.H, cp.T)) return cudaErrorInvalidValue;
+  if (!make_tma_4d_act(&ta, x, cp.Cp, cp.W, cp.H, cp.T, KB)) return cudaErrorInvalidValue;
   const long long K = static_cast<long long>(cp.kt) * cp.kh * cp.kw * cp.Cp;
-  if (!make_tma_2d_bf16(&tb, w, K, cp.Coutp, K * 2, CBK, BN / 2)) return cudaErrorInvalidValue;
+  if (!make_tma_w(&tb, w, K, cp.Coutp, KB, BN / 2)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -318,7 +355,7 @@ cudaError_t launch_conv(const void* x, const void* w, const ConvParams& cp, int 
   at.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, conv3d_tc_kernel<BN>, ta, tb, cp);
+  return cudaLaunchKernelEx(&cfg, conv3d_tc_kernel<BN, KB>, ta, tb, cp);
 }
 }  // namespace
 
@@ -326,23 +363,34 @@ int conv_bn(int Coutp) {
   if (Coutp % 256 == 0) return 256;
   if (Coutp % 192 == 0) return 192;
   if (Coutp % 128 == 0) return 128;
-  return 64;
+  if (Coutp % 96 == 0) return 96;
+  if (Coutp % 64 == 0) return 64;
+  return 32;
+}
+
+template <int KB>
+cudaError_t launch_kb(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
+  switch (conv_bn(cp.Coutp)) {
+    case 256: return launch_conv<256, KB>(x, w, cp, num_sms, stream);
+    case 192: return launch_conv<192, KB>(x, w, cp, num_sms, stream);
+    case 128: return launch_conv<128, KB>(x, w, cp, num_sms, stream);
+    case 96: return launch_conv<96, KB>(x, w, cp, num_sms, stream);
+    case 64: return launch_conv<64, KB>(x, w, cp, num_sms, stream);
+    default: return launch_conv<32, KB>(x, w, cp, num_sms, stream);
+  }
 }
 
 cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
   if (cp.T <= 0 || cp.H <= 0 || cp.W <= 0) return cudaSuccess;
-  if (cp.Cp % CBK || cp.Coutp % 64 || cp.kt < 1 || cp.kh < 1 || cp.kw < 1 || !cp.bias || !cp.out)
+  if (cp.Cp % 32 || cp.Coutp % 32 || cp.kt < 1 || cp.kh < 1 || cp.kw < 1 || !cp.bias || !cp.out)
     return cudaErrorInvalidValue;
   if ((cp.mode == CONV_OUT_BF16 || cp.mode == CONV_OUT_F32) && (cp.out_cs % 8 || cp.out_cs < cp.Coutp))
     return cudaErrorInvalidValue;
   if (cp.mode == CONV_OUT_TIME_INTERLEAVE && (cp.out_real % 32 || 2 * cp.out_real > cp.Coutp || cp.out_cs % 8))
     return cudaErrorInvalidValue;
-  switch (conv_bn(cp.Coutp)) {
-    case 256: return launch_conv<256>(x, w, cp, num_sms, stream);
-    case 192: return launch_conv<192>(x, w, cp, num_sms, stream);
-    case 128: return launch_conv<128>(x, w, cp, num_sms, stream);
-    default: return launch_conv<64>(x, w, cp, num_sms, stream);
-  }
+  // 64-channel K blocks (128B swizzle) when the input channels allow, else 32 (64B swizzle)
+  return cp.Cp % 64 == 0 ? launch_kb<64>(x, w, cp, num_sms, stream) : launch_kb<32>(x, w, cp, num_sms, stream);
+
 }
 
 }  // namespace gs

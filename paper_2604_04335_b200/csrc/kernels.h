@@ -143,8 +143,8 @@ cudaError_t peer_wait_probe(const PeerFlags& f, int timeout_ms, int* ok, cudaStr
 
 // ----------------------------------------------------------------- VAE decode (conv.cu, vae_kernels.cu)
 // Implicit-GEMM causal 3-D convolution (oracle/vae.py causal_conv3d): x bf16 [T][H][W][Cp]
-// channels-last, w bf16 [Coutp][kt][kh][kw][Cp], bias bf16 [Coutp], optional residual bf16
-// [T][H][W][Coutp] added in fp32.  Cp, Coutp multiples of 64.  Output modes:
+// channels-last, w bf16 [Coutp][kt][kh][kw][Cp], bias bf16 [Coutp], optional residual bf16 or fp32
+// [T][H][W][Coutp] added in fp32.  Cp, Coutp multiples of 32.  Output modes:
 enum ConvOut : int {
   CONV_OUT_BF16 = 0,             // out bf16 [T][H][W][out_cs], channels [0, Coutp)
   CONV_OUT_TIME_INTERLEAVE = 1,  // temporal upsample: channels [0, out_real) -> frame 2t+1,
@@ -161,10 +161,10 @@ struct ConvParams {
   int resid_f32;
 };
 cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream);
-// DiT latent [F*Ht*Wt, 64] fp32 (features (c, pt, ph, pw)) -> z bf16 [F][2Ht][2Wt][64]:
-// z = lat * std[c] + mean[c] for the 16 channels, channels 16..63 = 0 (reading V6).
+// DiT latent [F*Ht*Wt, 64] fp32 (features (c, pt, ph, pw)) -> z bf16 [F][2Ht][2Wt][zc] (zc = 32 or 64):
+// z = lat * std[c] + mean[c] for the 16 channels, channels 16..zc-1 = 0 (reading V6).
 cudaError_t vae_unpatchify(const float* lat, int F, int Ht, int Wt, const float* mean, const float* stdv,
-                           __nv_bfloat16* z, cudaStream_t stream);
+                           __nv_bfloat16* z, int zc, cudaStream_t stream);
 // y = SiLU(x sqrt(C) / max(||x||, 1e-12) gamma) per voxel over the C real channels of Cp (pad -> 0);
 // x fp32 (the residual stream) or bf16 (x_bf16 != null).
 cudaError_t vae_rmsnorm_silu(const float* x, const __nv_bfloat16* x_bf16, long long nvox, int C, int Cp,

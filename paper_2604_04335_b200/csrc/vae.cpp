@@ -9,7 +9,7 @@
 //   RMS norm + SiLU -> conv_out 3x3x3 -> clamp.
 // Every convolution is conv3d_tc (tcgen05 implicit GEMM, conv.cu); norms, upsampling and the
 // unpatchify are the HBM-bound kernels of vae_kernels.cu.  Activations bf16 channels-last with
-// channels padded to multiples of 64 (pad channels are zero; padded weight rows / columns are zero).
+// channels padded to multiples of 32 (pad channels are zero; padded weight rows / columns are zero).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -51,7 +51,8 @@ int vfail(gs_ctx* c, int code, const char* fmt, ...) {
     if (rc_ != GS_OK) return rc_; \
   } while (0)
 
-inline int pad64(int c) { return (c + 63) / 64 * 64; }
+// channels padded to a multiple of 32 (the conv's K blocks are 64 or 32 channels wide)
+inline int padc(int c) { return (c + 31) / 32 * 32; }
 
 int vlocal(gs_ctx* c, int rank) {
   if (c->emulated) return (rank >= 0 && rank < c->world) ? rank : -1;
@@ -78,8 +79,8 @@ struct Gen {
     cv.kt = kt;
     cv.kh = kh;
     cv.kw = kw;
-    cv.cp = pad64(cin);
-    cv.coutp = pad64(cout);
+    cv.cp = padc(cin);
+    cv.coutp = padc(cout);
     const int taps = kt * kh * kw;
     const long long dense = static_cast<long long>(cout) * taps * cin;
     const uint32_t tid = 200 + 4 * module++;
@@ -202,10 +203,10 @@ struct Decoder {
   int run(const float* lat_dev, int F, int Ht, int Wt, float* video_dev) {
     int T = F, H = 2 * Ht, W = 2 * Wt;
     size_t vox = static_cast<size_t>(T) * H * W;
-    bf16* z = role<bf16>(2, vox * 64);
-    if (!dry) VRET(ck(vae_unpatchify(lat_dev, F, Ht, Wt, v->mean, v->stdv, z, s), "unpatchify"));
+    bf16* z = role<bf16>(2, vox * v->post.cp);
+    if (!dry) VRET(ck(vae_unpatchify(lat_dev, F, Ht, Wt, v->mean, v->stdv, z, v->post.cp, s), "unpatchify"));
     bf16* N = role<bf16>(1, vox * v->post.coutp);
-    VRET(conv(v->post, z, T, H, W, 64, N, CONV_OUT_BF16));
+    VRET(conv(v->post, z, T, H, W, v->post.cp, N, CONV_OUT_BF16));
     VRET(conv(v->conv_in, N, T, H, W, v->post.coutp, role<float>(0, vox * v->conv_in.coutp), CONV_OUT_F32));
     int C = v->conv_in.cout, cp = v->conv_in.coutp;
     for (const VaeRes& r : v->mid) VRET(res(r, T, H, W, C, cp));

@@ -15,7 +15,7 @@ namespace {
 // output voxel writes its 64 padded channels (8 x 16 B).
 __global__ void vae_unpatchify_kernel(const float* __restrict__ lat, int F, int Ht, int Wt,
                                       const float* __restrict__ mean, const float* __restrict__ stdv,
-                                      __nv_bfloat16* __restrict__ z) {
+                                      __nv_bfloat16* __restrict__ z, int zc) {
   const long long nvox = static_cast<long long>(F) * 2 * Ht * 2 * Wt;
   const long long v = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (v >= nvox) return;
@@ -31,9 +31,8 @@ __global__ void vae_unpatchify_kernel(const float* __restrict__ lat, int F, int 
                             __ldg(src + (c + 1) * 4 + sub) * __ldg(stdv + c + 1) + __ldg(mean + c + 1));
 #pragma unroll
   for (int i = 8; i < 32; ++i) pk[i] = 0u;
-  uint4* dst = reinterpret_cast<uint4*>(z + v * 64);
-#pragma unroll
-  for (int q = 0; q < 8; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+  uint4* dst = reinterpret_cast<uint4*>(z + v * zc);
+  for (int q = 0; q < zc / 8; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
 }
 
 // One warp per voxel: lane l holds channels [8 l, 8 l + 8) of each 256-channel slice (Cp <= 512);
@@ -145,10 +144,11 @@ inline unsigned blocks(long long n, int t) { return static_cast<unsigned>((n + t
 }  // namespace
 
 cudaError_t vae_unpatchify(const float* lat, int F, int Ht, int Wt, const float* mean, const float* stdv,
-                           __nv_bfloat16* z, cudaStream_t stream) {
+                           __nv_bfloat16* z, int zc, cudaStream_t stream) {
   const long long nvox = static_cast<long long>(F) * 4 * Ht * Wt;
   if (nvox == 0) return cudaSuccess;
-  vae_unpatchify_kernel<<<blocks(nvox, 256), 256, 0, stream>>>(lat, F, Ht, Wt, mean, stdv, z);
+  if (zc != 32 && zc != 64) return cudaErrorInvalidValue;
+  vae_unpatchify_kernel<<<blocks(nvox, 256), 256, 0, stream>>>(lat, F, Ht, Wt, mean, stdv, z, zc);
   return cudaGetLastError();
 }
 

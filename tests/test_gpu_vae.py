@@ -34,7 +34,9 @@ def _bf16(g, shape, scale=1.0):
 
 @pytest.mark.parametrize("k", [(3, 3, 3), (3, 1, 1), (1, 3, 3), (1, 1, 1)])
 @pytest.mark.parametrize("T,H,W,C,Co", [(3, 10, 37, 64, 64), (2, 9, 33, 128, 192), (4, 8, 32, 64, 384),
-                                        (1, 5, 70, 128, 256), (2, 17, 31, 192, 128)])
+                                        (1, 5, 70, 128, 256), (2, 17, 31, 192, 128),
+                                        # 32-channel K blocks (64B swizzle) and narrow N tiles
+                                        (2, 9, 40, 96, 96), (1, 6, 33, 32, 32), (2, 8, 35, 96, 192)])
 def test_conv3d_matches_oracle(ctx, T, H, W, C, Co, k):
     import torch
     g = np.random.default_rng(T * 1000 + H * 10 + W + C)
