@@ -37,20 +37,24 @@ constexpr int CBM = 128;                 // voxels per CTA (pair: 256)
 constexpr int PATCH_W = 32, PATCH_H = 4;  // CTA patch (pair: 8 rows)
 constexpr int CTHREADS = 192;
 
-// KB = channels per K block: 64 (rows of 128 B, 128-byte swizzle) or 32 (rows of 64 B, 64-byte
-// swizzle) for channel counts = 32 mod 64 (the 96-channel last stage runs unpadded).
-template <int BN, int KB>
+// KB = channels per TMA box / swizzle atom row: 64 (rows of 128 B, 128-byte swizzle) or 32 (rows of
+// 64 B, 64-byte swizzle) for channel counts = 32 mod 64 (the 96-channel last stage runs unpadded).
+// NS boxes per pipeline stage (a 96-channel tap = 3 x 32 in one stage, so each barrier round trip
+// still feeds 6 MMAs).
+template <int BN, int KB, int NS>
 struct CCfg {
-  static constexpr int A_BYTES = CBM * KB * 2;
-  static constexpr int B_BYTES = (BN / 2) * KB * 2;
+  static constexpr int A_SUB = CBM * KB * 2;
+  static constexpr int B_SUB = (BN / 2) * KB * 2;
+  static constexpr int A_BYTES = NS * A_SUB;
+  static constexpr int B_BYTES = NS * B_SUB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int MAXST = KB == 64 ? 8 : 16;
+  static constexpr int MAXST = 8;
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > MAXST ? MAXST : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
   static constexpr uint32_t TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
                                       : 2 * BN <= 256 ? 256 : 512;
   static_assert(SMEM_BYTES <= 232448, "shared memory");
-  static_assert(A_BYTES % 1024 == 0 && STAGE_BYTES % 1024 == 0, "swizzle atoms stay 1024-aligned");
+  static_assert(A_SUB % 1024 == 0 && B_SUB % 512 == 0 && STAGE_BYTES % 1024 == 0, "swizzle atom alignment");
 };
 
 // Shared-memory descriptor of a K-major operand with KB-channel rows (128B or 64B swizzle).
@@ -87,11 +91,11 @@ struct TileGeom {
   }
 };
 
-template <int BN, int KB>
+template <int BN, int KB, int NS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
     conv3d_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ ConvParams cp) {
-  using C = CCfg<BN, KB>;
+  using C = CCfg<BN, KB, NS>;
   constexpr int CA_BYTES = C::A_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -111,7 +115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
   g.num_m = cp.T * g.num_hb * g.num_wb;
   g.num_n = cp.Coutp / BN;
   const int num_tiles = g.num_m * g.num_n;
-  const int cpb = cp.Cp / KB;
+  const int cpb = cp.Cp / (KB * NS);  // channel stage-blocks per tap
   const int num_k = cp.kt * cp.kh * cp.kw * cpb;
 
   if (threadIdx.x == 0) {
@@ -151,8 +155,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&full[stage]), 0), C::STAGE_BYTES);
-          tma_load_4d_2sm(&tmA, &full[stage], sa, cb * KB, w0 + dw - pw, h0 + dh - ph, t + dt - (cp.kt - 1));
-          tma_load_2d_2sm(&tmB, &full[stage], sa + CA_BYTES, kb * KB, nb * BN + static_cast<int>(rank) * (BN / 2));
+#pragma unroll
+          for (int sub = 0; sub < NS; ++sub) {
+            tma_load_4d_2sm(&tmA, &full[stage], sa + sub * C::A_SUB, (cb * NS + sub) * KB, w0 + dw - pw,
+                            h0 + dh - ph, t + dt - (cp.kt - 1));
+            tma_load_2d_2sm(&tmB, &full[stage], sa + CA_BYTES + sub * C::B_SUB, (kb * NS + sub) * KB,
+                            nb * BN + static_cast<int>(rank) * (BN / 2));
+          }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           if (++cb == cpb) {  // K order: tap-major (dt, dh, dw), channel block minor
             cb = 0;
@@ -181,9 +190,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + CA_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < KB / 16; ++kk)
-            mma_ss_2sm(d_tmem, sdesc_kb<KB>(sa + kk * 32), sdesc_kb<KB>(sb + kk * 32), idesc,
-                       (kb | kk) != 0);
+          for (int q = 0; q < NS * (KB / 16); ++q) {
+            const int sub = q / (KB / 16), kk = q % (KB / 16);
+            mma_ss_2sm(d_tmem, sdesc_kb<KB>(sa + sub * C::A_SUB + kk * 32), sdesc_kb<KB>(sb + sub * C::B_SUB + kk * 32),
+                       idesc, (kb | q) != 0);
+          }
           mma_commit_2sm_mc(&empty[stage], 0x3);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -329,16 +340,16 @@ bool make_tma_w(CUtensorMap* m, const void* base, long long K, int Coutp, int kb
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int KB>
+template <int BN, int KB, int NS>
 cudaError_t launch_conv(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
-  using C = CCfg<BN, KB>;
+  using C = CCfg<BN, KB, NS>;
   CUtensorMap ta, tb;
   if (!make_tma_4d_act(&ta, x, cp.Cp, cp.W, cp.H, cp.T, KB)) return cudaErrorInvalidValue;
   const long long K = static_cast<long long>(cp.kt) * cp.kh * cp.kw * cp.Cp;
   if (!make_tma_w(&tb, w, K, cp.Coutp, KB, BN / 2)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel<BN, KB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -355,7 +366,7 @@ cudaError_t launch_conv(const void* x, const void* w, const ConvParams& cp, int 
   at.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, conv3d_tc_kernel<BN, KB>, ta, tb, cp);
+  return cudaLaunchKernelEx(&cfg, conv3d_tc_kernel<BN, KB, NS>, ta, tb, cp);
 }
 }  // namespace
 
@@ -368,15 +379,15 @@ int conv_bn(int Coutp) {
   return 32;
 }
 
-template <int KB>
+template <int KB, int NS>
 cudaError_t launch_kb(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
   switch (conv_bn(cp.Coutp)) {
-    case 256: return launch_conv<256, KB>(x, w, cp, num_sms, stream);
-    case 192: return launch_conv<192, KB>(x, w, cp, num_sms, stream);
-    case 128: return launch_conv<128, KB>(x, w, cp, num_sms, stream);
-    case 96: return launch_conv<96, KB>(x, w, cp, num_sms, stream);
-    case 64: return launch_conv<64, KB>(x, w, cp, num_sms, stream);
-    default: return launch_conv<32, KB>(x, w, cp, num_sms, stream);
+    case 256: return launch_conv<256, KB, NS>(x, w, cp, num_sms, stream);
+    case 192: return launch_conv<192, KB, NS>(x, w, cp, num_sms, stream);
+    case 128: return launch_conv<128, KB, NS>(x, w, cp, num_sms, stream);
+    case 96: return launch_conv<96, KB, NS>(x, w, cp, num_sms, stream);
+    case 64: return launch_conv<64, KB, NS>(x, w, cp, num_sms, stream);
+    default: return launch_conv<32, KB, NS>(x, w, cp, num_sms, stream);
   }
 }
 
@@ -389,7 +400,9 @@ cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int nu
   if (cp.mode == CONV_OUT_TIME_INTERLEAVE && (cp.out_real % 32 || 2 * cp.out_real > cp.Coutp || cp.out_cs % 8))
     return cudaErrorInvalidValue;
   // 64-channel K blocks (128B swizzle) when the input channels allow, else 32 (64B swizzle)
-  return cp.Cp % 64 == 0 ? launch_kb<64>(x, w, cp, num_sms, stream) : launch_kb<32>(x, w, cp, num_sms, stream);
+  if (cp.Cp % 64 == 0) return launch_kb<64, 1>(x, w, cp, num_sms, stream);
+  if (cp.Cp % 96 == 0) return launch_kb<32, 3>(x, w, cp, num_sms, stream);  // 96-channel taps in one stage
+  return launch_kb<32, 1>(x, w, cp, num_sms, stream);
 
 }
 

@@ -32,9 +32,9 @@ print(f"decode 720p/81f: {ms:.1f} ms, {fl / ms / 1e9:.1f} TFLOP/s algorithmic")
 ctx.close()
 # per-shape conv timing (T, H, W, Cp, k, Coutp): the decoder's dominant layer shapes
 ctx = gs.Context(device=0)
-shapes = [("stage3 3x3x3 128->128 (96 real)", 81, 720, 1280, 128, (3, 3, 3), 128),
+shapes = [("stage3 3x3x3 96->96", 81, 720, 1280, 96, (3, 3, 3), 96),
           ("stage2 3x3x3 192->192", 81, 360, 640, 192, (3, 3, 3), 192),
-          ("stage2 sconv 1x3x3 192->128 (96)", 81, 720, 1280, 192, (1, 3, 3), 128),
+          ("stage2 sconv 1x3x3 192->96", 81, 720, 1280, 192, (1, 3, 3), 96),
           ("stage1 3x3x3 384->384", 41, 180, 320, 384, (3, 3, 3), 384),
           ("stage0 3x3x3 384->384", 21, 90, 160, 384, (3, 3, 3), 384)]
 for name, T, H, W, C, k, Co in shapes:
@@ -51,7 +51,7 @@ for name, T, H, W, C, k, Co in shapes:
     torch.cuda.synchronize()
     cms = (time.perf_counter() - a) * 1e3
     f = 2 * T * H * W * C * Co * k[0] * k[1] * k[2]
-    print(f"conv {name:36s} {cms:8.2f} ms {f / cms / 1e9:8.1f} TFLOP/s (padded channels)")
+    print(f"conv {name:36s} {cms:8.2f} ms {f / cms / 1e9:8.1f} TFLOP/s")
     del x, w, b, o
     torch.cuda.empty_cache()
 ctx.close()
