@@ -159,6 +159,9 @@ def cpu_model():
     return None
 
 
+_ORACLE_BLOCK = {}
+
+
 def oracle_sample(workload, rows=32):
     """Time the fp64 oracle (oracle/dit.py, as it stands) on SURVEY.md §8(d)'s bounded sample of the
     workload: the row-sampled block of §8(c) "Large configs" on the workload's FULL token grid --
@@ -171,7 +174,9 @@ def oracle_sample(workload, rows=32):
     w, h, f = reqs[0]
     grid = sm.token_grid(w, h, f)
     n = grid[0] * grid[1] * grid[2]
-    blk = sm.as_f64(sm.block_params(shape, 0))
+    if _ORACLE_BLOCK.get(shape.name) is None:  # generated once per process (not timed)
+        _ORACLE_BLOCK[shape.name] = sm.as_f64(sm.block_params(shape, 0))
+    blk = _ORACLE_BLOCK[shape.name]
     g = np.random.default_rng(5)
     x = g.standard_normal((n, shape.dim))
     e = g.uniform(-0.5, 0.5, (6, shape.dim))
