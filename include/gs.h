@@ -98,7 +98,9 @@ const char* gs_last_error(gs_ctx* ctx);
  * N % 192 == 0 and the narrower tiles fill a small grid's last wave better), 192 or 256 forced
  * (process-wide; both give identical bits).  "pdl": 1 (default) launches the step's kernels with
  * programmatic dependent launch (each kernel's setup overlaps the previous kernel's drain), 0 plain
- * stream order (process-wide; identical bits).  GS_EINVAL for an unknown key or value. */
+ * stream order (process-wide; identical bits).  "usp_ring": 1 (default) Ulysses only; 2, 4 or 8 = the USP hybrid's ring
+ * degree for batches whose p it divides with p / ring dividing the heads (gs_plan_a2a_usp; identical
+ * bits; every process of an SP group must use the same value).  GS_EINVAL for an unknown key or value. */
 int gs_set_option(gs_ctx* ctx, const char* key, long long value);
 /* Number of SMs of the context's device, world size, ranks owned by this process. */
 int gs_info(gs_ctx* ctx, int* num_sms, int* world_size, int* nlocal);
@@ -277,6 +279,13 @@ typedef struct {
  * too small or an argument is out of range. */
 int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
                 gs_xfer* out, int max_out, int* n_out, long long* stage_elems);
+/* The same for the USP hybrid (NEXT-2; xFuser's Unified Sequence Parallelism, §5): p = u x ring,
+ * every head cut into `ring` query chunks, unit (head h, chunk ci) on position (h / (H/u)) * ring + ci;
+ * each unit receives its query chunk and the head's K / V of every token in token order (the ring's
+ * K / V exchange as an in-order all-gather), so results are bit-exact with plain Ulysses.  Falls back
+ * to gs_plan_a2a's partition when ring does not divide p or p / ring does not divide heads. */
+int gs_plan_a2a_usp(int kind, int p, int ring, int me, int nreq, const int* n_tokens, int heads, int head_dim,
+                    gs_xfer* out, int max_out, int* n_out, long long* stage_elems);
 /* Peer-store addressing of the fused all-to-alls (p divides heads; DESIGN.md §8 "fused exchange"):
  * the QKV pack kernel of SP position `me` stores local row m of request r as full-batch row
  * m + row_delta[r] of the RECV buffer of the position owning each head, and its attention kernel

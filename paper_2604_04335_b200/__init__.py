@@ -88,6 +88,8 @@ _SIG = {
     "gs_debug_attention_ctatime": [_P, ctypes.c_size_t],
     "gs_plan_a2a": [_I, _I, _I, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP,
                     ctypes.POINTER(ctypes.c_longlong)],
+    "gs_plan_a2a_usp": [_I, _I, _I, _I, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP,
+                        ctypes.POINTER(ctypes.c_longlong)],
     "gs_plan_reshard": [_I, _I, _IP, _I, _IP, _I, _I, ctypes.POINTER(Xfer), _I, _IP],
     "gs_plan_peer": [_I, _I, _I, _IP, _I, _I, ctypes.POINTER(ctypes.c_longlong), _IP,
                      ctypes.POINTER(ctypes.c_longlong)],
@@ -157,13 +159,14 @@ def _xfers(call):
     return [{f: getattr(arr[i], f) for f, _t in Xfer._fields_} for i in range(n.value)]
 
 
-def plan_a2a(kind, p, me, n_tokens, heads, head_dim):
-    """Host-only Ulysses exchange plan of SP position `me` (kind 0: Q/K/V seq->head, 1: O
-    head->seq).  Returns (list of transfer dicts, staging elements)."""
+def plan_a2a(kind, p, me, n_tokens, heads, head_dim, ring=1):
+    """Host-only Ulysses exchange plan of SP position `me` (kind 0: K/V seq->head, 2: Q, 1: O
+    head->seq); ring > 1 = the USP hybrid's partition (gs_plan_a2a_usp).  Returns (list of transfer
+    dicts, staging elements)."""
     lib = load()
     stage = ctypes.c_longlong()
-    xs = _xfers(lambda out, mx, n: lib.gs_plan_a2a(kind, p, me, len(n_tokens), _ints(n_tokens),
-                                                   heads, head_dim, out, mx, n, ctypes.byref(stage)))
+    xs = _xfers(lambda out, mx, n: lib.gs_plan_a2a_usp(kind, p, ring, me, len(n_tokens), _ints(n_tokens),
+                                                       heads, head_dim, out, mx, n, ctypes.byref(stage)))
     return xs, stage.value
 
 

@@ -580,7 +580,7 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream) {
   if (M == 0) return cudaSuccess;
   const int d = D / heads;
-  if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > 16)
+  if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > kMaxChunks)
     return cudaErrorInvalidValue;
   const int tpr = row_tpr(D);
   const int vpl = (D / 8 + tpr - 1) / tpr;  // 1..8

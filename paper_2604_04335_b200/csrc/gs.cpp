@@ -379,7 +379,7 @@ struct Plan : A2aGeometry {
   std::vector<unsigned long long*> flags_of;
 };
 
-void make_plan(Plan& P, Model* m, const std::vector<Request*>& ureqs, const int* ranks, int p) {
+void make_plan(Plan& P, Model* m, const std::vector<Request*>& ureqs, const int* ranks, int p, int ring = 1) {
   P.text = m->desc.cross_attn != 0;
   P.ureqs = ureqs;
   P.reqs.clear();
@@ -393,7 +393,7 @@ void make_plan(Plan& P, Model* m, const std::vector<Request*>& ureqs, const int*
     }
   std::vector<int> n(P.reqs.size());
   for (size_t v = 0; v < P.reqs.size(); ++v) n[v] = P.reqs[v]->n;
-  P.init(p, n.data(), static_cast<int>(n.size()), m->desc.heads, m->hd);
+  P.init(p, n.data(), static_cast<int>(n.size()), m->desc.heads, m->hd, ring);
   P.m = m;
   P.D = m->desc.dim;
   P.F = m->desc.ffn;
@@ -802,6 +802,7 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
     RopeParams rp{A.row_req.as<int>(), A.row_tok.as<int>(), A.req_grid.as<int>(), P.m->cs_tab, P.m->slot_axis,
                   P.m->p_max};
     PackParams pk{};
+    if (P.nchunks() > kMaxChunks) return fail(c, GS_EUNSUPPORTED, "%d pack chunks (> %d)", P.nchunks(), kMaxChunks);
     pk.ndest = P.nchunks();
     pk.rows = M;
     for (int j = 0; j <= P.nchunks(); ++j) pk.head_off[j] = P.hoff[j];
@@ -1294,6 +1295,12 @@ int gs_set_option(gs_ctx* c, const char* key, long long value) {
     c->a2a_mode = static_cast<int>(value);
     return GS_OK;
   }
+  if (strcmp(key, "usp_ring") == 0) {
+    if (value != 1 && value != 2 && value != 4 && value != 8)
+      return fail(c, GS_EINVAL, "usp_ring %lld (1 = Ulysses only, 2 / 4 / 8 = ring degree)", value);
+    c->usp_ring = static_cast<int>(value);
+    return GS_OK;
+  }
   if (strcmp(key, "gemm_bn") == 0) {
     if (value != 0 && value != 192 && value != 256) return fail(c, GS_EINVAL, "gemm_bn %lld (0, 192, 256)", value);
     g_gemm_bn_override.store(static_cast<int>(value));
@@ -1606,7 +1613,7 @@ void run_body(gs_ctx* c, Ticket* t, std::vector<Request*> reqs, int k) {
   LaneGuard lane(c, ranks[0]);
   Model* m = c->models[reqs[0]->model].get();
   Plan P;
-  make_plan(P, m, reqs, ranks, nranks);
+  make_plan(P, m, reqs, ranks, nranks, c->usp_ring);
   const std::vector<int> mine = local_positions(c, P);
   int done = 0, rc = GS_OK;
   for (int i : mine) {

@@ -83,10 +83,11 @@ struct RopeParams {
   const int* slot_axis;  // [d/2] axis (0 = f, 1 = h, 2 = w) of each pair slot
   int p_max;
 };
+constexpr int kMaxChunks = 64;  // p + partial heads (the USP hybrid cuts every head: 8 + 40 at Wan-14B)
 struct PackParams {
-  int ndest;              // pack chunks: p full-head chunks + one per partial head (<= 16)
-  int head_off[17];       // head_off[j]..head_off[j+1]: heads of chunk j
-  long long dest_off[16]; // element offset of chunk j in each send buffer
+  int ndest;              // pack chunks: p full-head chunks + one per partial head (<= kMaxChunks)
+  int head_off[65];       // head_off[j]..head_off[j+1]: heads of chunk j
+  long long dest_off[64]; // element offset of chunk j in each send buffer
   int rows;               // M (local rows; chunk j is [rows][H_j][d])
   // peer-store mode (fused seq->head exchange): chunk j goes straight into the
   // RECV buffers of the position holding it (peer memory over NVLink, or a local buffer), local

@@ -19,28 +19,42 @@ void shard_bounds(int n, int p, int i, int* lo, int* hi) {
 }
 
 
-void A2aGeometry::init(int p_, const int* n_tokens, int nreq, int heads_, int hd_) {
+void A2aGeometry::init(int p_, const int* n_tokens, int nreq, int heads_, int hd_, int ring_) {
   p = p_;
   B = nreq;
   H = heads_;
   hd = hd_;
   n.assign(n_tokens, n_tokens + nreq);
-  Hf = H / p;
-  R = H % p;
-  const int gg = R ? std::gcd(R, p) : p;
-  c = R ? p / gg : 1;
+  // the USP hybrid needs p = u x ring with u dividing H; otherwise plain Ulysses (+ balanced units)
+  ring = (ring_ > 1 && p % ring_ == 0 && H % (p / ring_) == 0) ? ring_ : 1;
+  units.clear();
+  units_of.assign(p, {});
+  if (ring > 1) {
+    const int u = p / ring, hg = H / u;  // Ulysses degree, heads per head group
+    Hf = 0;
+    R = H;
+    c = ring;
+    for (int h = 0; h < H; ++h)
+      for (int ci = 0; ci < c; ++ci) {
+        units.push_back({(h / hg) * ring + ci, h, ci});
+        units_of[(h / hg) * ring + ci].push_back(static_cast<int>(units.size()) - 1);
+      }
+  } else {
+    Hf = H / p;
+    R = H % p;
+    const int gg = R ? std::gcd(R, p) : p;
+    c = R ? p / gg : 1;
+    if (R) {
+      const int per = R / gg;  // units per position
+      for (int k = 0; k < R * c; ++k) {
+        units.push_back({k / per, p * Hf + k / c, k % c});
+        units_of[k / per].push_back(k);
+      }
+    }
+  }
   hoff.resize(p + R + 1);
   for (int j = 0; j <= p; ++j) hoff[j] = j * Hf;
   for (int u = 1; u <= R; ++u) hoff[p + u] = p * Hf + u;
-  units.clear();
-  units_of.assign(p, {});
-  if (R) {
-    const int per = R / gg;  // units per position
-    for (int k = 0; k < R * c; ++k) {
-      units.push_back({k / per, p * Hf + k / c, k % c});
-      units_of[k / per].push_back(k);
-    }
-  }
   off_full.resize(B);
   rows_full = 0;
   for (int r = 0; r < B; ++r) {
@@ -329,14 +343,14 @@ int copy_out(const std::vector<gs_xfer>& v, gs_xfer* out, int max_out, int* n_ou
 }
 }  // namespace
 
-extern "C" int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
-                           gs_xfer* out, int max_out, int* n_out, long long* stage_elems) {
-  if (p < 1 || p > 8 || me < 0 || me >= p || nreq < 1 || !n_tokens || heads < 1 || head_dim < 1)
+extern "C" int gs_plan_a2a_usp(int kind, int p, int ring, int me, int nreq, const int* n_tokens, int heads,
+                               int head_dim, gs_xfer* out, int max_out, int* n_out, long long* stage_elems) {
+  if (p < 1 || p > 8 || me < 0 || me >= p || nreq < 1 || !n_tokens || heads < 1 || head_dim < 1 || ring < 1)
     return GS_EINVAL;
   for (int r = 0; r < nreq; ++r)
     if (n_tokens[r] < 0) return GS_EINVAL;
   gs::A2aGeometry g;
-  g.init(p, n_tokens, nreq, heads, head_dim);
+  g.init(p, n_tokens, nreq, heads, head_dim, ring);
   std::vector<gs_xfer> v;
   if (kind == 0 || kind == 2) {
     if (kind == 0)
@@ -350,6 +364,11 @@ extern "C" int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_token
     return GS_EINVAL;
   }
   return copy_out(v, out, max_out, n_out);
+}
+
+extern "C" int gs_plan_a2a(int kind, int p, int me, int nreq, const int* n_tokens, int heads, int head_dim,
+                           gs_xfer* out, int max_out, int* n_out, long long* stage_elems) {
+  return gs_plan_a2a_usp(kind, p, 1, me, nreq, n_tokens, heads, head_dim, out, max_out, n_out, stage_elems);
 }
 
 extern "C" int gs_plan_reshard(int n_tokens, int lat, const int* old_ranks, int old_p, const int* new_ranks,

@@ -19,8 +19,13 @@ struct Unit {
 // query chunks each, dealt out R / gcd(R, p) per position, so every position does H / p heads of
 // attention work.  Pack chunks (send layout of every position): chunk j < p = full heads of
 // position j, chunk p + u = partial head Hf p + u.
+// ring > 1 (USP hybrid, DESIGN.md §8 "Ulysses x Ring"): p = u x ring; every head is cut into c = ring
+// query chunks; unit (head h, chunk ci) runs on position (h / (H / u)) * ring + ci -- Ulysses over u
+// head groups, a ring of `ring` positions per head group, each position attending its query chunk
+// against the head's K / V gathered in token order (the ring's exchange as an in-order all-gather,
+// so results stay bit-exact with every other degree).
 struct A2aGeometry {
-  int p = 1, B = 0, H = 0, hd = 0;
+  int p = 1, B = 0, H = 0, hd = 0, ring = 1;
   int Hf = 0, R = 0, c = 1;                     // full heads per position, partial heads, chunks
   std::vector<int> n;                           // tokens per request
   std::vector<int> hoff;                        // p + R + 1 head offsets of the pack chunks
@@ -30,7 +35,7 @@ struct A2aGeometry {
   std::vector<int> rows;                        // [pos] packed rows
   std::vector<Unit> units;                      // all partial units (position-major)
   std::vector<std::vector<int>> units_of;       // [pos] indices into units
-  void init(int p, const int* n_tokens, int nreq, int heads, int hd);
+  void init(int p, const int* n_tokens, int nreq, int heads, int hd, int ring = 1);
   int nchunks() const { return p + R; }
   long long H_loc(int j) const { return hoff[j + 1] - hoff[j]; }  // heads of pack chunk j
   int chunk_lo(int r, int ci) const { return static_cast<int>((static_cast<long long>(ci) * n[r]) / c); }

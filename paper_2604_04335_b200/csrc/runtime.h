@@ -189,6 +189,10 @@ struct gs_ctx {
   // fused (peer-store) all-to-alls: mode 1 = peer stores wherever p divides the
   // heads (default), 0 = transfer plans (NCCL send / recv, emulated device copies)
   int a2a_mode = 1;
+  // USP hybrid (NEXT-2): ring degree r > 1 runs SP degree p as Ulysses over p / r head
+  // groups x a ring of r query chunks per head (K / V gathered in token order; bit-exact with every
+  // other degree); applies to batches whose p is a multiple of r with p / r dividing the heads
+  int usp_ring = 1;
   unsigned long long* flags = nullptr;                    // [world (emulated) or 1][8] barrier words
   unsigned long long sig_sent[8][8] = {}, sig_seen[8][8] = {};  // per (src, dst) global rank pair
   unsigned long long probe_sent[8] = {}, probe_seen[8] = {};      // NCCL mode: mapping probes per peer

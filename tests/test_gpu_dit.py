@@ -243,6 +243,28 @@ def test_preempt_from_another_thread_stops_at_step_boundary(gs):
     assert np.array_equal(z.view(np.uint32), zr.view(np.uint32))
 
 
+@pytest.mark.parametrize("p,ring", [(8, 2), (8, 4), (8, 8), (4, 2), (2, 2)])
+def test_usp_hybrid_bit_exact_vs_sp1(gs, p, ring):
+    """NEXT-2 USP hybrid (gs_set_option "usp_ring"): Ulysses over p / ring head groups x a ring of
+    `ring` query chunks per head (K / V gathered in token order) gives the same bytes as SP = 1, and
+    the exchanges run as transfer plans (every head is cut, so no peer-store path)."""
+    shape = sm.WAN_1_3B.with_layers(2)
+    w, h, f = 416, 240, 5
+    z1 = _run_sp(gs, shape, w, h, f, 1, 2)
+    ctx = gs.Context(device=0, world_size=8, emulated=True)
+    ctx.set_option("usp_ring", ring)
+    mid = _mk(ctx, shape)
+    ranks = list(range(p))
+    req = ctx.submit(mid, w, h, f, 50, 1000, ranks)
+    st0 = ctx.stats()
+    assert ctx.run_steps([req], ranks, 2) == 2
+    st = ctx.stats()
+    z = ctx.read_latent(req)
+    ctx.close()
+    assert st["a2a_plan"] > st0["a2a_plan"] and st["a2a_peer"] == st0["a2a_peer"]
+    assert np.array_equal(z.view(np.uint32), z1.view(np.uint32))
+
+
 def test_async_runs_on_disjoint_sets_concurrent_and_bit_exact(gs):
     """gs_run_steps_async: two SP groups ({0,1} and {2,3,4,5}) in flight together from one thread
     give the same bytes as serial runs; a run on a set overlapping an in-flight run is refused

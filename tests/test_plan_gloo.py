@@ -21,9 +21,18 @@ def shards(n, p):
 
 
 class Units:
-    """Balanced head partition (reading 9), re-derived independently of plan.cpp."""
+    """Balanced head partition (reading 9), re-derived independently of plan.cpp; with
+    ring > 1 the USP hybrid's: every head cut into `ring` query chunks, unit (h, ci) on
+    position (h // (H // u)) * ring + ci, u = p // ring."""
 
-    def __init__(self, H, p):
+    def __init__(self, H, p, ring=1):
+        if ring > 1 and p % ring == 0 and H % (p // ring) == 0:
+            hg = H // (p // ring)
+            self.Hf, self.R, self.c = 0, H, ring
+            self.units = [((h // hg) * ring + ci, h, ci) for h in range(H) for ci in range(ring)]
+            self.of = [[u for u in self.units if u[0] == j] for j in range(p)]
+            self.chunks = [[] for _ in range(p)] + [[h] for h in range(H)]
+            return
         self.Hf, self.R = H // p, H % p
         g = math.gcd(self.R, p) if self.R else p
         self.c = p // g if self.R else 1
@@ -39,19 +48,19 @@ class Units:
 
 
 # ----------------------------------------------------------------------------- reference layouts
-def send_buffer(q, ns, p, i, H, d):
+def send_buffer(q, ns, p, i, H, d, ring=1):
     """Pack layout of position i: chunk j = [rows_i][heads of chunk j][d], chunks in order."""
-    U = Units(H, p)
+    U = Units(H, p, ring)
     offs = np.cumsum([0] + ns[:-1])
     rows = np.concatenate([q[o + lo:o + hi] for o, n in zip(offs, ns) for lo, hi in [shards(n, p)[i]]])
     return np.concatenate([rows[:, hs, :].ravel() for hs in U.chunks if hs] + [np.zeros(0, q.dtype)])
 
 
-def recv_layout(x, ns, p, j, H, kind):
+def recv_layout(x, ns, p, j, H, kind, ring=1):
     """Receive layout at position j: full heads [rows][Hf][d], then per local unit a [rows][d]
     block: all rows (kind 'kv') or the unit's query-chunk rows of every request (kind 'q', also the
     attention-output layout)."""
-    U = Units(H, p)
+    U = Units(H, p, ring)
     offs = np.cumsum([0] + ns[:-1])
     parts = [x[:, j * U.Hf:(j + 1) * U.Hf, :].ravel()]
     for _pos, h, ci in U.of[j]:
@@ -112,8 +121,29 @@ def test_balanced_units_cover_every_head_row_once_and_balance_work():
             assert len(cover) == U.R * U.c and set(cover.values()) <= {1}
 
 
-@pytest.mark.parametrize("p,ns,H,d", CASES)
-def test_a2a_plans_realise_ulysses_layouts(p, ns, H, d):
+USP_CASES = [(8, [300], 12, 4, 2), (8, [75600 // 100], 40, 4, 2), (8, [7, 300, 13], 12, 4, 4),
+             (8, [101, 29], 40, 2, 8), (4, [55, 2, 77], 6, 4, 2), (4, [1001], 40, 4, 4), (2, [33, 17], 12, 8, 2)]
+
+
+def test_usp_units_cover_every_head_chunk_once_and_balance_work():
+    """USP hybrid partition: every (head, query chunk) exactly once, H / u units per position (each a
+    1 / ring share of a head), the units of one head on the `ring` positions of its head group."""
+    for H in (6, 12, 40):
+        for p in (2, 4, 8):
+            for ring in (2, 4, 8):
+                if ring > p or p % ring or H % (p // ring):
+                    continue
+                U = Units(H, p, ring)
+                assert sorted((h, ci) for _p, h, ci in U.units) == [(h, ci) for h in range(H) for ci in range(ring)]
+                assert all(len(U.of[j]) == H // (p // ring) for j in range(p))
+                for h in range(H):
+                    pos = sorted(pp for pp, hh, _ci in U.units if hh == h)
+                    g = pos[0] // ring
+                    assert pos == list(range(g * ring, g * ring + ring))
+
+
+@pytest.mark.parametrize("p,ns,H,d,ring", [c + (1,) for c in CASES] + USP_CASES)
+def test_a2a_plans_realise_ulysses_layouts(p, ns, H, d, ring):
     g = np.random.default_rng(p * 1000 + H)
     N = sum(ns)
     q = g.integers(-1000, 1000, (N, H, d)).astype(np.int64)
@@ -121,18 +151,20 @@ def test_a2a_plans_realise_ulysses_layouts(p, ns, H, d):
     offs = np.cumsum([0] + ns[:-1])
     # seq -> head: K / V (kind 0) and Q (kind 2)
     for kind, name in ((0, "kv"), (2, "q")):
-        plans = [gs.plan_a2a(kind, p, i, ns, H, d)[0] for i in range(p)]
-        bufs = [{gs.BUF_SEND: send_buffer(q, ns, p, i, H, d),
-                 gs.BUF_RECV: np.full(recv_layout(q, ns, p, i, H, name).size, -7, np.int64)} for i in range(p)]
+        plans = [gs.plan_a2a(kind, p, i, ns, H, d, ring)[0] for i in range(p)]
+        bufs = [{gs.BUF_SEND: send_buffer(q, ns, p, i, H, d, ring),
+                 gs.BUF_RECV: np.full(recv_layout(q, ns, p, i, H, name, ring).size, -7, np.int64)}
+                for i in range(p)]
         execute(plans, bufs)
         for j in range(p):
-            np.testing.assert_array_equal(bufs[j][gs.BUF_RECV], recv_layout(q, ns, p, j, H, name), err_msg=name)
+            np.testing.assert_array_equal(bufs[j][gs.BUF_RECV], recv_layout(q, ns, p, j, H, name, ring),
+                                          err_msg=name)
     # head -> seq
-    plans, stages = zip(*[gs.plan_a2a(1, p, i, ns, H, d) for i in range(p)])
+    plans, stages = zip(*[gs.plan_a2a(1, p, i, ns, H, d, ring) for i in range(p)])
     bufs = []
     for i in range(p):
         rows_i = sum(hi - lo for n in ns for lo, hi in [shards(n, p)[i]])
-        bufs.append({gs.BUF_O: recv_layout(o, ns, p, i, H, "q").copy(),
+        bufs.append({gs.BUF_O: recv_layout(o, ns, p, i, H, "q", ring).copy(),
                      gs.BUF_STAGE: np.full(max(stages[i], 1), -9, np.int64),
                      gs.BUF_ORECV: np.full(rows_i * H * d, -5, np.int64)})
     execute(plans, bufs)
