@@ -136,6 +136,13 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], floa
 
 // SCATTER: the fused head->seq exchange epilogue (OScatter); a separate instantiation so the plain
 // kernel keeps its register allocation (the scatter lookup in the shared epilogue cost ~5%).
+// SPLITP (-DGS_ATTN_SPLITP=1, development A/B): the softmax hands P over in two 64-key halves so the
+// issuer can start PV on the first half while the second is still being exponentiated.
+#ifndef GS_ATTN_SPLITP
+#define GS_ATTN_SPLITP 0
+#endif
+constexpr int NPH = GS_ATTN_SPLITP ? 2 : 1;  // P hand-offs per group per KV tile
+
 template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false>
 __global__ void __launch_bounds__(THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -157,8 +164,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* vfull = kempty + C::KST;    // [VST]
   uint64_t* vempty = vfull + C::VST;    // [VST]
   uint64_t* sfull = vempty + C::VST;    // [2]
-  uint64_t* pfull = sfull + 2;        // [2]
-  uint64_t* ofull = pfull + 2;        // [2]
+  uint64_t* pfull = sfull + 2;        // [2] (SPLITP: [2 groups][2 key halves])
+  uint64_t* ofull = pfull + 2 * NPH;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ofull + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int w = 0; w < 2; ++w) {
       mbar_init(&sfull[w], 1);
-      mbar_init(&pfull[w], 4 * NC);
+      for (int hh = 0; hh < NPH; ++hh) mbar_init(&pfull[w * NPH + hh], 4 * NC);
       mbar_init(&ofull[w], 1);
     }
     fence_barrier_init();
@@ -301,11 +308,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit(&sfull[w]);
         TRACE_EV(13, w, j);
       };
-      auto issue_pv = [&](int w, int j) {  // O_w += P_w V_j, P_w read from TMEM (bf16 over S_w)
+      auto issue_pv = [&](int w, int j, int half = -1) {  // O_w += P_w V_j, P_w from TMEM (bf16 over S_w)
         TRACE_EV(1, w, j);
         const uint64_t vb = vdesc0 + (((j % C::VST) * C::VT_BYTES) >> 4);
+        const int k0 = half < 0 ? 0 : 4 * half, k1 = half < 0 ? 8 : k0 + 4;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int kk = k0; kk < k1; ++kk) {
           if (PAIR)
             mma_ts_2sm(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, vb + ((kk * 2048) >> 4), idesc_o,
                        (j > 0) || (kk > 0));
@@ -315,11 +323,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         TRACE_EV(14, w, j);
       };
-      auto wait_p = [&](int w, int j) {
+      auto wait_p = [&](int w, int j, int half = 0) {
         TRACE_EV(12, w, j);
-        mbar_wait_spin(&pfull[w], j & 1);
+        mbar_wait_spin(&pfull[w * NPH + half], j & 1);
         TRACE_EV(10, w, j);
         tc_fence_after();
+      };
+      auto pv = [&](int w, int j) {  // wait for P_w and issue PV_w (in two halves with SPLITP)
+        if (NPH == 2) {
+          wait_p(w, j, 0);
+          issue_pv(w, j, 0);
+          wait_p(w, j, 1);
+          issue_pv(w, j, 1);
+        } else {
+          wait_p(w, j);
+          issue_pv(w, j);
+        }
       };
       mbar_wait_spin(&kfull[0], 0);
       tc_fence_after();
@@ -335,11 +354,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait_spin(&vfull[j % C::VST], (j / C::VST) & 1);
         if (more) mbar_wait_spin(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
         TRACE_EV(11, 0, j);
-        wait_p(0, j);
-        issue_pv(0, j);
+        pv(0, j);
         if (more) issue_s(0, j + 1);
-        wait_p(1, j);
-        issue_pv(1, j);
+        pv(1, j);
         commit(&vempty[j % C::VST]);
         if (more) {
           issue_s(1, j + 1);
@@ -409,21 +426,39 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       l_run *= alpha;
       float2 acc;
-      if (full)
+      auto hand_over = [&](int hh) {  // P (or its half hh) is in TMEM: tell the MMA issuer
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (PAIR)
+            mbar_arrive_cluster(mapa_shared(smem_u32(&pfull[w * NPH + hh]), 0));
+          else
+            mbar_arrive(&pfull[w * NPH + hh]);
+        }
+      };
+      if (NPH == 2) {  // keys [0, 64) then [64, 128), each half handed over as soon as it is stored
+        const uint32_t(&va)[64] = *reinterpret_cast<const uint32_t(*)[64]>(v);
+        const uint32_t(&vb)[64] = *reinterpret_cast<const uint32_t(*)[64]>(v + 64);
+        float2 a0, a1;
+        if (full) {
+          a0 = exp_pack_store<POLY8, true, 64>(va, sc2, make_float2(-m_run, -m_run), kv_valid, tS, 0);
+          hand_over(0);
+          a1 = exp_pack_store<POLY8, true, 64>(vb, sc2, make_float2(-m_run, -m_run), kv_valid, tS + 32, 64);
+        } else {
+          a0 = exp_pack_store<POLY8, false, 64>(va, sc2, make_float2(-m_run, -m_run), kv_valid, tS, 0);
+          hand_over(0);
+          a1 = exp_pack_store<POLY8, false, 64>(vb, sc2, make_float2(-m_run, -m_run), kv_valid, tS + 32, 64);
+        }
+        acc = __fadd2_rn(a0, a1);
+      } else if (full) {
         acc = exp_pack_store<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
-      else
+      } else {
         acc = exp_pack_store<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
-      l_run += acc.x + acc.y;
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      const long long t_done = TRACE ? clock64() : 0;
-      if (lane == 0) {
-        if (PAIR)
-          mbar_arrive_cluster(mapa_shared(smem_u32(&pfull[w]), 0));
-        else
-          mbar_arrive(&pfull[w]);
       }
+      l_run += acc.x + acc.y;
+      const long long t_done = TRACE ? clock64() : 0;
+      hand_over(NPH - 1);
       if (TRACE && lane == 0 && blockIdx.x < 2 && blockIdx.y == 0 && j < 32)
         g_attn_trace[blockIdx.x * 1024 + ((4 + quarter) * 32 + j) * 2 + w] = t_done;
     }
