@@ -99,8 +99,10 @@ __device__ __forceinline__ constexpr bool poly_pair(int k) {
 // P = exp2(S * scale - m) for the 128 columns of this thread's row, packed to bf16 pairs and
 // stored over the S columns [0, 64) in TMEM (P aliases S).  Returns the fp32 partial row sums.
 // FULL = false is the last (partial) KV tile of a request: masked columns get p = 0 exactly.
-template <int POLY8, bool FULL, int NCOL = 128>
-__device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], float2 sc2, float2 nm2,
+// KEEP: also write the fp32 p values back over v (the row sum is then taken after the P hand-off,
+// off the softmax -> MMA chain; -DGS_ATTN_LSUM=1) and return zeros.
+template <int POLY8, bool FULL, int NCOL = 128, bool KEEP = false>
+__device__ __forceinline__ float2 exp_pack_store(uint32_t (&v)[NCOL], float2 sc2, float2 nm2,
                                                  int kv_valid, uint32_t tS, int col0 = 0) {
   float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -123,10 +125,14 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], floa
         p.x = col0 + col < kv_valid ? p.x : 0.f;
         p.y = col0 + col + 1 < kv_valid ? p.y : 0.f;
       }
-      if (i & 1)
+      if (KEEP) {
+        v[col] = __float_as_uint(p.x);
+        v[col + 1] = __float_as_uint(p.y);
+      } else if (i & 1) {
         acc1 = __fadd2_rn(acc1, p);
-      else
+      } else {
         acc0 = __fadd2_rn(acc0, p);
+      }
       pk[i] = pack_bf16x2(p.x, p.y);
     }
     GS_TMEM_ST16(tS + c * 16, pk);
@@ -142,6 +148,19 @@ __device__ __forceinline__ float2 exp_pack_store(const uint32_t (&v)[NCOL], floa
 #define GS_ATTN_SPLITP 0
 #endif
 constexpr int NPH = GS_ATTN_SPLITP ? 2 : 1;  // P hand-offs per group per KV tile
+// SEQ (-DGS_ATTN_SEQ=1, development A/B): phase lock between the two softmax warpgroups through two
+// named barriers -- WG1 pauses after the first 64 keys of its exps until WG0 has handed over its
+// whole P of the same tile, and WG0 continues past its hand-off only once WG1 reached that midpoint,
+// so WG1 runs half a softmax behind WG0 and the two never drift into lock-step.
+#ifndef GS_ATTN_SEQ
+#define GS_ATTN_SEQ 0
+#endif
+// LSUM (-DGS_ATTN_LSUM=1, development A/B): the row sum of p is taken after P is handed over.
+#ifndef GS_ATTN_LSUM
+#define GS_ATTN_LSUM 0
+#endif
+constexpr bool kSeq = GS_ATTN_SEQ != 0, kLsum = GS_ATTN_LSUM != 0;
+constexpr int kBarSeqA = 1, kBarSeqB = 2;  // named barrier ids (0 = __syncthreads)
 
 template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -283,6 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         else
           mma_commit(bar);
       };
+      auto wait = [&](uint64_t* bar, uint32_t parity) { mbar_wait_spin(bar, parity); };
       const uint32_t sq = smem_u32(smem + C::Q_OFF);
       const uint32_t sk0 = smem_u32(smem + C::K_OFF);
       const uint32_t sv0 = smem_u32(smem + C::V_OFF);
@@ -325,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       auto wait_p = [&](int w, int j, int half = 0) {
         TRACE_EV(12, w, j);
-        mbar_wait_spin(&pfull[w * NPH + half], j & 1);
+        wait(&pfull[w * NPH + half], j & 1);
         TRACE_EV(10, w, j);
         tc_fence_after();
       };
@@ -340,7 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           issue_pv(w, j);
         }
       };
-      mbar_wait_spin(&kfull[0], 0);
+      wait(&kfull[0], 0);
       tc_fence_after();
       if (TRACE && cta_lin < 8192) g_attn_ctatime[cta_lin * 4 + 1] = gtimer();
       issue_s(0, 0);
@@ -351,8 +371,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // V_j and K_{j+1} landed long ago in steady state: check them before waiting on P (folding
         // these checks into P0's barrier via a helper warp was measured: no gain, see r01_notes.md)
         TRACE_EV(15, 0, j);
-        mbar_wait_spin(&vfull[j % C::VST], (j / C::VST) & 1);
-        if (more) mbar_wait_spin(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
+        wait(&vfull[j % C::VST], (j / C::VST) & 1);
+        if (more) wait(&kfull[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
         TRACE_EV(11, 0, j);
         pv(0, j);
         if (more) issue_s(0, j + 1);
@@ -437,28 +457,43 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_arrive(&pfull[w * NPH + hh]);
         }
       };
-      if (NPH == 2) {  // keys [0, 64) then [64, 128), each half handed over as soon as it is stored
-        const uint32_t(&va)[64] = *reinterpret_cast<const uint32_t(*)[64]>(v);
-        const uint32_t(&vb)[64] = *reinterpret_cast<const uint32_t(*)[64]>(v + 64);
+      if (NPH == 2 || kSeq) {  // keys [0, 64) then [64, 128)
+        uint32_t(&va)[64] = *reinterpret_cast<uint32_t(*)[64]>(v);
+        uint32_t(&vb)[64] = *reinterpret_cast<uint32_t(*)[64]>(v + 64);
+        const float2 nm2 = make_float2(-m_run, -m_run);
         float2 a0, a1;
-        if (full) {
-          a0 = exp_pack_store<POLY8, true, 64>(va, sc2, make_float2(-m_run, -m_run), kv_valid, tS, 0);
-          hand_over(0);
-          a1 = exp_pack_store<POLY8, true, 64>(vb, sc2, make_float2(-m_run, -m_run), kv_valid, tS + 32, 64);
-        } else {
-          a0 = exp_pack_store<POLY8, false, 64>(va, sc2, make_float2(-m_run, -m_run), kv_valid, tS, 0);
-          hand_over(0);
-          a1 = exp_pack_store<POLY8, false, 64>(vb, sc2, make_float2(-m_run, -m_run), kv_valid, tS + 32, 64);
+        a0 = full ? exp_pack_store<POLY8, true, 64, kLsum>(va, sc2, nm2, kv_valid, tS, 0)
+                  : exp_pack_store<POLY8, false, 64, kLsum>(va, sc2, nm2, kv_valid, tS, 0);
+        if (NPH == 2) hand_over(0);  // the first half goes to the MMA issuer as soon as it is stored
+        if (kSeq && w == 1) {        // WG1's midpoint: wait for WG0's hand-off of this tile
+          asm volatile("bar.sync %0, 256;" ::"n"(kBarSeqB) : "memory");
+          asm volatile("bar.arrive %0, 256;" ::"n"(kBarSeqA) : "memory");
         }
+        a1 = full ? exp_pack_store<POLY8, true, 64, kLsum>(vb, sc2, nm2, kv_valid, tS + 32, 64)
+                  : exp_pack_store<POLY8, false, 64, kLsum>(vb, sc2, nm2, kv_valid, tS + 32, 64);
         acc = __fadd2_rn(a0, a1);
       } else if (full) {
-        acc = exp_pack_store<POLY8, true>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
+        acc = exp_pack_store<POLY8, true, 128, kLsum>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
       } else {
-        acc = exp_pack_store<POLY8, false>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
+        acc = exp_pack_store<POLY8, false, 128, kLsum>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
       }
-      l_run += acc.x + acc.y;
+      if (!kLsum) l_run += acc.x + acc.y;
       const long long t_done = TRACE ? clock64() : 0;
       hand_over(NPH - 1);
+      if (kSeq && w == 0) {  // WG0 past its hand-off: release WG1's midpoint, wait until WG1 is there
+        asm volatile("bar.arrive %0, 256;" ::"n"(kBarSeqB) : "memory");
+        asm volatile("bar.sync %0, 256;" ::"n"(kBarSeqA) : "memory");
+      }
+      if (kLsum) {  // row sum of this tile's p (fp32, kept in v), two chains
+        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          s0 = __fadd2_rn(s0, make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1])));
+          s1 = __fadd2_rn(s1, make_float2(__uint_as_float(v[2 * i + 2]), __uint_as_float(v[2 * i + 3])));
+        }
+        acc = __fadd2_rn(s0, s1);
+        l_run += acc.x + acc.y;
+      }
       if (TRACE && lane == 0 && blockIdx.x < 2 && blockIdx.y == 0 && j < 32)
         g_attn_trace[blockIdx.x * 1024 + ((4 + quarter) * 32 + j) * 2 + w] = t_done;
     }
