@@ -18,7 +18,10 @@
 //     one of: bf16 store (64 B per thread per 32-channel chunk); fp32 store (the decoder's residual
 //     stream, 128 B per chunk); the temporal-upsample interleave (the
 //     two channel halves of frame t go to output frames 2t + 1, 2t + 2; reading V5); fp32 clamp to
-//     [-1, 1] of the first `out_real` channels (the decoder output, reading V7).
+//     [-1, 1] of the first `out_real` channels (the decoder output, reading V7); optionally also the
+//     next residual block's RMS norm + SiLU of the same values (ConvParams::norm_*: a second pass over
+//     the voxel's channels once their square sum is known -- one TMEM lane holds all of a voxel's
+//     channels when one N tile spans Coutp), which removes the decoder's stand-alone norm passes.
 // Each output depends only on its own inputs; no split-K, no atomics.
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -216,19 +219,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
       const bool valid = h < cp.H && w < cp.W;
       const long long vox = (static_cast<long long>(t) * cp.H + h) * cp.W + w;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * BN;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        GS_TMEM_LD32(tbase + c * 32, r);
-        tmem_ld_wait();
-        if (c + 1 == BN / 32) {  // accumulator fully in registers: hand it back to the MMA issuer
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(tempty_leader + as * 8);
-        }
-        if (!valid) continue;
-        const int ch0 = nb * BN + c * 32;
-        float v[32];
+      // fused norm (host-checked: one N tile per voxel): pass 1 below accumulates the square sum, pass 2
+      // writes the normalised activation; with no main output pass 2 re-reads TMEM, so the accumulator
+      // is handed back to the MMA issuer only after it
+      const bool fuse = cp.norm_gamma != nullptr;
+      const bool reread = fuse && cp.mode == CONV_OUT_NONE;
+      float ss = 0.f;
+      auto add_bias = [&](const uint32_t(&r)[32], int ch0, float(&v)[32]) {
 #pragma unroll
         for (int i = 0; i < 32; i += 8) {
           const uint4 braw = __ldg(reinterpret_cast<const uint4*>(cp.bias + ch0 + i));
@@ -240,6 +237,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
             v[i + 2 * j + 1] = __uint_as_float(r[i + 2 * j + 1]) + bf.y;
           }
         }
+      };
+      auto hand_back = [&]() {  // accumulator fully in registers: hand it back to the MMA issuer
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + as * 8);
+      };
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        GS_TMEM_LD32(tbase + c * 32, r);
+        tmem_ld_wait();
+        if (c + 1 == BN / 32 && !reread) hand_back();
+        if (!valid) continue;
+        const int ch0 = nb * BN + c * 32;
+        float v[32];
+        add_bias(r, ch0, v);
         if (cp.resid != nullptr && cp.resid_f32) {
           const float4* rp = reinterpret_cast<const float4*>(static_cast<const float*>(cp.resid) + vox * cp.Coutp + ch0);
 #pragma unroll
@@ -265,6 +278,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
             }
           }
         }
+        if (fuse) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (ch0 + i < cp.norm_c) ss = fmaf(v[i], v[i], ss);
+        }
+        if (cp.mode == CONV_OUT_NONE) continue;
         if (cp.mode == CONV_OUT_F32_CLAMP) {
           float* o = static_cast<float*>(cp.out) + vox * cp.out_real;
           for (int i = 0; i < 32 && ch0 + i < cp.out_real; ++i) o[ch0 + i] = fminf(fmaxf(v[i], -1.0f), 1.0f);
@@ -288,6 +307,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
         for (int q = 0; q < 4; ++q)
           o[q] = make_uint4(pack_bf16x2(v[8 * q], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
                             pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+      }
+      if (fuse) {  // pass 2: y = SiLU(v sqrt(C) / max(||v||, 1e-12) gamma), the same v as pass 1
+        const float scale = sqrtf(static_cast<float>(cp.norm_c)) / fmaxf(sqrtf(ss), 1e-12f);
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          const int ch0 = nb * BN + c * 32;
+          float v[32];
+          if (reread) {
+            uint32_t r[32];
+            GS_TMEM_LD32(tbase + c * 32, r);
+            tmem_ld_wait();
+            if (c + 1 == BN / 32) hand_back();
+            if (!valid) continue;
+            add_bias(r, ch0, v);
+          } else {  // F32: v as stored by pass 1 (this thread's own writes; exact)
+            if (!valid) continue;
+            const float4* src = reinterpret_cast<const float4*>(static_cast<const float*>(cp.out) + vox * cp.out_cs + ch0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 t4 = src[q];
+              v[4 * q] = t4.x;
+              v[4 * q + 1] = t4.y;
+              v[4 * q + 2] = t4.z;
+              v[4 * q + 3] = t4.w;
+            }
+          }
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 32; i += 8) {
+            const uint4 graw = __ldg(reinterpret_cast<const uint4*>(cp.norm_gamma + ch0 + i));
+            const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&graw);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 gf = __bfloat1622float2(g2[j]);
+              float u[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int ci = i + 2 * j + e;
+                const float n = v[ci] * scale * (e ? gf.y : gf.x);
+                u[e] = ch0 + ci < cp.norm_c ? n / (1.0f + __expf(-n)) : 0.f;
+              }
+              pk[(i + 2 * j) / 2] = pack_bf16x2(u[0], u[1]);
+            }
+          }
+          uint4* o = reinterpret_cast<uint4*>(cp.norm_out + vox * cp.Coutp + ch0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) o[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
       }
     }
   }
@@ -393,12 +460,17 @@ cudaError_t launch_kb(const void* x, const void* w, const ConvParams& cp, int nu
 
 cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
   if (cp.T <= 0 || cp.H <= 0 || cp.W <= 0) return cudaSuccess;
-  if (cp.Cp % 32 || cp.Coutp % 32 || cp.kt < 1 || cp.kh < 1 || cp.kw < 1 || !cp.bias || !cp.out)
+  if (cp.Cp % 32 || cp.Coutp % 32 || cp.kt < 1 || cp.kh < 1 || cp.kw < 1 || !cp.bias ||
+      (!cp.out && cp.mode != CONV_OUT_NONE))
     return cudaErrorInvalidValue;
   if ((cp.mode == CONV_OUT_BF16 || cp.mode == CONV_OUT_F32) && (cp.out_cs % 8 || cp.out_cs < cp.Coutp))
     return cudaErrorInvalidValue;
   if (cp.mode == CONV_OUT_TIME_INTERLEAVE && (cp.out_real % 32 || 2 * cp.out_real > cp.Coutp || cp.out_cs % 8))
     return cudaErrorInvalidValue;
+  if (cp.norm_gamma && (!cp.norm_out || conv_bn(cp.Coutp) != cp.Coutp || cp.norm_c < 1 || cp.norm_c > cp.Coutp ||
+                        !(cp.mode == CONV_OUT_F32 || (cp.mode == CONV_OUT_NONE && !cp.resid))))
+    return cudaErrorInvalidValue;
+  if (cp.mode == CONV_OUT_NONE && !cp.norm_gamma) return cudaErrorInvalidValue;
   // 64-channel K blocks (128B swizzle) when the input channels allow, else 32 (64B swizzle)
   if (cp.Cp % 64 == 0) return launch_kb<64, 1>(x, w, cp, num_sms, stream);
   if (cp.Cp % 96 == 0) return launch_kb<32, 3>(x, w, cp, num_sms, stream);  // 96-channel taps in one stage

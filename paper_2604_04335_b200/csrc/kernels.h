@@ -152,6 +152,7 @@ enum ConvOut : int {
                                  // [out_real, 2 out_real) -> frame 2t+2 (out bf16 [.][H][W][out_cs])
   CONV_OUT_F32_CLAMP = 2,        // out fp32 [T][H][W][out_real] = clamp(acc + b, -1, 1), channels < out_real
   CONV_OUT_F32 = 3,              // out fp32 [T][H][W][out_cs] (the decoder's fp32 residual stream)
+  CONV_OUT_NONE = 4,             // no main output (only the fused norm output below)
 };
 struct ConvParams {
   int T, H, W, Cp, kt, kh, kw, Coutp;
@@ -160,7 +161,16 @@ struct ConvParams {
   void* out;
   int out_cs, mode, out_real;
   int resid_f32;
+  // Fused RMS norm + SiLU of the result (the next residual block's norm, oracle/vae.py rms_norm_c +
+  // silu): with norm_gamma set, y = SiLU(v sqrt(norm_c) / max(||v||, 1e-12) gamma) over the first norm_c
+  // channels of v = acc + b (+ resid) is also written, bf16 [T][H][W][Coutp] to norm_out (pad channels
+  // 0).  Needs one N tile per voxel (conv_bn(Coutp) == Coutp) and mode F32 or NONE (NONE: no resid).
+  const __nv_bfloat16* norm_gamma;
+  __nv_bfloat16* norm_out;
+  int norm_c;
 };
+// N tile width of conv3d_tc for Coutp output channels (a fused norm needs conv_bn(Coutp) == Coutp).
+int conv_bn(int Coutp);
 cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream);
 // DiT latent [F*Ht*Wt, 64] fp32 (features (c, pt, ph, pw)) -> z bf16 [F][2Ht][2Wt][zc] (zc = 32 or 64):
 // z = lat * std[c] + mean[c] for the 16 channels, channels 16..zc-1 = 0 (reading V6).

@@ -152,9 +152,14 @@ struct Decoder {
   int ck(cudaError_t e, const char* what) {
     return e == cudaSuccess ? GS_OK : vfail(c, GS_ECUDA, "%s: %s", what, cudaGetErrorString(e));
   }
-  // one convolution; x bf16 [T][H][W][x_cp]
+  // Buffer role holding SiLU(norm(X)) for the next consumer (fused into the producing conv's
+  // epilogue), or -1.  Roles 1 and 2 alternate so a conv never writes the buffer it reads.
+  int ready = -1;
+  static bool fusable(int coutp) { return conv_bn(coutp) == coutp; }
+  // one convolution; x bf16 [T][H][W][x_cp]; with `nrm` its epilogue also writes SiLU(nrm(v)) to nout
   int conv(const VaeConv& cv, const bf16* x, int T, int H, int W, int x_cp, void* out, int mode,
-           const void* resid = nullptr, bool resid_f32 = false, int out_real = 0, int out_cs = 0) {
+           const void* resid = nullptr, bool resid_f32 = false, int out_real = 0, int out_cs = 0,
+           const VaeNorm* nrm = nullptr, bf16* nout = nullptr) {
     if (dry) return GS_OK;
     ConvParams p{};
     p.T = T;
@@ -172,33 +177,63 @@ struct Decoder {
     p.out_cs = out_cs ? out_cs : cv.coutp;
     p.mode = mode;
     p.out_real = out_real;
+    if (nrm) {
+      p.norm_gamma = nrm->gamma;
+      p.norm_out = nout;
+      p.norm_c = nrm->c;
+    }
     return ck(conv3d_tc(x, cv.w, p, c->num_sms, s), "conv3d");
   }
-  // residual block on the fp32 stream X [T][H][W][cp] (C real channels); returns the new width
-  int res(const VaeRes& r, int T, int H, int W, int& C, int& cp) {
+  // residual block on the fp32 stream X [T][H][W][cp] (C real channels); returns the new width.  `next`
+  // is the norm applied to the block's output by the following consumer (the next block's norm1 or
+  // norm_out), fused into conv2's epilogue when the width allows; null when X is read raw next.
+  int res(const VaeRes& r, int T, int H, int W, int& C, int& cp, const VaeNorm* next) {
     const size_t vox = static_cast<size_t>(T) * H * W;
     const size_t wide = vox * std::max(cp, r.c1.coutp);
     float* X = role<float>(0, wide);
-    bf16* N = role<bf16>(1, wide);
-    bf16* Hb = role<bf16>(2, wide);
     const void* resid = X;
     if (r.skip.cout) {  // shortcut conv of x (bf16 copy of the stream) -> S (fp32)
       float* S = role<float>(3, vox * r.skip.coutp);
-      if (!dry) VRET(ck(vae_cast_bf16(X, static_cast<long long>(vox) * cp, N, s), "cast"));
-      VRET(conv(r.skip, N, T, H, W, cp, S, CONV_OUT_F32));
+      bf16* xb = role<bf16>(1, wide);
+      if (!dry) VRET(ck(vae_cast_bf16(X, static_cast<long long>(vox) * cp, xb, s), "cast"));
+      VRET(conv(r.skip, xb, T, H, W, cp, S, CONV_OUT_F32));
       resid = S;
+      ready = -1;
     }
-    if (!dry) VRET(ck(vae_rmsnorm_silu(X, nullptr, static_cast<long long>(vox), C, cp, r.n1.gamma, N, s), "norm1"));
-    VRET(conv(r.c1, N, T, H, W, cp, Hb, CONV_OUT_BF16));
-    if (!dry)
-      VRET(ck(vae_rmsnorm_silu(nullptr, Hb, static_cast<long long>(vox), r.c1.cout, r.c1.coutp, r.n2.gamma, N, s),
-              "norm2"));
+    int in = ready;  // norm1(x): fused by the producer of X, else a stand-alone pass into role 1
+    if (in < 0) {
+      in = 1;
+      if (!dry)
+        VRET(ck(vae_rmsnorm_silu(X, nullptr, static_cast<long long>(vox), C, cp, r.n1.gamma, role<bf16>(1, wide), s),
+                "norm1"));
+    }
+    int ra = in, rb = 3 - in;  // conv1 reads role ra; conv2 reads role rb (norm2 output)
+    bf16* A = role<bf16>(ra, wide);
+    bf16* B = role<bf16>(rb, wide);
+    if (fusable(r.c1.coutp)) {  // conv1's epilogue writes SiLU(norm2(h)) directly; h is never stored
+      VRET(conv(r.c1, A, T, H, W, cp, nullptr, CONV_OUT_NONE, nullptr, false, 0, 0, &r.n2, B));
+    } else {
+      VRET(conv(r.c1, A, T, H, W, cp, B, CONV_OUT_BF16));
+      if (!dry)
+        VRET(ck(vae_rmsnorm_silu(nullptr, B, static_cast<long long>(vox), r.c1.cout, r.c1.coutp, r.n2.gamma, A, s),
+                "norm2"));
+      std::swap(A, B);  // conv2 reads the norm output
+      std::swap(ra, rb);
+    }
     // x' = x + conv2(...) in the epilogue, fp32, in place over X when the widths agree (each thread
-    // reads its own residual element before writing it)
-    VRET(conv(r.c2, N, T, H, W, r.c1.coutp, X, CONV_OUT_F32, resid, true));
+    // reads its own residual element before writing it); the next norm into the buffer conv2 does not read
+    const bool fuse_next = next && fusable(r.c2.coutp);
+    VRET(conv(r.c2, B, T, H, W, r.c1.coutp, X, CONV_OUT_F32, resid, true, 0, 0, fuse_next ? next : nullptr,
+              fuse_next ? A : nullptr));
+    ready = fuse_next ? ra : -1;
     C = r.c2.cout;
     cp = r.c2.coutp;
     return GS_OK;
+  }
+  // the norm the consumer after block b of stage list `blocks` applies to its output
+  const VaeNorm* next_norm(const std::vector<VaeRes>& blocks, size_t b, const VaeNorm* after) const {
+    if (b + 1 < blocks.size()) return blocks[b + 1].skip.cout ? nullptr : &blocks[b + 1].n1;
+    return after;
   }
   int run(const float* lat_dev, int F, int Ht, int Wt, float* video_dev) {
     int T = F, H = 2 * Ht, W = 2 * Wt;
@@ -209,10 +244,21 @@ struct Decoder {
     VRET(conv(v->post, z, T, H, W, v->post.cp, N, CONV_OUT_BF16));
     VRET(conv(v->conv_in, N, T, H, W, v->post.coutp, role<float>(0, vox * v->conv_in.coutp), CONV_OUT_F32));
     int C = v->conv_in.cout, cp = v->conv_in.coutp;
-    for (const VaeRes& r : v->mid) VRET(res(r, T, H, W, C, cp));
+    ready = -1;
+    // first block of up stage i (its norm1 can be fused into the stage's entry conv), or null
+    auto first_n1 = [&](size_t i) -> const VaeNorm* {
+      if (i >= v->up.size() || v->up[i].empty() || v->up[i][0].skip.cout) return nullptr;
+      return &v->up[i][0].n1;
+    };
+    for (size_t b = 0; b < v->mid.size(); ++b)
+      VRET(res(v->mid[b], T, H, W, C, cp, next_norm(v->mid, b, first_n1(0))));
     for (size_t i = 0; i < v->up.size(); ++i) {
-      for (const VaeRes& r : v->up[i]) VRET(res(r, T, H, W, C, cp));
-      if (i >= v->sconv.size() || !v->sconv[i].cout) continue;
+      const bool last = i + 1 == v->up.size();
+      const bool resample = i < v->sconv.size() && v->sconv[i].cout;  // X is read raw (cast / upsample) next
+      for (size_t b = 0; b < v->up[i].size(); ++b)
+        VRET(res(v->up[i][b], T, H, W, C, cp,
+                 next_norm(v->up[i], b, last ? &v->norm_out : (resample ? nullptr : first_n1(i + 1)))));
+      if (!resample) continue;
       vox = static_cast<size_t>(T) * H * W;
       bf16* up = nullptr;
       if (v->tconv[i].cout) {  // temporal x2 (reading V5): frame 0 kept, time-conv of frames 1..T-1
@@ -235,14 +281,24 @@ struct Decoder {
       H *= 2;
       W *= 2;
       vox = static_cast<size_t>(T) * H * W;
-      VRET(conv(v->sconv[i], up, T, H, W, cp, role<float>(0, vox * v->sconv[i].coutp), CONV_OUT_F32));
+      // the upsampled input is role 1; the next block's norm1 (fused) goes to role 2
+      const VaeNorm* nn = fusable(v->sconv[i].coutp) ? first_n1(i + 1) : nullptr;
+      VRET(conv(v->sconv[i], up, T, H, W, cp, role<float>(0, vox * v->sconv[i].coutp), CONV_OUT_F32, nullptr,
+                false, 0, 0, nn, nn ? role<bf16>(2, vox * v->sconv[i].coutp) : nullptr));
+      ready = nn ? 2 : -1;
       C = v->sconv[i].cout;
       cp = v->sconv[i].coutp;
     }
     vox = static_cast<size_t>(T) * H * W;
-    bf16* n = role<bf16>(1, vox * cp);
-    if (!dry) VRET(ck(vae_rmsnorm_silu(role<float>(0, 0), nullptr, static_cast<long long>(vox), C, cp,
-                                       v->norm_out.gamma, n, s), "norm_out"));
+    bf16* n = nullptr;
+    if (ready > 0) {  // norm_out fused into the last block's conv2
+      n = role<bf16>(ready, vox * cp);
+    } else {
+      n = role<bf16>(1, vox * cp);
+      if (!dry) VRET(ck(vae_rmsnorm_silu(role<float>(0, 0), nullptr, static_cast<long long>(vox), C, cp,
+                                         v->norm_out.gamma, n, s), "norm_out"));
+    }
+    ready = -1;
     VRET(conv(v->conv_out, n, T, H, W, cp, video_dev, CONV_OUT_F32_CLAMP, nullptr, false, v->conv_out.cout));
     out_T = T;
     out_H = H;

@@ -1,27 +1,20 @@
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) by kernel: launches,
-total ms and share.  usage: launch_summary.py launches.csv header-line..."""
+"""Aggregate an ncu --metrics gpu__time_duration.sum --csv launch list by kernel name (ms, launches).
+  python tools/launch_summary.py LAUNCHES.csv [top]"""
 import collections
 import csv
 import sys
 
-
-def main(path, header):
-    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
-    h = rows[0]
-    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    scale = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "ns": 1.0, "us": 1e3, "ms": 1e6}
-    tot, cnt = collections.OrderedDict(), collections.Counter()
-    for r in rows[1:]:
-        k = r[ki].split("(")[0]
-        v = float(r[vi].replace(",", "")) * scale[r[ui]]
-        tot[k] = tot.get(k, 0.0) + v
-        cnt[k] += 1
-    T = sum(tot.values())
-    out = list(header) + [f"{'kernel':60s} {'launches':>8s} {'total ms':>10s} {'share':>7s}"]
-    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-        out.append(f"{k[:60]:60s} {cnt[k]:8d} {v / 1e6:10.2f} {100 * v / T:6.2f}%")
-    return "\n".join(out) + "\n"
-
-
-if __name__ == "__main__":
-    sys.stdout.write(main(sys.argv[1], sys.argv[2:]))
+lines = [ln for ln in open(sys.argv[1]) if ln.startswith('"')]
+top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+agg = collections.defaultdict(lambda: [0, 0.0])
+scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
+for r in csv.DictReader(lines):
+    if r["Metric Name"] != "gpu__time_duration.sum":
+        continue
+    name = r["Kernel Name"].split("(")[0][:90]
+    agg[name][0] += 1
+    agg[name][1] += float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1.0)
+tot = sum(a[1] for a in agg.values())
+print(f"launches {sum(a[0] for a in agg.values())}  total {tot:.2f} ms")
+for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:top]:
+    print(f"{t:10.2f} ms {c:5d}  {k}")
