@@ -44,13 +44,23 @@ constexpr int CTHREADS = 192;
 // 64 B, 64-byte swizzle) for channel counts = 32 mod 64 (the 96-channel last stage runs unpadded).
 // NS boxes per pipeline stage (a 96-channel tap = 3 x 32 in one stage, so each barrier round trip
 // still feeds 6 MMAs).
-template <int BN, int KB, int NS>
+// WR (W-row reuse, kw = 3 convolutions): the CTA's 128 voxels are one h-row of 128 w, and one TMA box
+// of 130 w (the row plus its +-1 halo) per (dt, dh, channel block) serves all three dw taps -- the
+// UMMA descriptor of tap dw starts dw rows into the box (uniform 8-row core groups; UMMA applies the
+// swizzle to absolute shared-memory address bits like TMA, so a row-shifted start with the matrix
+// base-offset field left 0 reads what TMA wrote -- measured: the field set to the start's 128-byte
+// line gives wrong results).
+// A-operand traffic per tile drops from kt kh kw to kt kh boxes.
+template <int BN, int KB, int NS, bool WR = false>
 struct CCfg {
-  static constexpr int A_SUB = CBM * KB * 2;
+  static constexpr int A_ROWS = WR ? CBM + 2 : CBM;                          // rows TMA writes per box
+  static constexpr int A_SUB = (A_ROWS * KB * 2 + 1023) / 1024 * 1024;       // swizzle-atom aligned
+  static constexpr int TAPS = WR ? 3 : 1;                                    // dw taps per stage
   static constexpr int B_SUB = (BN / 2) * KB * 2;
   static constexpr int A_BYTES = NS * A_SUB;
-  static constexpr int B_BYTES = NS * B_SUB;
+  static constexpr int B_BYTES = TAPS * NS * B_SUB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_TX = NS * A_ROWS * KB * 2 + B_BYTES;            // bytes TMA delivers
   static constexpr int MAXST = 8;
   static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > MAXST ? MAXST : (200 * 1024) / STAGE_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 1024;
@@ -83,7 +93,7 @@ __device__ __forceinline__ void tma_load_4d_2sm(const CUtensorMap* map, uint64_t
 }
 
 struct TileGeom {
-  int num_hb, num_wb, num_m, num_n;
+  int num_hb, num_wb, num_m, num_n;  // h blocks of 2 * patch_h rows (pair), w blocks of patch_w
   __device__ void coords(int tile, int& t, int& hb, int& wb, int& nb) const {
     // n fastest (the A patch is reused from L2 by the pair's consecutive N tiles)
     nb = tile % num_n;
@@ -94,11 +104,12 @@ struct TileGeom {
   }
 };
 
-template <int BN, int KB, int NS>
+template <int BN, int KB, int NS, bool WR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
     conv3d_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ ConvParams cp) {
-  using C = CCfg<BN, KB, NS>;
+  using C = CCfg<BN, KB, NS, WR>;
+  constexpr int PH = WR ? 1 : PATCH_H, PW = WR ? CBM : PATCH_W;  // CTA patch (rows x cols)
   constexpr int CA_BYTES = C::A_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -113,13 +124,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
   const uint32_t rank = cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   TileGeom g;
-  g.num_hb = (cp.H + 2 * PATCH_H - 1) / (2 * PATCH_H);
-  g.num_wb = (cp.W + PATCH_W - 1) / PATCH_W;
+  g.num_hb = (cp.H + 2 * PH - 1) / (2 * PH);
+  g.num_wb = (cp.W + PW - 1) / PW;
   g.num_m = cp.T * g.num_hb * g.num_wb;
   g.num_n = cp.Coutp / BN;
   const int num_tiles = g.num_m * g.num_n;
   const int cpb = cp.Cp / (KB * NS);  // channel stage-blocks per tap
-  const int num_k = cp.kt * cp.kh * cp.kw * cpb;
+  const int num_k = cp.kt * cp.kh * (WR ? 1 : cp.kw) * cpb;  // pipeline stages per tile
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -152,23 +163,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
       for (int tile = pair; tile < num_tiles; tile += npairs) {
         int t, hb, wb, nb;
         g.coords(tile, t, hb, wb, nb);
-        const int h0 = hb * 2 * PATCH_H + static_cast<int>(rank) * PATCH_H, w0 = wb * PATCH_W;
+        const int h0 = hb * 2 * PH + static_cast<int>(rank) * PH, w0 = wb * PW;
         int cb = 0, dw = 0, dh = 0, dt = 0;
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
-          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&full[stage]), 0), C::STAGE_BYTES);
+          mbar_arrive_expect_tx_cluster(mapa_shared(smem_u32(&full[stage]), 0), C::STAGE_TX);
 #pragma unroll
           for (int sub = 0; sub < NS; ++sub) {
-            tma_load_4d_2sm(&tmA, &full[stage], sa + sub * C::A_SUB, (cb * NS + sub) * KB, w0 + dw - pw,
-                            h0 + dh - ph, t + dt - (cp.kt - 1));
-            tma_load_2d_2sm(&tmB, &full[stage], sa + CA_BYTES + sub * C::B_SUB, (kb * NS + sub) * KB,
-                            nb * BN + static_cast<int>(rank) * (BN / 2));
+            const int ch = (cb * NS + sub) * KB;
+            // WR: the row with its halo, [w0 - pw, w0 - pw + 130), once for all dw taps
+            tma_load_4d_2sm(&tmA, &full[stage], sa + sub * C::A_SUB, ch, w0 + (WR ? 0 : dw) - pw, h0 + dh - ph,
+                            t + dt - (cp.kt - 1));
+#pragma unroll
+            for (int q = 0; q < C::TAPS; ++q) {  // weights of tap (dt, dh, dw + q), K = tap * Cp + ch
+              const int tap = (dt * cp.kh + dh) * cp.kw + dw + q;
+              tma_load_2d_2sm(&tmB, &full[stage], sa + CA_BYTES + (q * NS + sub) * C::B_SUB, tap * cp.Cp + ch,
+                              nb * BN + static_cast<int>(rank) * (BN / 2));
+            }
           }
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
           if (++cb == cpb) {  // K order: tap-major (dt, dh, dw), channel block minor
             cb = 0;
-            if (++dw == cp.kw) {
+            if (WR || ++dw == cp.kw) {
               dw = 0;
               if (++dh == cp.kh) { dh = 0; ++dt; }
             }
@@ -193,10 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + CA_BYTES;
 #pragma unroll
-          for (int q = 0; q < NS * (KB / 16); ++q) {
-            const int sub = q / (KB / 16), kk = q % (KB / 16);
-            mma_ss_2sm(d_tmem, sdesc_kb<KB>(sa + sub * C::A_SUB + kk * 32), sdesc_kb<KB>(sb + sub * C::B_SUB + kk * 32),
-                       idesc, (kb | q) != 0);
+          for (int q = 0; q < C::TAPS * NS * (KB / 16); ++q) {
+            const int tq = q / (NS * (KB / 16)), sub = (q / (KB / 16)) % NS, kk = q % (KB / 16);
+            const uint32_t a = sa + sub * C::A_SUB + tq * (KB * 2) + kk * 32;  // WR: dw = tq rows down
+            mma_ss_2sm(d_tmem, sdesc_kb<KB>(a),
+                       sdesc_kb<KB>(sb + (tq * NS + sub) * C::B_SUB + kk * 32), idesc, (kb | q) != 0);
           }
           mma_commit_2sm_mc(&empty[stage], 0x3);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -215,7 +233,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(CTHREADS, 1)
       const int as = it & 1;
       mbar_wait(&tfull[as], (it >> 1) & 1);
       tc_fence_after();
-      const int h = hb * 2 * PATCH_H + static_cast<int>(rank) * PATCH_H + quarter, w = wb * PATCH_W + lane;
+      // TMEM lane (quarter * 32 + lane) = voxel of the CTA patch, row-major over PH x PW
+      const int pv = quarter * 32 + lane;
+      const int h = hb * 2 * PH + static_cast<int>(rank) * PH + pv / PW, w = wb * PW + pv % PW;
       const bool valid = h < cp.H && w < cp.W;
       const long long vox = (static_cast<long long>(t) * cp.H + h) * cp.W + w;
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * BN;
@@ -379,14 +399,14 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
   return enc;
 }
 
-bool make_tma_4d_act(CUtensorMap* m, const void* base, int Cp, int W, int H, int T, int kb) {
+bool make_tma_4d_act(CUtensorMap* m, const void* base, int Cp, int W, int H, int T, int kb, int box_w, int box_h) {
   auto enc = tma_encoder();
   if (!enc) return false;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(Cp), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                         static_cast<cuuint64_t>(T)};
   cuuint64_t strides[3] = {static_cast<cuuint64_t>(Cp) * 2, static_cast<cuuint64_t>(W) * Cp * 2,
                            static_cast<cuuint64_t>(H) * W * Cp * 2};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(kb), PATCH_W, PATCH_H, 1};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -407,21 +427,24 @@ bool make_tma_w(CUtensorMap* m, const void* base, long long K, int Coutp, int kb
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int KB, int NS>
+template <int BN, int KB, int NS, bool WR>
 cudaError_t launch_conv(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
-  using C = CCfg<BN, KB, NS>;
+  using C = CCfg<BN, KB, NS, WR>;
+  constexpr int PH = WR ? 1 : PATCH_H, PW = WR ? CBM : PATCH_W;
   CUtensorMap ta, tb;
-  if (!make_tma_4d_act(&ta, x, cp.Cp, cp.W, cp.H, cp.T, KB)) return cudaErrorInvalidValue;
+  if (!make_tma_4d_act(&ta, x, cp.Cp, cp.W, cp.H, cp.T, KB, WR ? C::A_ROWS : PATCH_W, PH))
+    return cudaErrorInvalidValue;
   const long long K = static_cast<long long>(cp.kt) * cp.kh * cp.kw * cp.Cp;
   if (!make_tma_w(&tb, w, K, cp.Coutp, KB, BN / 2)) return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel<BN, KB, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(conv3d_tc_kernel<BN, KB, NS, WR>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const long long tiles = static_cast<long long>(cp.T) * ((cp.H + 7) / 8) * ((cp.W + 31) / 32) * (cp.Coutp / BN);
+  const long long tiles =
+      static_cast<long long>(cp.T) * ((cp.H + 2 * PH - 1) / (2 * PH)) * ((cp.W + PW - 1) / PW) * (cp.Coutp / BN);
   const int pairs = static_cast<int>(std::min<long long>(tiles, num_sms / 2));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
@@ -433,7 +456,7 @@ cudaError_t launch_conv(const void* x, const void* w, const ConvParams& cp, int 
   at.val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = &at;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, conv3d_tc_kernel<BN, KB, NS>, ta, tb, cp);
+  return cudaLaunchKernelEx(&cfg, conv3d_tc_kernel<BN, KB, NS, WR>, ta, tb, cp);
 }
 }  // namespace
 
@@ -446,16 +469,22 @@ int conv_bn(int Coutp) {
   return 32;
 }
 
+template <int KB, int NS, bool WR>
+cudaError_t launch_bn(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
+  switch (conv_bn(cp.Coutp)) {
+    case 256: return launch_conv<256, KB, NS, WR>(x, w, cp, num_sms, stream);
+    case 192: return launch_conv<192, KB, NS, WR>(x, w, cp, num_sms, stream);
+    case 128: return launch_conv<128, KB, NS, WR>(x, w, cp, num_sms, stream);
+    case 96: return launch_conv<96, KB, NS, WR>(x, w, cp, num_sms, stream);
+    case 64: return launch_conv<64, KB, NS, WR>(x, w, cp, num_sms, stream);
+    default: return launch_conv<32, KB, NS, WR>(x, w, cp, num_sms, stream);
+  }
+}
 template <int KB, int NS>
 cudaError_t launch_kb(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
-  switch (conv_bn(cp.Coutp)) {
-    case 256: return launch_conv<256, KB, NS>(x, w, cp, num_sms, stream);
-    case 192: return launch_conv<192, KB, NS>(x, w, cp, num_sms, stream);
-    case 128: return launch_conv<128, KB, NS>(x, w, cp, num_sms, stream);
-    case 96: return launch_conv<96, KB, NS>(x, w, cp, num_sms, stream);
-    case 64: return launch_conv<64, KB, NS>(x, w, cp, num_sms, stream);
-    default: return launch_conv<32, KB, NS>(x, w, cp, num_sms, stream);
-  }
+  // 3-wide w taps: one halo row box serves all three (WR); other widths tap by tap
+  return cp.kw == 3 ? launch_bn<KB, NS, true>(x, w, cp, num_sms, stream)
+                    : launch_bn<KB, NS, false>(x, w, cp, num_sms, stream);
 }
 
 cudaError_t conv3d_tc(const void* x, const void* w, const ConvParams& cp, int num_sms, cudaStream_t stream) {
