@@ -93,7 +93,6 @@ __device__ __forceinline__ constexpr bool poly_pair(int k) {
   return POLY8 == 0 ? false
        : POLY8 == 2 ? (k == 2 || k == 6)
        : POLY8 == 3 ? (k == 1 || k == 4 || k == 6)
-       : POLY8 == 8 ? true
        : (k & 1) == 1;
 }
 
@@ -161,16 +160,6 @@ constexpr int NPH = GS_ATTN_SPLITP ? 2 : 1;  // P hand-offs per group per KV til
 #define GS_ATTN_LSUM 0
 #endif
 constexpr bool kSeq = GS_ATTN_SEQ != 0, kLsum = GS_ATTN_LSUM != 0;
-// QPOLY (-DGS_ATTN_QPOLY=4|8, development A/B): the softmax warps of TMEM lane quarter GS_ATTN_QPQ (default 1: the
-// SMSP the MMA issuer warp shares) compute QPOLY of every 8 exp2 pairs on the FMA pipe, so fewer MUFU
-// instructions queue ahead of the issuer's mbarrier tests in that SMSP's MIO queue.
-#ifndef GS_ATTN_QPOLY
-#define GS_ATTN_QPOLY 0
-#endif
-#ifndef GS_ATTN_QPQ
-#define GS_ATTN_QPQ 1
-#endif
-constexpr bool kQPoly = GS_ATTN_QPOLY != 0;
 constexpr int kBarSeqA = 1, kBarSeqB = 2;  // named barrier ids (0 = __syncthreads)
 
 template <int HD, int POLY8, bool TRACE = false, bool PAIR = (HD == 128), bool SCATTER = false>
@@ -484,11 +473,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   : exp_pack_store<POLY8, false, 64, kLsum>(vb, sc2, nm2, kv_valid, tS + 32, 64);
         acc = __fadd2_rn(a0, a1);
       } else if (full) {
-        if (kQPoly && (quarter == GS_ATTN_QPQ || (GS_ATTN_QPQ == 5 && quarter < 2)))
-          acc = exp_pack_store<(kQPoly ? GS_ATTN_QPOLY : POLY8), true, 128, kLsum>(v, sc2, make_float2(-m_run, -m_run),
-                                                                                  kv_valid, tS);
-        else
-          acc = exp_pack_store<POLY8, true, 128, kLsum>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
+        acc = exp_pack_store<POLY8, true, 128, kLsum>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
       } else {
         acc = exp_pack_store<POLY8, false, 128, kLsum>(v, sc2, make_float2(-m_run, -m_run), kv_valid, tS);
       }
