@@ -585,7 +585,9 @@ def run_gpu(args, rank, world, local_rank):
     work = {"gemm_qkv": ("tensor", 2 * rows * D * 3 * D), "gemm_o": ("tensor", 2 * rows * D * D),
             "gemm_mlp_up": ("tensor", 2 * rows * D * F), "gemm_mlp_down": ("tensor", 2 * rows * F * D),
             "ln_mod": ("hbm", rows * D * (4 + 2)),            # x fp32 in, a bf16 out
-            "qk_norm_rope": ("hbm", rows * 3 * D * 2 * 2)}    # q|k|v bf16 in, packed q, k, v out
+            # q, k bf16 in, normalised / rotated q, k out; v is moved too (packed for the exchange) only at SP > 1
+            # -- at SP = 1 the attention reads V in place from the QKV GEMM output
+            "qk_norm_rope": ("hbm", rows * (2 if p == 1 else 3) * D * 2 * 2)}
     kernels = {}
     for k, (bound, per_launch) in work.items():
         v = st.get(k)

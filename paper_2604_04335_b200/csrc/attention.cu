@@ -926,16 +926,17 @@ cudaError_t launch_alt(const void* Q, const void* K, const void* V, void* O, int
 template <int HD, int POLY8>
 cudaError_t launch_t(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
                    int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream,
-                   const OScatter& osc) {
+                   const OScatter& osc, int v_rs) {
   constexpr bool PAIR = HD == 128;
 #if GS_ATTN_ALT
+  if (HD == 128 && v_rs != kv_rs) return cudaErrorInvalidValue;
   if (HD == 128) return launch_alt<POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
 #endif
   using C = Cfg<HD, PAIR>;
   CUtensorMap tq, tk, tv;
   if (!make_tma_3d_bf16(&tq, Q, HD, heads, q_rows, HD * 2ull, q_rs * 2ull, 64, 1, 128) ||
       !make_tma_3d_bf16(&tk, K, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, PAIR ? 64 : 128) ||
-      !make_tma_3d_bf16(&tv, V, HD, heads, kv_rows, HD * 2ull, kv_rs * 2ull, 64, 1, 128))
+      !make_tma_3d_bf16(&tv, V, HD, heads, kv_rows, HD * 2ull, v_rs * 2ull, 64, 1, 128))
     return cudaErrorInvalidValue;
   static const bool trace = getenv("GS_ATTN_TRACE") != nullptr;
   auto kern = osc.nown > 0 ? attn_tc_kernel<HD, POLY8, false, PAIR, true>
@@ -975,15 +976,16 @@ static_assert(GS_ATTN_POLY8 == 0 || GS_ATTN_POLY8 == 2 || GS_ATTN_POLY8 == 3 || 
 template <int HD>
 cudaError_t launch(const void* Q, const void* K, const void* V, void* O, int heads, int q_rs,
                    int kv_rs, int o_rs, const SeqTable& tab, int q_rows, int kv_rows, cudaStream_t stream,
-                   const OScatter& osc) {
-  return launch_t<HD, GS_ATTN_POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
+                   const OScatter& osc, int v_rs) {
+  return launch_t<HD, GS_ATTN_POLY8>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc, v_rs);
 }
 }  // namespace
 
 cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                                   int q_rs, int kv_rs, int o_rs, const int* q_off, const int* q_len,
                                   const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream,
-                                  const OScatter* scatter) {
+                                  const OScatter* scatter, int v_rs) {
+  if (v_rs == 0) v_rs = kv_rs;  // V's row stride (the QKV GEMM output's 3 D when V is read in place at SP = 1)
   if (nreq < 1 || nreq > MAX_REQ || (d != 64 && d != 128) || heads < 1) return cudaErrorInvalidValue;
   OScatter osc{};
   if (scatter && scatter->nown > 0) {
@@ -1006,18 +1008,18 @@ cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, v
     q_rows = std::max(q_rows, q_off[r] + q_len[r]);
     kv_rows = std::max(kv_rows, kv_off[r] + kv_len[r]);
   }
-  return d == 128 ? launch<128>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc)
-                  : launch<64>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc);
+  return d == 128 ? launch<128>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc, v_rs)
+                  : launch<64>(Q, K, V, O, heads, q_rs, kv_rs, o_rs, tab, q_rows, kv_rows, stream, osc, v_rs);
 }
 
 cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                          int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
-                         int nreq, int num_sms, cudaStream_t stream, const OScatter* scatter) {
+                         int nreq, int num_sms, cudaStream_t stream, const OScatter* scatter, int v_rs) {
   (void)num_sms;
   for (int r = 0; r < nreq; ++r)
     if (seq_len[r] < 1) return cudaErrorInvalidValue;
   return attention_tc_segments(Q, K, V, O, heads, d, q_rs, kv_rs, o_rs, seq_off, seq_len, seq_off, seq_len, nreq,
-                               stream, scatter);
+                               stream, scatter, v_rs);
 }
 
 }  // namespace gs

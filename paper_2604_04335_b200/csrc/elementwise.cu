@@ -8,7 +8,11 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -165,6 +169,11 @@ __device__ __forceinline__ void ln_finish(const float4 (&v)[VPL], float s, long 
   }
 }
 
+// Grid-stride over row groups (RPC rows per CTA per iteration).  When a group's rows belong to one request (rows
+// are request segments, so all but the groups at a request boundary), the combined shift / 1 + scale vectors of
+// that request are formed in shared memory (dynamic, 2 D floats) and kept while the CTA's next groups belong to
+// the same request: per row 2 shared-memory float4 reads per 4 elements instead of 4 L1 loads and 8 adds (the same
+// fp32 operations, hence the same bits).
 template <int TPR, int VPL, int MINB>
 __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
     ln_modulate_kernel(const float* __restrict__ x, int M, int D, const float* __restrict__ sh_a,
@@ -172,27 +181,26 @@ __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
                        const float* __restrict__ sc_b, int b_stride, const int* __restrict__ row_req,
                        float eps, __nv_bfloat16* __restrict__ out) {
   __shared__ float red[16];
+  extern __shared__ float4 ln_stage[];  // [D / 4] shift, then [D / 4] 1 + scale
   pdl_wait();
   pdl_launch_dependents();
-  if (TPR < 128) {
-    // Warp per row, 8 rows per CTA.  When the CTA's rows belong to one request (rows are request
-    // segments, so all but the boundary CTAs), the combined shift / 1 + scale vectors are formed
-    // once per CTA in shared memory: per row 2 shared-memory float4 reads per 4 elements instead
-    // of 4 L1 loads and 8 adds (the same fp32 operations, hence the same bits).  Three CTAs per SM
-    // (80 registers): at four (64) the row's 48 values spilled.  Config 2 (r01h, same-box A/B):
-    // 3.26 -> 2.72 ms per step, bit-identical.
-    __shared__ float4 s_sh[kWarpRowMaxD / 4], s_sc[kWarpRowMaxD / 4];
-    const long long row0 = blockIdx.x * (long long)kWarpRowsPerCta;
-    const long long row = row0 + threadIdx.x / TPR;
-    const long long rlast = row0 + kWarpRowsPerCta - 1 < M ? row0 + kWarpRowsPerCta - 1 : M - 1;
-    const int tid = threadIdx.x & (TPR - 1);
-    const int nv = D >> 2;
+  constexpr int RPC = TPR < 128 ? kWarpRowsPerCta : 1;
+  const int nv = D >> 2;
+  const int tid = TPR < 128 ? (threadIdx.x & (TPR - 1)) : threadIdx.x;
+  float4* s_sh = ln_stage;
+  float4* s_sc = ln_stage + nv;
+  int staged_r = -1;  // request whose vectors the stage holds (CTA-uniform)
+  for (long long row0 = static_cast<long long>(blockIdx.x) * RPC; row0 < M;
+       row0 += static_cast<long long>(gridDim.x) * RPC) {
+    const long long row = row0 + (TPR < 128 ? threadIdx.x / TPR : 0);
+    const long long rlast = row0 + RPC - 1 < M ? row0 + RPC - 1 : M - 1;
     float4 v[VPL];
     float s = 0.f;
     if (row < M) s = ln_load<TPR, VPL>(reinterpret_cast<const float4*>(x + row * D), tid, nv, v);
     const int r0 = row_req[row0];
     const bool staged = r0 == row_req[rlast];
-    if (staged) {
+    if (staged && r0 != staged_r) {
+      __syncthreads();  // every reader of the previous request's vectors is done
       const float4* sha = reinterpret_cast<const float4*>(sh_a);
       const float4* sca = reinterpret_cast<const float4*>(sc_a);
       const float4* shb = reinterpret_cast<const float4*>(sh_b + (long long)r0 * b_stride);
@@ -203,18 +211,15 @@ __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
         s_sc[c] = make_float4(1.f + (a2.x + b2.x), 1.f + (a2.y + b2.y), 1.f + (a2.z + b2.z), 1.f + (a2.w + b2.w));
       }
       __syncthreads();
+      staged_r = r0;
     }
-    if (row >= M) return;
-    if (staged)
-      ln_finish<TPR, VPL, true>(v, s, row, tid, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red, s_sh,
-                                s_sc);
-    else
-      ln_finish<TPR, VPL>(v, s, row, tid, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red);
-  } else {
-    const long long row = blockIdx.x;
-    float4 v[VPL];
-    const float s = ln_load<TPR, VPL>(reinterpret_cast<const float4*>(x + row * D), threadIdx.x, D >> 2, v);
-    ln_finish<TPR, VPL>(v, s, row, threadIdx.x, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red);
+    if (TPR >= 128 || row < M) {
+      if (staged)
+        ln_finish<TPR, VPL, true>(v, s, row, tid, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red, s_sh,
+                                  s_sc);
+      else
+        ln_finish<TPR, VPL>(v, s, row, tid, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out, red);
+    }
   }
 }
 
@@ -253,101 +258,33 @@ __device__ __forceinline__ void qk_tables_build(QkTables& t, const PackParams& p
   __syncthreads();
 }
 
-template <int TPR, int VPL>
-__device__ __forceinline__ void qk_load(const uint4* src, int tid, int nv, uint4 (&qv)[VPL], uint4 (&kv)[VPL],
-                                        float& sq, float& sk) {
-  sq = 0.f;
-  sk = 0.f;
-#pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int c = tid + i * TPR;
-    if (c < nv) {
-      qv[i] = src[c];
-      kv[i] = src[nv + c];
-      float f[8];
-      unpack8(qv[i], f);
-      sq += ((f[0] * f[0] + f[1] * f[1]) + (f[2] * f[2] + f[3] * f[3])) +
-            ((f[4] * f[4] + f[5] * f[5]) + (f[6] * f[6] + f[7] * f[7]));
-      unpack8(kv[i], f);
-      sk += ((f[0] * f[0] + f[1] * f[1]) + (f[2] * f[2] + f[3] * f[3])) +
-            ((f[4] * f[4] + f[5] * f[5]) + (f[6] * f[6] + f[7] * f[7]));
-    }
-  }
+// bf16 pair word -> (lo, hi) as fp32 (exact)
+__device__ __forceinline__ float2 bf2f(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+// Sum of squares of the 8 bf16 values of a chunk: ((f0^2 + f1^2) + (f2^2 + f3^2)) + ((f4^2 + f5^2) + (f6^2 + f7^2)),
+// the even / odd halves of each word as the two lanes of packed FMUL2 / FFMA2.
+__device__ __forceinline__ float sumsq8(const uint4& u) {
+  const float2 a = bf2f(u.x), b = bf2f(u.y), c = bf2f(u.z), e = bf2f(u.w);
+  const float2 ab = __ffma2_rn(make_float2(a.y, b.y), make_float2(a.y, b.y), __fmul2_rn(make_float2(a.x, b.x),
+                                                                                         make_float2(a.x, b.x)));
+  const float2 ce = __ffma2_rn(make_float2(c.y, e.y), make_float2(c.y, e.y), __fmul2_rn(make_float2(c.x, e.x),
+                                                                                         make_float2(c.x, e.x)));
+  return (ab.x + ab.y) + (ce.x + ce.y);
+}
+// One bf16 pair (x0, x1) of q or k: y = (x * r) * g (RMSNorm with gain), then the RoPE rotation
+// (y0 c - y1 s, y0 s + y1 c) with ncs = (-s, c), cs = (c, s); packed to a bf16 pair word.
+__device__ __forceinline__ uint32_t norm_rope_pair(uint32_t xw, uint32_t gw, float2 r2, float2 cs, float2 ncs) {
+  const float2 y = __fmul2_rn(__fmul2_rn(bf2f(xw), r2), bf2f(gw));
+  const float2 t = __fmul2_rn(make_float2(y.y, y.y), ncs);  // (-y1 s, y1 c)
+  const float2 o = __ffma2_rn(make_float2(y.x, y.x), cs, t);
+  return pack_bf16x2(o.x, o.y);
 }
 
-// src = the row's q|k|v (global or a shared-memory stage); v is copied from src[2 nv + c].
-// Destination of (row, head h, element i0): the send layout [rows][H_j][d] at dest_off[j], or (peer
-// mode) row + row_delta[seq] of the receiving position's [rows_full][H_j][d] buffer.
-template <int TPR, int VPL>
-__device__ __forceinline__ void qk_finish(const QkTables& tb, const uint4* src, const uint4 (&qv)[VPL],
-                                          const uint4 (&kv)[VPL], float sq, float sk, long long row, int tid, int D,
-                                          int d, const __nv_bfloat16* __restrict__ g_q,
-                                          const __nv_bfloat16* __restrict__ g_k, float eps, const RopeParams& rp,
-                                          const PackParams& pk, __nv_bfloat16* __restrict__ q_out,
-                                          __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out,
-                                          float* red) {
-  const int nv = D >> 3;
-  const float2 ssum = row_sum2<TPR>(sq, sk, red);
-  const float rq = rsqrtf(ssum.x / D + eps);
-  const float rk = rsqrtf(ssum.y / D + eps);
-
-  const int r = rp.row_req[row];
-  const int tok = rp.row_tok[row];
-  const int Ht = rp.req_grid[3 * r + 1], Wt = rp.req_grid[3 * r + 2];
-  const int half = d >> 1;
-  const int pf = tok / (Ht * Wt), ph = (tok / Wt) % Ht, pw = tok % Wt;
-  const float2* cs_f = rp.cs_tab + (long long)pf * half;
-  const float2* cs_h = rp.cs_tab + (long long)ph * half;
-  const float2* cs_w = rp.cs_tab + (long long)pw * half;
-  long long prow = row;  // destination row
-  if (pk.peer) {
-    int sqi = 0;
-    for (int t = 1; t < pk.nseq; ++t)
-      if (row >= pk.seq_lo[t]) sqi = t;
-    prow = row + pk.row_delta[sqi];
-  }
-  const int lgd = __ffs(d) - 1;  // d in {64, 128}
-  const uint4* gq = reinterpret_cast<const uint4*>(g_q);
-  const uint4* gk = reinterpret_cast<const uint4*>(g_k);
-#pragma unroll
-  for (int i = 0; i < VPL; ++i) {
-    const int c = tid + i * TPR;
-    if (c < nv) {
-      const int e0 = c * 8;
-      const int h = e0 >> lgd, i0 = e0 & (d - 1);
-      const int jc = tb.jc[h], hn = tb.hn[h], hr = tb.hr[h];
-      __nv_bfloat16 *dq = q_out, *dk = k_out, *dv = v_out;
-      long long o = (prow * hn + hr) * (long long)d + i0;
-      if (pk.peer) {
-        dq = pk.dst_q[jc];
-        dk = pk.dst_k[jc];
-        dv = pk.dst_v[jc];
-      } else {
-        o += pk.dest_off[jc];
-      }
-      float fq[8], fk[8], wq[8], wk[8];
-      unpack8(qv[i], fq);
-      unpack8(kv[i], fk);
-      unpack8(__ldg(gq + c), wq);
-      unpack8(__ldg(gk + c), wk);
-      uint32_t oq[4], ok[4];
-#pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        const int slot = (i0 >> 1) + p;
-        const int ax = tb.ax[slot];
-        const float2 cs = __ldg((ax == 0 ? cs_f : (ax == 1 ? cs_h : cs_w)) + slot);
-        const float q0 = fq[2 * p] * rq * wq[2 * p], q1 = fq[2 * p + 1] * rq * wq[2 * p + 1];
-        const float k0 = fk[2 * p] * rk * wk[2 * p], k1 = fk[2 * p + 1] * rk * wk[2 * p + 1];
-        oq[p] = pack_bf16x2(q0 * cs.x - q1 * cs.y, q0 * cs.y + q1 * cs.x);
-        ok[p] = pack_bf16x2(k0 * cs.x - k1 * cs.y, k0 * cs.y + k1 * cs.x);
-      }
-      *reinterpret_cast<uint4*>(dq + o) = make_uint4(oq[0], oq[1], oq[2], oq[3]);
-      *reinterpret_cast<uint4*>(dk + o) = make_uint4(ok[0], ok[1], ok[2], ok[3]);
-      *reinterpret_cast<uint4*>(dv + o) = src[2 * nv + c];
-    }
-  }
-}
-
+// One row per (TPR threads) per iteration; the CTA loops over rows (grid-stride) so the lookup tables and the
+// per-thread constants (gain / RoPE slots, the same for every row: TPR * 8 is a multiple of d) are set up once
+// per CTA instead of once per row.  v is copied to its destination unless v_out == nullptr in the plain
+// (non-peer) layout: at SP = 1 the attention reads V in place from the QKV GEMM output.
 template <int TPR, int VPL, int MINB>
 __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
     qk_norm_rope_pack_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
@@ -359,15 +296,210 @@ __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
   __shared__ QkTables tb;
   pdl_wait();
   pdl_launch_dependents();
-  qk_tables_build(tb, pk, rp, D / d, d >> 1);
-  const long long row = TPR < 128 ? blockIdx.x * (long long)kWarpRowsPerCta + threadIdx.x / TPR : blockIdx.x;
+  const int half = d >> 1;
+  qk_tables_build(tb, pk, rp, D / d, half);
+  constexpr int RPC = TPR < 128 ? kWarpRowsPerCta : 1;  // rows per CTA per iteration
   const int tid = TPR < 128 ? (threadIdx.x & (TPR - 1)) : threadIdx.x;
-  if (TPR < 128 && row >= M) return;
-  const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
-  uint4 qv[VPL], kv[VPL];
-  float sq, sk;
-  qk_load<TPR, VPL>(src, tid, D >> 3, qv, kv, sq, sk);
-  qk_finish<TPR, VPL>(tb, src, qv, kv, sq, sk, row, tid, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out, red);
+  const int nv = D >> 3;
+  const int lgd = __ffs(d) - 1;  // d in {64, 128}
+  const int i0 = (tid * 8) & (d - 1);  // element offset within the head: the same for all chunks of this thread
+  int ax[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) ax[p] = tb.ax[(i0 >> 1) + p];
+  const bool copy_v = pk.peer || v_out != nullptr;
+  const uint4* gq = reinterpret_cast<const uint4*>(g_q);
+  const uint4* gk = reinterpret_cast<const uint4*>(g_k);
+  for (long long row = static_cast<long long>(blockIdx.x) * RPC + (TPR < 128 ? threadIdx.x / TPR : 0); row < M;
+       row += static_cast<long long>(gridDim.x) * RPC) {
+    const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
+    uint4 qv[VPL], kv[VPL];
+    float sq = 0.f, sk = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = tid + i * TPR;
+      if (c < nv) {
+        qv[i] = src[c];
+        kv[i] = src[nv + c];
+        sq += sumsq8(qv[i]);
+        sk += sumsq8(kv[i]);
+      }
+    }
+    const int r = rp.row_req[row];
+    const int tok = rp.row_tok[row];
+    const int Ht = rp.req_grid[3 * r + 1], Wt = rp.req_grid[3 * r + 2];
+    const int pos[3] = {tok / (Ht * Wt), (tok / Wt) % Ht, tok % Wt};
+    float2 cs[4], ncs[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int a = ax[p];
+      cs[p] = __ldg(rp.cs_tab + static_cast<long long>(a == 0 ? pos[0] : (a == 1 ? pos[1] : pos[2])) * half +
+                    (i0 >> 1) + p);
+      ncs[p] = make_float2(-cs[p].y, cs[p].x);
+    }
+    long long prow = row;  // destination row
+    if (pk.peer) {
+      int sqi = 0;
+      for (int t = 1; t < pk.nseq; ++t)
+        if (row >= pk.seq_lo[t]) sqi = t;
+      prow = row + pk.row_delta[sqi];
+    }
+    const float2 ssum = row_sum2<TPR>(sq, sk, red);
+    const float rq = rsqrtf(ssum.x / D + eps);
+    const float rk = rsqrtf(ssum.y / D + eps);
+    const float2 rq2 = make_float2(rq, rq), rk2 = make_float2(rk, rk);
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int c = tid + i * TPR;
+      if (c < nv) {
+        const int h = (c * 8) >> lgd;
+        const int jc = tb.jc[h], hn = tb.hn[h], hr = tb.hr[h];
+        __nv_bfloat16 *dq = q_out, *dk = k_out, *dv = v_out;
+        long long o = (prow * hn + hr) * (long long)d + i0;
+        if (pk.peer) {
+          dq = pk.dst_q[jc];
+          dk = pk.dst_k[jc];
+          dv = pk.dst_v[jc];
+        } else {
+          o += pk.dest_off[jc];
+        }
+        const uint4 wq = __ldg(gq + c), wk = __ldg(gk + c);
+        uint4 oq, ok;
+        oq.x = norm_rope_pair(qv[i].x, wq.x, rq2, cs[0], ncs[0]);
+        oq.y = norm_rope_pair(qv[i].y, wq.y, rq2, cs[1], ncs[1]);
+        oq.z = norm_rope_pair(qv[i].z, wq.z, rq2, cs[2], ncs[2]);
+        oq.w = norm_rope_pair(qv[i].w, wq.w, rq2, cs[3], ncs[3]);
+        ok.x = norm_rope_pair(kv[i].x, wk.x, rk2, cs[0], ncs[0]);
+        ok.y = norm_rope_pair(kv[i].y, wk.y, rk2, cs[1], ncs[1]);
+        ok.z = norm_rope_pair(kv[i].z, wk.z, rk2, cs[2], ncs[2]);
+        ok.w = norm_rope_pair(kv[i].w, wk.w, rk2, cs[3], ncs[3]);
+        *reinterpret_cast<uint4*>(dq + o) = oq;
+        *reinterpret_cast<uint4*>(dk + o) = ok;
+        if (copy_v) *reinterpret_cast<uint4*>(dv + o) = src[2 * nv + c];
+      }
+    }
+  }
+}
+
+// Streaming form for D > 1024 (kQkStreamMinD): a warp per row, grid-stride over rows, no block barrier.  Pass 1
+// streams q and k from HBM (U chunks per lane in flight) and forms the lane's sums of squares (chunks in lane
+// order, then the xor-shuffle tree: a fixed order that depends on D alone); pass 2 re-reads the row (L2-resident:
+// the warp read it a moment ago) and writes the normalised, rotated q and k (and v, unless it stays in place).
+// Few registers per row, so many rows are in flight per SM: the row-per-CTA form above is bound by its per-row
+// latency chain (load -> block reduction -> compute -> store) at ~3 rows per SM.
+constexpr int kQkStreamMinD = 1025;
+#ifndef GS_QK_U
+#define GS_QK_U 2  // pass-1 chunks per lane in flight
+#endif
+constexpr int kQkStreamWarps = 8;  // warps (rows) per CTA
+template <int U>
+__global__ void __launch_bounds__(32 * kQkStreamWarps, 3)
+    qk_norm_rope_stream_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
+                               const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
+                               float eps, const RopeParams rp, const PackParams pk,
+                               __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
+                               __nv_bfloat16* __restrict__ v_out) {
+  __shared__ QkTables tb;
+  pdl_wait();
+  pdl_launch_dependents();
+  const int half = d >> 1;
+  qk_tables_build(tb, pk, rp, D / d, half);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = D >> 3;
+  const int lgd = __ffs(d) - 1;
+  const int i0 = (lane * 8) & (d - 1);  // the same for every chunk of this lane (256 is a multiple of d)
+  int ax[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) ax[p] = tb.ax[(i0 >> 1) + p];
+  const bool copy_v = pk.peer || v_out != nullptr;
+  const uint4* gq = reinterpret_cast<const uint4*>(g_q);
+  const uint4* gk = reinterpret_cast<const uint4*>(g_k);
+  for (long long row = static_cast<long long>(blockIdx.x) * kQkStreamWarps + warp; row < M;
+       row += static_cast<long long>(gridDim.x) * kQkStreamWarps) {
+    const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
+    // pass 1: sums of squares
+    float sq = 0.f, sk = 0.f;
+    for (int c0 = lane; c0 < nv; c0 += 32 * U) {
+      uint4 qv[U], kv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 32 * u;
+        if (c < nv) {
+          qv[u] = src[c];
+          kv[u] = src[nv + c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (c0 + 32 * u < nv) {
+          sq += sumsq8(qv[u]);
+          sk += sumsq8(kv[u]);
+        }
+    }
+    // per-row constants (overlap the reduction)
+    const int r = rp.row_req[row];
+    const int tok = rp.row_tok[row];
+    const int Ht = rp.req_grid[3 * r + 1], Wt = rp.req_grid[3 * r + 2];
+    const int pos[3] = {tok / (Ht * Wt), (tok / Wt) % Ht, tok % Wt};
+    float2 cs[4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int a = ax[p];
+      cs[p] = __ldg(rp.cs_tab + static_cast<long long>(a == 0 ? pos[0] : (a == 1 ? pos[1] : pos[2])) * half +
+                    (i0 >> 1) + p);
+    }
+    long long prow = row;
+    if (pk.peer) {
+      int sqi = 0;
+      for (int t = 1; t < pk.nseq; ++t)
+        if (row >= pk.seq_lo[t]) sqi = t;
+      prow = row + pk.row_delta[sqi];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      sk += __shfl_xor_sync(0xffffffffu, sk, o);
+    }
+    const float rq = rsqrtf(sq / D + eps), rk = rsqrtf(sk / D + eps);
+    const float2 rq2 = make_float2(rq, rq), rk2 = make_float2(rk, rk);
+    // pass 2: normalise, rotate, store; the next chunk's q / k (and v) are loaded before this one is computed
+    uint4 q = src[lane], k = src[nv + lane], v = copy_v ? src[2 * nv + lane] : make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+    for (int c = lane; c < nv; c += 32) {
+      uint4 qn = q, kn = k, vn = v;
+      if (c + 32 < nv) {
+        qn = src[c + 32];
+        kn = src[nv + c + 32];
+        if (copy_v) vn = src[2 * nv + c + 32];
+      }
+      const int h = (c * 8) >> lgd;
+      const int jc = tb.jc[h], hn = tb.hn[h], hr = tb.hr[h];
+      __nv_bfloat16 *dq = q_out, *dk = k_out, *dv = v_out;
+      long long o = (prow * hn + hr) * (long long)d + i0;
+      if (pk.peer) {
+        dq = pk.dst_q[jc];
+        dk = pk.dst_k[jc];
+        dv = pk.dst_v[jc];
+      } else {
+        o += pk.dest_off[jc];
+      }
+      const uint4 wq = __ldg(gq + c), wk = __ldg(gk + c);
+      uint4 oq, ok;
+      oq.x = norm_rope_pair(q.x, wq.x, rq2, cs[0], make_float2(-cs[0].y, cs[0].x));
+      oq.y = norm_rope_pair(q.y, wq.y, rq2, cs[1], make_float2(-cs[1].y, cs[1].x));
+      oq.z = norm_rope_pair(q.z, wq.z, rq2, cs[2], make_float2(-cs[2].y, cs[2].x));
+      oq.w = norm_rope_pair(q.w, wq.w, rq2, cs[3], make_float2(-cs[3].y, cs[3].x));
+      ok.x = norm_rope_pair(k.x, wk.x, rk2, cs[0], make_float2(-cs[0].y, cs[0].x));
+      ok.y = norm_rope_pair(k.y, wk.y, rk2, cs[1], make_float2(-cs[1].y, cs[1].x));
+      ok.z = norm_rope_pair(k.z, wk.z, rk2, cs[2], make_float2(-cs[2].y, cs[2].x));
+      ok.w = norm_rope_pair(k.w, wk.w, rk2, cs[3], make_float2(-cs[3].y, cs[3].x));
+      *reinterpret_cast<uint4*>(dq + o) = oq;
+      *reinterpret_cast<uint4*>(dk + o) = ok;
+      if (copy_v) *reinterpret_cast<uint4*>(dv + o) = v;
+      q = qn;
+      k = kn;
+      v = vn;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ time embedding
@@ -520,6 +652,54 @@ cudaError_t launch_pdl(K kernel, dim3 grid, dim3 block, cudaStream_t stream, Arg
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+template <class K, class... Args>
+cudaError_t launch_pdl_smem(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+    return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// Grid of a grid-stride row kernel: as many CTAs as are resident at once (per-CTA set-up done once), never more
+// than there are row groups.
+// (resident CTAs per device, cached per kernel / device / block / shared-memory size: the occupancy query is a
+// host-side cost on every launch otherwise)
+template <class K>
+dim3 resident_grid(K kern, dim3 block, size_t smem, long long units) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, unsigned, size_t>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), dev, block.x, smem);
+  int resident = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) resident = it->second;
+  }
+  if (resident == 0) {
+    int nb = 0, nsm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, block.x, smem) != cudaSuccess || nb < 1) nb = 1;
+    resident = nb * std::max(nsm, 1);
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = resident;
+  }
+  return dim3(static_cast<unsigned>(std::min<long long>(units, resident)));
+}
+
 // Threads per row, from D alone (every row of a model takes the same reduction order).  Two warps
 // per row for 1024 < D <= 2048 (Wan-1.3B): half the registers per thread, 32 instead of 24
 // resident warps per SM; config 2 (r01k, same box) LN 2.72 -> 2.41, qk 2.54 -> 2.37 ms per step.
@@ -537,14 +717,17 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
   if (D % 4 || D > 4 * MAXV * ROW_THREADS) return cudaErrorInvalidValue;
   const int tpr = row_tpr(D);
   const int vpl = (D / 4 + tpr - 1) / tpr;  // 1..16
-  const dim3 grid(tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
+  const long long units = tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M;
   const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : tpr);
+  const size_t smem = 2ull * D * sizeof(float);  // the staged shift / 1 + scale vectors
 #define GS_LN_CASE(T, V)                                                                                       \
-  case V:                                                                                                      \
-    if (cudaError_t e = launch_pdl(ln_modulate_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : (T == 256 ? 3 : 1))>, grid, block, stream, \
-                                   x, M, D, sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out))                 \
+  case V: {                                                                                                    \
+    auto kern = ln_modulate_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : (T == 256 ? 3 : 1))>;                  \
+    if (cudaError_t e = launch_pdl_smem(kern, resident_grid(kern, block, smem, units), block, smem, stream, x, M, D, \
+                                        sh_a, sh_b, sc_a, sc_b, b_stride, row_req, eps, out))                   \
       return e;                                                                                                 \
-    break;
+    break;                                                                                                      \
+  }
 #define GS_LN_SWITCH(T)                                                                                     \
   switch (vpl) {                                                                                           \
     GS_LN_CASE(T, 1) GS_LN_CASE(T, 2) GS_LN_CASE(T, 3) GS_LN_CASE(T, 4) GS_LN_CASE(T, 5) GS_LN_CASE(T, 6)  \
@@ -582,16 +765,25 @@ cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
   const int d = D / heads;
   if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > kMaxChunks)
     return cudaErrorInvalidValue;
+  if (!pk.peer && (!q_out || !k_out)) return cudaErrorInvalidValue;
+  if (D >= kQkStreamMinD) {
+    auto kern = qk_norm_rope_stream_kernel<GS_QK_U>;
+    const dim3 block(32 * kQkStreamWarps);
+    return launch_pdl(kern, resident_grid(kern, block, 0, (M + kQkStreamWarps - 1) / kQkStreamWarps), block, stream,
+                      qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out);
+  }
   const int tpr = row_tpr(D);
   const int vpl = (D / 8 + tpr - 1) / tpr;  // 1..8
-  const dim3 grid(tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M);
+  const long long units = tpr < 128 ? (M + kWarpRowsPerCta - 1) / kWarpRowsPerCta : M;
   const dim3 block(tpr < 128 ? tpr * kWarpRowsPerCta : tpr);
 #define GS_QK_CASE(T, V)                                                                                     \
-  case V:                                                                                                    \
-    if (cudaError_t e = launch_pdl(qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : (T == 256 ? 3 : 1))>, grid, block,  \
-                                   stream, qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out))            \
+  case V: {                                                                                                  \
+    auto kern = qk_norm_rope_pack_kernel<T, V, T == 32 ? 3 : (T == 64 ? 2 : (T == 256 ? 3 : 1))>;            \
+    if (cudaError_t e = launch_pdl(kern, resident_grid(kern, block, 0, units), block, stream, qkv, M, D, d, g_q, g_k, eps, rp, pk,  \
+                                   q_out, k_out, v_out))                                                     \
       return e;                                                                                               \
-    break;
+    break;                                                                                                   \
+  }
 #define GS_QK_SWITCH(T)                                                                                         \
   switch (vpl) {                                                                                               \
     GS_QK_CASE(T, 1) GS_QK_CASE(T, 2) GS_QK_CASE(T, 3) GS_QK_CASE(T, 4) GS_QK_CASE(T, 5) GS_QK_CASE(T, 6)      \

@@ -823,8 +823,9 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
         pk.seq_lo[r] = P.loff[i][r];
       }
     }
+    // SP = 1: no exchange, so V is not copied -- the attention reads it in place from the QKV output
     if (M) CK(qk_norm_rope_pack(A.qkv.as<bf16>(), M, D, P.H, w.g_q, w.g_k, eps, rp, pk, A.qs.as<bf16>(),
-                                A.ks.as<bf16>(), A.vs.as<bf16>(), strm(c)));
+                                A.ks.as<bf16>(), P.p == 1 ? nullptr : A.vs.as<bf16>(), strm(c)));
   }
   return GS_OK;
 }
@@ -837,9 +838,9 @@ int block_attn(gs_ctx* c, const Plan& P, int j, RankArena& A) {
     sl[r] = P.reqs[r]->n;
   }
   if (P.p == 1) {
-    const int rs = P.H * P.hd;
-    CK(attention_tc(A.qs.p, A.ks.p, A.vs.p, A.o.p, P.H, P.hd, rs, rs, rs, so.data(), sl.data(), P.B, c->num_sms,
-                    strm(c)));
+    const int rs = P.H * P.hd;  // V in place: columns [2D, 3D) of the QKV GEMM output (row stride 3D)
+    CK(attention_tc(A.qs.p, A.ks.p, A.qkv.as<bf16>() + 2 * rs, A.o.p, P.H, P.hd, rs, rs, rs, so.data(), sl.data(),
+                    P.B, c->num_sms, strm(c), nullptr, 3 * rs));
     return GS_OK;
   }
   if (P.peer) {  // fused head->seq exchange: output rows straight into their owners' ORECV

@@ -59,13 +59,14 @@ struct OScatter {
 };
 cudaError_t attention_tc(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                          int q_rs, int kv_rs, int o_rs, const int* seq_off, const int* seq_len,
-                         int nreq, int num_sms, cudaStream_t stream, const OScatter* scatter = nullptr);
+                         int nreq, int num_sms, cudaStream_t stream, const OScatter* scatter = nullptr,
+                         int v_rs = 0);  // V's row stride when it differs from K's (0: kv_rs)
 // General form: segment r's q_len[r] query rows (from q_off[r]) attend to its kv_len[r] key/value
 // rows (from kv_off[r]) -- text cross-attention uses a separate context K/V buffer.
 cudaError_t attention_tc_segments(const void* Q, const void* K, const void* V, void* O, int heads, int d,
                                   int q_rs, int kv_rs, int o_rs, const int* q_off, const int* q_len,
                                   const int* kv_off, const int* kv_len, int nreq, cudaStream_t stream,
-                                  const OScatter* scatter = nullptr);
+                                  const OScatter* scatter = nullptr, int v_rs = 0);
 
 // ----------------------------------------------------------------- element-wise (elementwise.cu)
 // out[m, :] = LN(x[m, :]) * (1 + sc) + sh, sh = sh_a + sh_b[req(m)*b_stride], same for sc.
