@@ -21,18 +21,22 @@ STALL = 'smsp__average_warps_issue_stalled_'
 
 
 def raw(path):
+    """One dict per captured kernel launch: metric -> (unit, value)."""
     out = subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    return {h: (u, v) for h, u, v in zip(rows[0], rows[1], rows[2])}
+    return [{h: (u, v) for h, u, v in zip(rows[0], rows[1], r)} for r in rows[2:]]
 
 
 def summary(path):
-    r = raw(path)
-    d = {k: f"{r[k][1]} {r[k][0]}".strip() for k in KEYS if k in r}
-    st = {k[len(STALL):].replace('_per_issue_active.ratio', ''): float(v[1]) for k, v in r.items()
-          if k.startswith(STALL) and k.endswith('_per_issue_active.ratio')}
-    d['stalls'] = {k: round(v, 3) for k, v in sorted(st.items(), key=lambda x: -x[1]) if v > 0.02}
-    return d
+    res = []
+    for r in raw(path):
+        d = {'kernel': r.get('Kernel Name', ('', ''))[1][:80]}
+        d.update({k: f"{r[k][1]} {r[k][0]}".strip() for k in KEYS if k in r})
+        st = {k[len(STALL):].replace('_per_issue_active.ratio', ''): float(v[1]) for k, v in r.items()
+              if k.startswith(STALL) and k.endswith('_per_issue_active.ratio') and v[1]}
+        d['stalls'] = {k: round(v, 3) for k, v in sorted(st.items(), key=lambda x: -x[1]) if v > 0.02}
+        res.append(d)
+    return res
 
 
 if __name__ == '__main__':
