@@ -277,10 +277,10 @@ def kernel_class_rates(st, steps, shape, rows_per_pos, seqlens, heads_local, nb=
             "gemm_flops_per_position_step": gf}
 
 
-def t2i_secondary(gs, torch, pk, steps=25, warmup=3):
+def t2i_secondary(gs, torch, pk, steps=40, warmup=3):
     """The T2I half of the headline metric (BASELINE.json: "... 720p T2V + 1024px T2I"): config 2,
     4 x 1024^2 images batched on one GPU (Wan-1.3B-shaped, L = 30), device-timed steps with the
-    clocks sampled through a >= 1 s timed region, then one per-kernel-profiled step."""
+    clocks sampled through a ~2 s timed region (>= 10 samples), then one per-kernel-profiled step."""
     shape, reqs_spec, _ = WORKLOADS["t2i1024"]
     ctx = gs.Context(device=0)
     mid = ctx.model_create(shape.dim, shape.heads, shape.ffn, shape.layers, shape.weight_seed)

@@ -326,6 +326,25 @@ __device__ __forceinline__ void mma_commit_2sm_mc(uint64_t* bar, uint16_t cta_ma
       : "memory");
 }
 
+// ------------------------------------------------------------------ L2 eviction-priority hints
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ldg_l2hint(const uint4* ptr, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+
 // ------------------------------------------------------------------ math helpers
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
