@@ -390,14 +390,17 @@ constexpr int kQkStreamMinD = 1025;
 #ifndef GS_QK_U
 #define GS_QK_U 2  // pass-1 chunks per lane in flight
 #endif
+#ifndef GS_QK_SSQ_MINB
+#define GS_QK_SSQ_MINB 4  // resident CTAs per SM of the single-pass form (64 registers)
+#endif
 constexpr int kQkStreamWarps = 8;  // warps (rows) per CTA
-template <int U>
-__global__ void __launch_bounds__(32 * kQkStreamWarps, 3)
+template <int U, bool SSQ>
+__global__ void __launch_bounds__(32 * kQkStreamWarps, SSQ ? GS_QK_SSQ_MINB : 3)
     qk_norm_rope_stream_kernel(const __nv_bfloat16* __restrict__ qkv, int M, int D, int d,
                                const __nv_bfloat16* __restrict__ g_q, const __nv_bfloat16* __restrict__ g_k,
                                float eps, const RopeParams rp, const PackParams pk,
                                __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ k_out,
-                               __nv_bfloat16* __restrict__ v_out) {
+                               __nv_bfloat16* __restrict__ v_out, const float* __restrict__ ssq) {
   __shared__ QkTables tb;
   pdl_wait();
   pdl_launch_dependents();
@@ -420,8 +423,17 @@ __global__ void __launch_bounds__(32 * kQkStreamWarps, 3)
   for (long long row = static_cast<long long>(blockIdx.x) * kQkStreamWarps + warp; row < M;
        row += static_cast<long long>(gridDim.x) * kQkStreamWarps) {
     const uint4* src = reinterpret_cast<const uint4*>(qkv + row * 3LL * D);
-    // pass 1: sums of squares
     float sq = 0.f, sk = 0.f;
+    if constexpr (SSQ) {
+      // the QKV GEMM's per-32-column sums of squares (lane-strided, then the xor tree below): q and k are read once
+      const int nc = D >> 5;
+      const float* sr = ssq + row * 2LL * nc;
+      for (int c = lane; c < nc; c += 32) {
+        sq += sr[c];
+        sk += sr[nc + c];
+      }
+    } else {
+    // pass 1: sums of squares
     for (int c0 = lane; c0 < nv; c0 += 32 * U) {
       uint4 qv[U], kv[U];
 #pragma unroll
@@ -438,6 +450,7 @@ __global__ void __launch_bounds__(32 * kQkStreamWarps, 3)
           sq += sumsq8(qv[u]);
           sk += sumsq8(kv[u]);
         }
+    }
     }
     // per-row constants (overlap the reduction)
     const int r = rp.row_req[row];
@@ -762,20 +775,23 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
   return cudaGetLastError();
 }
 
+bool qk_uses_ssq(int D) { return D >= kQkStreamMinD; }
+
 cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,
                               const RopeParams& rp, const PackParams& pk, __nv_bfloat16* q_out,
-                              __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream) {
+                              __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream, const float* ssq) {
   if (M == 0) return cudaSuccess;
   const int d = D / heads;
+  if (ssq != nullptr && (!qk_uses_ssq(D) || D % 32)) return cudaErrorInvalidValue;
   if (D % heads || d % 8 || D > 8 * (MAXV / 2) * ROW_THREADS || pk.ndest < 1 || pk.ndest > kMaxChunks)
     return cudaErrorInvalidValue;
   if (!pk.peer && (!q_out || !k_out)) return cudaErrorInvalidValue;
   if (D >= kQkStreamMinD) {
-    auto kern = qk_norm_rope_stream_kernel<GS_QK_U>;
+    auto kern = ssq ? qk_norm_rope_stream_kernel<GS_QK_U, true> : qk_norm_rope_stream_kernel<GS_QK_U, false>;
     const dim3 block(32 * kQkStreamWarps);
     return launch_pdl(kern, resident_grid(kern, block, 0, (M + kQkStreamWarps - 1) / kQkStreamWarps), block, stream,
-                      qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out);
+                      qkv, M, D, d, g_q, g_k, eps, rp, pk, q_out, k_out, v_out, ssq);
   }
   const int tpr = row_tpr(D);
   const int vpl = (D / 8 + tpr - 1) / tpr;  // 1..8

@@ -94,6 +94,35 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(uint32_t tw, const uint32_t (&r)[32], int row0, int col0, int M,
                                                const EpiParams& ep) {
   const int lane = threadIdx.x & 31;
+  if (EPI == EPI_BF16 && ep.ssq != nullptr && col0 < ep.ssq_cols) {
+    // this thread holds row row0 + lane's 32 columns: sum of (acc + bias)^2 in column order (two chains)
+    float b[32];
+    if (ep.bias != nullptr) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 braw = __ldg(reinterpret_cast<const uint4*>(ep.bias + col0) + q);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&braw);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(b2[e]);
+          b[8 * q + 2 * e] = f.x;
+          b[8 * q + 2 * e + 1] = f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) b[i] = 0.f;
+    }
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+      const float u0 = __uint_as_float(r[i]) + b[i], u1 = __uint_as_float(r[i + 1]) + b[i + 1];
+      s0 = fmaf(u0, u0, s0);
+      s1 = fmaf(u1, u1, s1);
+    }
+    const int row = row0 + lane;
+    if (row < M) ep.ssq[static_cast<size_t>(row) * (ep.ssq_cols >> 5) + (col0 >> 5)] = s0 + s1;
+  }
 #pragma unroll
   for (int q = 0; q < 8; ++q)
     sts_v4(tw + (lane * EP_PITCH + 4 * q) * 4,

@@ -408,6 +408,7 @@ int prepare_rank(gs_ctx* c, const Plan& P, int i, RankArena& A) {
   RET(ensure(c, A.x, rows * D * 4));
   RET(ensure(c, A.a, rows * D * 2));
   RET(ensure(c, A.qkv, rows * 3 * D * 2));
+  if (qk_uses_ssq(D)) RET(ensure(c, A.ssq, rows * (2 * D / 32) * 4));  // QKV GEMM sums of squares of q | k
   RET(ensure(c, A.qs, rows * D * 2));
   RET(ensure(c, A.ks, rows * D * 2));
   RET(ensure(c, A.vs, rows * D * 2));
@@ -796,7 +797,13 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
     if (M) CK(ln_modulate(A.x.as<float>(), M, D, w.mod + 0 * D, A.e.as<float>() + 0 * D, w.mod + 1 * D,
                           A.e.as<float>() + 1 * D, 6 * D, A.row_req.as<int>(), eps, A.a.as<bf16>(), strm(c)));
   }
-  RET(gemm(c, "gemm_qkv", EPI_BF16, M, 3 * D, D, A.a.p, w.w_qkv, epi(A.qkv.p, 3 * D, w.b_qkv)));
+  EpiParams eq = epi(A.qkv.p, 3 * D, w.b_qkv);
+  const bool ssq = qk_uses_ssq(D);
+  if (ssq) {  // the qk-RMSNorm sums come out of the QKV GEMM epilogue
+    eq.ssq = A.ssq.as<float>();
+    eq.ssq_cols = 2 * D;
+  }
+  RET(gemm(c, "gemm_qkv", EPI_BF16, M, 3 * D, D, A.a.p, w.w_qkv, eq));
   {
     Scope sc(c, "qk_norm_rope", 1);
     RopeParams rp{A.row_req.as<int>(), A.row_tok.as<int>(), A.req_grid.as<int>(), P.m->cs_tab, P.m->slot_axis,
@@ -825,7 +832,8 @@ int block_pre(gs_ctx* c, const Plan& P, int i, RankArena& A, int l) {
     }
     // SP = 1: no exchange, so V is not copied -- the attention reads it in place from the QKV output
     if (M) CK(qk_norm_rope_pack(A.qkv.as<bf16>(), M, D, P.H, w.g_q, w.g_k, eps, rp, pk, A.qs.as<bf16>(),
-                                A.ks.as<bf16>(), P.p == 1 ? nullptr : A.vs.as<bf16>(), strm(c)));
+                                A.ks.as<bf16>(), P.p == 1 ? nullptr : A.vs.as<bf16>(), strm(c),
+                                ssq ? A.ssq.as<float>() : nullptr));
   }
   return GS_OK;
 }
@@ -1265,7 +1273,7 @@ void gs_destroy(gs_ctx* c) {
   for (auto& A : c->local) {
     DevBuf* bufs[] = {&A.x, &A.a, &A.qkv, &A.qs, &A.ks, &A.vs, &A.qr, &A.kr, &A.vr, &A.o, &A.orecv,
                       &A.ostage, &A.h, &A.zpack, &A.zb, &A.e0, &A.e, &A.temb, &A.row_req, &A.row_tok,
-                      &A.req_grid, &A.qc, &A.vbuf};
+                      &A.req_grid, &A.qc, &A.vbuf, &A.ssq};
     for (DevBuf* b : bufs)
       if (b->p) cudaFree(b->p);
   }

@@ -31,6 +31,11 @@ struct EpiParams {
   const int* row_req;         // [M] request index of each row
   float dsig[8];              // per-request sigma_{i+1} - sigma_i
   int group_m;                // tile rasterisation band (M-tiles); set by the launcher
+  // EPI_BF16 only, optional: for output columns < ssq_cols, ssq[row * (ssq_cols / 32) + col / 32]
+  // = the sum over that 32-column chunk of (acc + bias)^2 in fp32 (fixed order; chunks are 32-column aligned for
+  // every tile width), so the qk-RMSNorm needs no pass of its own over q and k
+  float* ssq;
+  int ssq_cols;
 };
 
 // Programmatic dependent launch for the step's GEMM / attention / row kernels (elementwise.cu):
@@ -103,10 +108,15 @@ struct PackParams {
   __nv_bfloat16* dst_v[16];
   long long row_delta[16];
 };
+// ssq (optional, D > 1024): the QKV GEMM's per-32-column sums of squares of q | k ([M][2D / 32] fp32); the row
+// sums are then formed from it and q, k are read once.
 cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,
                               const RopeParams& rp, const PackParams& pk, __nv_bfloat16* q_out,
-                              __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream);
+                              __nv_bfloat16* k_out, __nv_bfloat16* v_out, cudaStream_t stream,
+                              const float* ssq = nullptr);
+// Whether qk_norm_rope_pack uses the GEMM's sums of squares at this D (the QKV GEMM must then produce them).
+bool qk_uses_ssq(int D);
 
 // Time embedding for B requests: e0 = W_t2 SiLU(W_t1 s(t) + b) + b, e = W_tp SiLU(e0) + b.
 struct TimeEmbedW {

@@ -114,7 +114,7 @@ struct Request {
 struct RankArena {
   int rank = 0;
   DevBuf x, a, qkv, qs, ks, vs, qr, kr, vr, o, orecv, ostage, h, zpack, zb, e0, e, temb, row_req,
-      row_tok, req_grid, qc, vbuf;
+      row_tok, req_grid, qc, vbuf, ssq;
 };
 
 struct Prof {
