@@ -775,7 +775,9 @@ cudaError_t ln_modulate(const float* x, int M, int D, const float* sh_a, const f
   return cudaGetLastError();
 }
 
-bool qk_uses_ssq(int D) { return D >= kQkStreamMinD; }
+// Only above D = 2048: at config 2 (D = 1536, K = 1536) the extra epilogue work costs the QKV GEMM ~6 us per launch
+// (164 -> 170 us), more than the 3.5 us the single-pass qk kernel saves (profiles/r02c/ssq/).
+bool qk_uses_ssq(int D) { return D > kWarpRowMaxD; }
 
 cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,

@@ -108,7 +108,7 @@ struct PackParams {
   __nv_bfloat16* dst_v[16];
   long long row_delta[16];
 };
-// ssq (optional, D > 1024): the QKV GEMM's per-32-column sums of squares of q | k ([M][2D / 32] fp32); the row
+// ssq (optional, D > 2048, qk_uses_ssq): the QKV GEMM's per-32-column sums of squares of q | k ([M][2D / 32] fp32); the row
 // sums are then formed from it and q, k are read once.
 cudaError_t qk_norm_rope_pack(const __nv_bfloat16* qkv, int M, int D, int heads,
                               const __nv_bfloat16* g_q, const __nv_bfloat16* g_k, float eps,
