@@ -311,6 +311,12 @@ int gs_plan_reshard(int n_tokens, int lat, const int* old_ranks, int old_p, cons
 int gs_debug_gemm(gs_ctx* ctx, int epi, int M, int N, int K, const void* A, const void* W,
                   const void* bias, void* out, const float* gate_a, const float* gate_b,
                   int gate_b_stride, const int* row_req, const float* dsig_host);
+/* The QKV GEMM's bf16 epilogue with the qk-RMSNorm sums of squares: out [M,N] bf16 =
+ * A W^T + bias, and for the output columns c < ssq_cols (a multiple of 32), ssq[row * (ssq_cols / 32) + c / 32]
+ * = the fp32 sum over that 32-column chunk of (acc + bias)^2.  Device pointers; ssq holds M * ssq_cols / 32
+ * floats.  GS_EINVAL for ssq_cols % 32 != 0 or ssq_cols > N. */
+int gs_debug_gemm_ssq(gs_ctx* ctx, int M, int N, int K, const void* A, const void* W, const void* bias, void* out,
+                      float* ssq, int ssq_cols);
 /* Attention over packed requests: Q/K/V/O bf16 [rows, heads, d] with row strides (elements);
  * seq_off/seq_len host int arrays of nreq entries (rows of each request). d in {64, 128}. */
 int gs_debug_attention(gs_ctx* ctx, const void* q, const void* k, const void* v, void* o, int heads,

@@ -81,6 +81,7 @@ _SIG = {
     "gs_stats": [_P, ctypes.c_char_p, ctypes.c_size_t],
     "gs_stream": [_P, _I, ctypes.POINTER(_P)],
     "gs_debug_gemm": [_P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _I, _P, _FP],
+    "gs_debug_gemm_ssq": [_P, _I, _I, _I, _P, _P, _P, _P, _P, _I],
     "gs_debug_attention": [_P, _P, _P, _P, _P, _I, _I, _I, _I, _I, _IP, _IP, _I],
     "gs_debug_block": [_P, _I, _I, _FP, _I, _IP, _IP, _IP, _FP, _P],
     "gs_debug_time_embed": [_P, _I, _I, _FP, _FP, _FP],
@@ -449,6 +450,10 @@ class Context:
         self._ck(self._lib.gs_debug_gemm(self._h, epi, M, N, K, _ptr(A), _ptr(W), _ptr(bias),
                                          _ptr(out), _ptr(gate_a), _ptr(gate_b), gate_b_stride,
                                          _ptr(row_req), ds))
+
+    def debug_gemm_ssq(self, M, N, K, A, W, bias, out, ssq, ssq_cols):
+        self._ck(self._lib.gs_debug_gemm_ssq(self._h, M, N, K, _ptr(A), _ptr(W), _ptr(bias), _ptr(out),
+                                             _ptr(ssq), ssq_cols))
 
     def debug_attention(self, q, k, v, o, heads, d, seq_off, seq_len, q_rs=None, kv_rs=None,
                         o_rs=None):

@@ -2021,6 +2021,25 @@ int gs_debug_gemm(gs_ctx* c, int e, int M, int N, int K, const void* A, const vo
   return GS_OK;
 }
 
+int gs_debug_gemm_ssq(gs_ctx* c, int M, int N, int K, const void* A, const void* W, const void* bias, void* out,
+                      float* ssq, int ssq_cols) {
+  if (!c || !ssq || ssq_cols <= 0 || ssq_cols % 32 || ssq_cols > N) return GS_EINVAL;
+  std::lock_guard<std::mutex> g(c->api_mu);
+  RET(no_runs_in_flight(c, "gs_debug_gemm_ssq"));
+  CK(cudaSetDevice(c->device));
+  RET(order_after_legacy(c));
+  EpiParams ep{};
+  ep.out = out;
+  ep.ldo = N;
+  ep.bias = static_cast<const bf16*>(bias);
+  ep.ssq = ssq;
+  ep.ssq_cols = ssq_cols;
+  cudaError_t err = gemm_bf16_tc(EPI_BF16, M, N, K, A, K, W, K, ep, c->num_sms, strm(c));
+  if (err != cudaSuccess) return fail(c, err == cudaErrorInvalidValue ? GS_EINVAL : GS_ECUDA, "gemm: %s", cudaGetErrorString(err));
+  CK(cudaStreamSynchronize(strm(c)));
+  return GS_OK;
+}
+
 int gs_debug_attention(gs_ctx* c, const void* q, const void* k, const void* v, void* o, int heads, int d, int q_rs,
                        int kv_rs, int o_rs, const int* seq_off, const int* seq_len, int nreq) {
   if (!c || !seq_off || !seq_len) return GS_EINVAL;

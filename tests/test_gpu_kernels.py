@@ -241,3 +241,46 @@ def test_gemm_pair_tile_width_does_not_change_bits(ctx, torch, epi):
         outs.append(out.view(torch.int16 if out.dtype == torch.bfloat16 else torch.int32).cpu())
     ctx.set_option("gemm_bn", 0)
     assert torch.equal(outs[0], outs[1])
+
+
+# ----------------------------------------------------------------------------- QKV epilogue sums of squares
+@pytest.mark.parametrize("M,N,K,cols", [(300, 768, 256, 512), (1000, 15360 // 4, 1280, 2560)])
+def test_gemm_ssq_partials(ctx, torch, M, N, K, cols):
+    """per row and 32-column chunk the QKV GEMM epilogue writes sum (acc + bias)^2 in fp32 for
+    the q | k columns.  Against the fp64 oracle linear on the same bf16 inputs (fp32 accumulation: ~1e-6 relative);
+    chunks at or beyond ssq_cols are not written; the bf16 output equals the plain EPI_BF16 GEMM bit for bit."""
+    import paper_2604_04335_b200 as gs
+    a, w, b, ref = _gemm_inputs(M, N, K, seed=11)
+    out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    nc = cols // 32
+    ssq = torch.full((M * nc + 64,), -7.0, dtype=torch.float32, device="cuda")  # sentinel tail
+    ctx.debug_gemm_ssq(M, N, K, to_dev_bf16(a), to_dev_bf16(w), to_dev_bf16(b), out, ssq, cols)
+    got = ssq.cpu().numpy()
+    want = (ref[:, :cols] ** 2).reshape(M, nc, 32).sum(axis=2).reshape(-1)
+    assert np.max(np.abs(got[:M * nc] - want) / want) < 1e-4
+    assert np.all(got[M * nc:] == -7.0)
+    plain = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+    ctx.debug_gemm(gs.EPI_BF16, M, N, K, to_dev_bf16(a), to_dev_bf16(w), to_dev_bf16(b), plain)
+    assert torch.equal(out.view(torch.int16), plain.view(torch.int16))
+
+
+def test_gemm_ssq_bits_independent_of_M_and_tile_width(ctx, torch):
+    """The partials of a row depend on that row alone: the same rows give the same bits inside a larger M and with
+    the 192- or 256-wide pair tiles (chunks are 32-column aligned for both), so SP degree and batch composition
+    cannot change the qk-RMSNorm through them."""
+    g = torch.Generator(device="cuda").manual_seed(21)
+    N, K, cols = 1536, 1536, 1024
+    A = torch.randn(1000, K, device="cuda", generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.03).to(torch.bfloat16)
+    b = (torch.randn(N, device="cuda", generator=g) * 0.1).to(torch.bfloat16)
+    res = []
+    for M, bn in ((1000, 256), (1000, 192), (333, 0)):
+        ctx.set_option("gemm_bn", bn)
+        out = torch.empty((M, N), dtype=torch.bfloat16, device="cuda")
+        ssq = torch.empty((M * cols // 32,), dtype=torch.float32, device="cuda")
+        ctx.debug_gemm_ssq(M, N, K, A[:M].contiguous(), W, b, out, ssq, cols)
+        res.append(ssq.view(torch.int32).cpu().reshape(M, -1))
+    ctx.set_option("gemm_bn", 0)
+    assert torch.equal(res[0], res[1])
+    assert torch.equal(res[0][:333], res[2])
+
