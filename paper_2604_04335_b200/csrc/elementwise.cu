@@ -386,6 +386,8 @@ __global__ void __launch_bounds__(TPR < 128 ? TPR * kWarpRowsPerCta : TPR, MINB)
 // the warp read it a moment ago) and writes the normalised, rotated q and k (and v, unless it stays in place).
 // Few registers per row, so many rows are in flight per SM: the row-per-CTA form above is bound by its per-row
 // latency chain (load -> block reduction -> compute -> store) at ~3 rows per SM.
+// SSQ (D > 2048, qk_uses_ssq): the sums come from the QKV GEMM epilogue's per-32-column partials instead of pass 1,
+// so q and k are read once.
 constexpr int kQkStreamMinD = 1025;
 #ifndef GS_QK_U
 #define GS_QK_U 2  // pass-1 chunks per lane in flight
